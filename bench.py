@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the spring-mass step (BASELINE.json metric).
+
+Default workload = config B of BASELINE.json / SURVEY.md 8(d): a 100^3
+lattice (1,000,000 masses, 12,731,796 springs), spacing 0.05, E=1e5,
+rho=1000, positions stretched x1.01 (the reference bench recipe,
+cli.py:263-271), gravity -9.81 and a friction ground plane (k=2000,
+mu_s=1, mu_k=0.8) with the bottom layer on it; fp32, deterministic gather.
+
+One "step" = one fused spring+mass step of the whole lattice.  ``value`` =
+alive springs x steps / device time (CUDA events on the library's stream,
+max over ranks); ``e2e`` = the same metric through the public API
+(SimController.start(duration) -> wait_for_event -> snapshot) with the host
+store authoritative before and after, host<->device copies inside the timed
+region.  Multi-GPU (torchrun): one independent lattice per rank (batched
+instances, no collective on the step path; scaling "weak").
+
+``--impl reference`` times the reference algorithm on the host CPU (the C
+restatement in oracle/, OpenMP, all cores, fp64 slotted accumulation -- the
+reference's fastest CPU variant) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_RATE = 3.0e8  # PAPER.md:10,20 headline (Titan X); north_star x50 base
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=100, help="lattice edge")
+    ap.add_argument("--precision", default="fp32",
+                    choices=["fp32", "mixed", "fp64"])
+    ap.add_argument("--accumulation", default="gather",
+                    choices=["gather", "atomic"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- workload
+def build_workload(n: int):
+    from paper_1911_10274_b200 import (ContactPlane, Environment, Material,
+                                       ObjectStore, Vec3)
+    from paper_1911_10274_b200.builder import LatticeSpec, build_lattice
+    st = ObjectStore()
+    body = build_lattice(LatticeSpec(Vec3(0, 0, 0), n, n, n, 0.05,
+                                     Material(1e5, 1000.0)), st)
+    st._m_pos[body.mass_handles.slots] *= 1.01
+    env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
+        normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
+        static_friction=1.0, kinetic_friction=0.8)])
+    return st, env
+
+
+def algorithmic_bytes(springs: int, masses: int, precision: str) -> int:
+    """B = S*Bs + M*Bm.  Bs = int32 i,j + k, L0 words;
+    Bm = pos r+w, vel r+w, m r (words of the state precision)."""
+    w_s = 8 if precision == "fp64" else 4
+    w_m = 4 if precision == "fp32" else 8
+    return springs * (8 + 2 * w_s) + masses * 13 * w_m
+
+
+def store_case(st, env):
+    from paper_1911_10274_b200 import engine
+    m, s = st.mass_slot_count, st.spring_slot_count
+    case = {k: getattr(st, "_" + k)[:m] for k in
+            ("m_pos", "m_vel", "m_acc", "m_fext", "m_load", "m_mass",
+             "m_fixed", "m_alive", "m_gen")}
+    for k in ("s_m1", "s_m2", "s_m1gen", "s_m2gen", "s_rest", "s_k",
+              "s_diam", "s_yield", "s_amp", "s_freq", "s_off", "s_per",
+              "s_alive", "s_degen"):
+        case[k] = getattr(st, "_" + k)[:s]
+    case["s_mode"] = st._s_act_mode[:s]
+    planes, balls = engine.flatten_contacts(env)
+    case.update(gravity=env.gravity.as_array(), drag=env.drag_coeff,
+                planes=planes, balls=balls)
+    return case
+
+
+# ------------------------------------------------------------ cpu timing
+def time_oracle(st, env, steps: int, warmup: int, threads: int,
+                budget_s: float = 120.0):
+    """Reference algorithm (oracle/ C restatement, fp64, slotted parallel =
+    the reference's parallel+slotted backend) on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    sim = oracle.OracleSim(store_case(st, env), nthreads=threads)
+    dt = 1e-4
+    t = 0.0
+    for _ in range(warmup):
+        sim.step(t, dt, "slotted")
+        t += dt
+    done = 0
+    w0 = time.perf_counter()
+    while done < steps:
+        sim.step(t, dt, "slotted")
+        t += dt
+        done += 1
+        if time.perf_counter() - w0 > budget_s:
+            break
+    return done, time.perf_counter() - w0
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) < 8:
+                    continue
+                try:
+                    sm.append(float(p[0]))
+                    mx.append(float(p[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, p[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def committed_traffic(workload_key: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(workload_key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    workload = (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
+                f"x1.01 stretch, {args.precision}, {args.accumulation}")
+    metric = "spring updates/sec"
+    unit = "spring_updates/s"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        st, env = build_workload(args.n)
+        threads = os.cpu_count() or 1
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        oracle.build()
+        threads = oracle.max_threads()
+        steps, wall = time_oracle(st, env, max(1, args.steps),
+                                  max(1, min(args.warmup, 2)), threads)
+        v = st.spring_count * steps / wall
+        line = {"impl": "reference", "metric": metric, "value": v,
+                "unit": unit, "n_gpus": args.gpus, "steps": steps,
+                "warmup": min(args.warmup, 2), "ms_per_step": 1e3 * wall /
+                steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": v / PAPER_RATE, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": workload.replace(args.precision,
+                                                        "fp64 (reference)"),
+                           "masses": st.mass_count,
+                           "springs": st.spring_count},
+                "cpu_baseline": {"value": v, "unit": unit, "cores": threads,
+                                 "kind": "port",
+                                 "sample": f"{steps} full steps of the "
+                                           f"{args.n}^3 lattice, oracle/ C "
+                                           f"restatement of kernels.py, "
+                                           f"slotted, {threads} threads"},
+                "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    from paper_1911_10274_b200 import StepConfig, engine
+    from paper_1911_10274_b200.control import SimController
+
+    st, env = build_workload(args.n)
+    cfg = StepConfig(dt=1e-4, precision=args.precision, device=local,
+                     accumulation=args.accumulation)
+    springs, masses = st.spring_count, st.mass_count
+    mir = engine.mirror_for(st, cfg)
+    mir.push(st, env)
+    acc = cfg.native_accumulation
+    counters = np.zeros(3, np.int64)
+    dt = cfg.dt
+    step = 0
+
+    def times(n):
+        nonlocal step
+        t = (step + np.arange(n, dtype=np.float64)) * dt
+        step += n
+        return t
+
+    mir.ctx.step(times(max(3, args.warmup)), dt, acc, counters)  # warm-up
+    launches0 = mir.ctx.stats()["kernel_launches"]
+    if dist is not None:
+        dist.barrier()
+    mir.ctx.sync()
+    clocks = ClockSampler(local)
+    mir.ctx.timer_start()
+    done, err = mir.ctx.step(times(args.steps), dt, acc, counters)
+    ms = mir.ctx.timer_stop()
+    clk = clocks.stop()
+    launches = mir.ctx.stats()["kernel_launches"] - launches0
+    if err:
+        raise SystemExit(f"numerical abort at step {done}")
+    sec = ms / 1e3
+    if dist is not None:
+        import torch
+        t = torch.tensor([sec], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+        dist.barrier()
+    value = world * springs * args.steps / sec
+    ms_per_step = 1e3 * sec / args.steps
+
+    # roofline of the dominant kernel (the fused gather step: one launch per
+    # step, so its average duration is the per-step device time)
+    algo = algorithmic_bytes(springs, masses, args.precision)
+    peak, peak_kind = peak_hbm()
+    achieved = algo / (sec / args.steps) / 1e9
+    key = f"{args.n}^3/{args.precision}/{args.accumulation}"
+    traffic = committed_traffic(key)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_kind": peak_kind, "algorithmic_bytes_per_step": algo,
+            "bytes_per_spring_update": algo / springs,
+            "kernel": "k_gather_step" if args.accumulation == "gather"
+            else "k_spring_atomic+k_mass"}
+
+    # e2e through the public API, host store authoritative at both ends
+    e2e = None
+    if not args.no_e2e:
+        ctl = SimController(st, env, cfg)
+        k = args.steps
+        m = st.mass_slot_count
+        if dist is not None:
+            dist.barrier()
+        w0 = time.perf_counter()
+        ctl.start(k * dt)
+        rep = ctl.wait_for_event()
+        snap = ctl.snapshot()
+        wall = time.perf_counter() - w0
+        ctl.stop()
+        assert rep.step_count == k, rep
+        if dist is not None:
+            import torch
+            t = torch.tensor([wall], device=f"cuda:{local}",
+                             dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        h2d = m * (5 * 24 + 8 + 1 + 1 + 8) + 16 * (m + 1)
+        d2h = m * 4 * 24
+        e2e = {"value": world * springs * k / wall, "unit": unit,
+               "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
+               "wall_s": wall, "api": "SimController.start/wait_for_event/"
+                                      "snapshot", "snapshot_rows":
+                   int(len(snap.ids))}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle
+            oracle.build()
+            thr = oracle.max_threads()
+            st2, env2 = build_workload(args.n)
+            n_s, wall = time_oracle(st2, env2, 3, 1, thr, budget_s=30.0)
+            cpu = {"value": st2.spring_count * n_s / wall, "unit": unit,
+                   "cores": thr, "kind": "port",
+                   "sample": f"{n_s} steps of the same {args.n}^3 lattice "
+                             f"(fp64, slotted, oracle/ C restatement of "
+                             f"kernels.py, OpenMP {thr} threads)"}
+        except Exception as exc:  # baseline is reported, never fatal
+            cpu = {"error": str(exc)}
+
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": unit,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": value / PAPER_RATE,
+                "dtype": "f32" if args.precision == "fp32" else "f64",
+                "data": "synthetic",
+                "config": {"workload": workload, "masses": masses,
+                           "springs": springs, "per_gpu_instances": 1,
+                           "precision": args.precision,
+                           "accumulation": args.accumulation,
+                           "l2": "working set > 126 MB L2 every step "
+                                 "(no flush needed)",
+                           "parallelism": f"batched instances x{world}"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches), "clocks": clk,
+                "vs_baseline_ref": "PAPER.md:10 3.0e8 spring updates/s"}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

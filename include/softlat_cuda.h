@@ -1,0 +1,191 @@
+/*
+ * softlat_cuda.h -- C ABI of the B200 spring-mass step library
+ * (paper_1911_10274_b200/libsoftlat_cuda.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (Python + numba, /root/reference/pkg/src/softlat) dispatches a step through
+ * engine.spring_pass / engine.mass_pass / engine.step (engine.py:158-264) into
+ * numba kernels that take flat store arrays, mutate them in place and report
+ * through out-parameters (kernels.py:28-32, 250-253; counters[3] at
+ * kernels.py:84-86; err_slot at kernels.py:374-376).  Each entry point below
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *   - plain pointers + sizes, no torch / CUDA types; host arrays are in the
+ *     reference store layout: vectors double[n][3] C-contiguous, indices
+ *     int64, flags one byte (numpy bool), generations int64
+ *     (store.py:123-151).
+ *   - every call returns an int status (SL_OK = 0).  No exception crosses the
+ *     ABI.  sl_last_error(ctx) holds a message for the last failure.
+ *   - one context = one device + one CUDA stream; a context is not
+ *     thread-safe (the reference's controller already serialises every call
+ *     under its condition lock, control.py:628-643).  Distinct contexts may
+ *     be driven from distinct threads.
+ *   - the host store is authoritative while paused, the device while a run
+ *     is in progress (store.lock_for_run, store.py:206-224).
+ */
+#ifndef SOFTLAT_CUDA_H
+#define SOFTLAT_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (engine.py:251-255 NumericalAbort maps to SL_ENUMERIC) */
+#define SL_OK 0
+#define SL_EINVAL 1       /* bad argument (InvalidValueError)            */
+#define SL_ECUDA 2        /* CUDA runtime failure                         */
+#define SL_ENUMERIC 3     /* non-finite state; err_slot = slot + 1        */
+#define SL_ESTATE 4       /* call illegal in the context's current state  */
+#define SL_EUNSUPPORTED 5 /* feature not available on this build/device   */
+
+/* arithmetic of the state and of the spring force (hard part 3) */
+#define SL_PREC_FP64 0  /* double everywhere; parity mode (bit-exact gather) */
+#define SL_PREC_FP32 1  /* float state + float spring math                  */
+#define SL_PREC_MIXED 2 /* double mass state, float spring parameters/math  */
+
+/* force accumulation (StepConfig.accumulation, engine.py:40,49):
+ *   GATHER = deterministic per-mass CSR gather in ascending spring-slot order
+ *            (== reference "slotted" == serial, engine.py:105-118)
+ *   ATOMIC = one thread per spring, vector atomics into f_ext
+ *            (reference "linearizable": order-dependent rounding)         */
+#define SL_ACC_GATHER 0
+#define SL_ACC_ATOMIC 1
+
+typedef struct sl_ctx sl_ctx;
+
+typedef struct sl_stats {
+  int64_t masses;          /* mass slots resident (high-water m_n)          */
+  int64_t springs;         /* spring slots resident (high-water s_n)        */
+  int64_t alive_springs;   /* springs alive at the last layout build        */
+  int64_t entries;         /* incidence entries incl. padding               */
+  int64_t slices;          /* 32-mass slices of the incidence layout        */
+  int64_t layout_builds;   /* number of device layout (re)builds            */
+  int64_t device_bytes;    /* device memory owned by the context            */
+  int64_t kernel_launches; /* kernels launched by the context so far        */
+  int32_t precision;
+  int32_t device;
+} sl_stats;
+
+/* ---------------------------------------------------------------- lifecycle */
+int sl_abi_version(void);
+int sl_device_count(int *count);
+/* one context per store per device (engine._StoreCache, engine.py:71-102) */
+int sl_create(int device, int precision, sl_ctx **out);
+int sl_destroy(sl_ctx *ctx);
+const char *sl_last_error(const sl_ctx *ctx); /* ctx may be NULL */
+int sl_get_stats(sl_ctx *ctx, sl_stats *out);
+
+/* ------------------------------------------------------------------ upload */
+/* Whole mass SoA, slots [0, m_n) (store.py:123-132; mass-pass arguments of
+ * kernels.py:250-253).  Vectors are double[m_n][3]; any of acc/fext/load may
+ * be NULL (= zero). */
+int sl_upload_masses(sl_ctx *ctx, int64_t m_n, const double *pos,
+                     const double *vel, const double *acc, const double *fext,
+                     const double *load, const double *mass,
+                     const uint8_t *fixed, const uint8_t *alive,
+                     const int64_t *gen);
+
+/* Whole spring SoA, slots [0, s_n) (store.py:134-151; spring-pass
+ * arguments of kernels.py:28-32).  mode: 0 none, 1 sine, 2 sine quiescent
+ * before offset, 3 custom (store.py:36-40).  Triggers a device rebuild of the
+ * incidence layout. */
+int sl_upload_springs(sl_ctx *ctx, int64_t s_n, const int64_t *m1,
+                      const int64_t *m2, const int64_t *m1gen,
+                      const int64_t *m2gen, const double *rest,
+                      const double *k, const double *diam,
+                      const double *yield, const int8_t *mode,
+                      const double *amp, const double *freq,
+                      const double *off, const double *per,
+                      const uint8_t *alive, const uint8_t *degen);
+
+/* Environment flattened as engine.mass_pass does every call
+ * (engine.py:223-245): gravity[3], drag, planes[n][7] =
+ * (nx,ny,nz,offset,k,mu_s,mu_k), balls[n][5] = (cx,cy,cz,r,k), global
+ * constraints kind (1 direction, 2 plane; kernels.py:24-25) + unit vector,
+ * v_stick (engine.py:38). */
+int sl_set_environment(sl_ctx *ctx, const double *gravity, double drag,
+                       const double *planes, int64_t n_planes,
+                       const double *balls, int64_t n_balls,
+                       const int8_t *gc_kind, const double *gc_vec,
+                       int64_t n_gc, double v_stick);
+
+/* Per-mass local constraints as the CSR of engine._refresh_constraints
+ * (engine.py:121-146): lc_off[m_n+1], lc_kind[n_lc], lc_vec[n_lc][3]. */
+int sl_set_local_constraints(sl_ctx *ctx, int64_t m_n, const int64_t *lc_off,
+                             const int8_t *lc_kind, const double *lc_vec,
+                             int64_t n_lc);
+
+/* Host-evaluated factors of callable waveforms (mode 3), the device copy of
+ * engine._fill_custom_factors (engine.py:149-155). */
+int sl_set_custom_factors(sl_ctx *ctx, int64_t n, const int64_t *slots,
+                          const double *factors);
+
+/* ------------------------------------------------------------ O(1) edits */
+/* Overwrite individual mass slots (store setters at a pause point,
+ * store.py:536-601, control.py:480-515).  Slots must be < current m_n. */
+int sl_write_masses(sl_ctx *ctx, int64_t n, const int64_t *slots,
+                    const double *pos, const double *vel, const double *acc,
+                    const double *fext, const double *load,
+                    const double *mass, const uint8_t *fixed,
+                    const uint8_t *alive, const int64_t *gen);
+/* Overwrite parameters of existing spring slots in place (set_spring_field,
+ * store.py:563-588): rest, k, diam, yield and actuation, same arrays as
+ * sl_upload_springs minus topology.  O(n), no layout rebuild. */
+int sl_write_spring_params(sl_ctx *ctx, int64_t n, const int64_t *slots,
+                           const double *rest, const double *k,
+                           const double *diam, const double *yield,
+                           const int8_t *mode, const double *amp,
+                           const double *freq, const double *off,
+                           const double *per);
+/* Kill spring slots (delete_spring / reconcile, store.py:440-473). O(n). */
+int sl_kill_springs(sl_ctx *ctx, int64_t n, const int64_t *slots);
+
+/* -------------------------------------------------------------------- step */
+/* n_steps of engine.step (engine.py:258-264): spring pass + mass pass per
+ * step, sim time of step i = sim_times[i] (engine.step's sim_t argument;
+ * the controller passes t0 + step_count*dt, control.py:306-307).
+ * Stops after the first step that produces non-finite state (that step's
+ * writes are kept, as the reference's mass pass writes before raising):
+ * returns SL_ENUMERIC, *err_slot = offending slot + 1 (highest, the serial
+ * loop's last write, kernels.py:374-376), *steps_done includes that step.
+ * counters[3] (+=) = (broken, invalid, degenerate_new), kernels.py:84-86.
+ * write_acc: also store per-mass acceleration of the final step. */
+int sl_step(sl_ctx *ctx, int64_t n_steps, const double *sim_times, double dt,
+            int accumulation, int64_t *counters, int64_t *err_slot,
+            int64_t *steps_done);
+
+/* Single spring pass only (engine.spring_pass, engine.py:158-202): spring
+ * forces are added into the device f_ext accumulator. */
+int sl_spring_pass(sl_ctx *ctx, double sim_t, int accumulation,
+                   int64_t *counters);
+/* Single mass pass only (engine.mass_pass, engine.py:218-255). */
+int sl_mass_pass(sl_ctx *ctx, double dt, int64_t *err_slot);
+
+/* ---------------------------------------------------------------- download */
+/* Copy mass state back into host arrays double[m_n][3]; NULL skips. */
+int sl_download_masses(sl_ctx *ctx, double *pos, double *vel, double *acc,
+                       double *fext);
+/* Spring liveness / zero-length flags back into bool[s_n]; NULL skips. */
+int sl_download_springs(sl_ctx *ctx, uint8_t *alive, uint8_t *degen);
+
+/* Asynchronous snapshot (north_star "pinned-memory async snapshots"):
+ * enqueue a D2H copy of positions + velocities into library-owned pinned
+ * buffers on a side stream, ordered after all work issued so far; returns
+ * immediately.  sl_snapshot_wait blocks until it lands and copies it out. */
+int sl_snapshot_begin(sl_ctx *ctx);
+int sl_snapshot_ready(sl_ctx *ctx, int *ready);
+int sl_snapshot_wait(sl_ctx *ctx, double *pos, double *vel);
+
+/* ---------------------------------------------------------- timing / sync */
+/* CUDA events on the context's stream (bench.py measures with these). */
+int sl_timer_start(sl_ctx *ctx);
+int sl_timer_stop(sl_ctx *ctx, float *ms);
+int sl_sync(sl_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOFTLAT_CUDA_H */

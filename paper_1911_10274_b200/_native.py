@@ -1,0 +1,315 @@
+"""ctypes binding of libsoftlat_cuda.so (include/softlat_cuda.h).
+
+This is the only path to the compute: there is no CPU fallback.  Loading
+fails loudly if the shared library was not built (run
+``python -c "import __graft_entry__ as g; g.build()"`` or
+``python paper_1911_10274_b200/_build.py``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import (DeviceError, InvalidValueError, NumericalAbort,
+                     SoftlatError)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsoftlat_cuda.so")
+
+SL_OK, SL_EINVAL, SL_ECUDA, SL_ENUMERIC, SL_ESTATE, SL_EUNSUPPORTED = range(6)
+PRECISIONS = {"fp64": 0, "fp32": 1, "mixed": 2}
+ACC_GATHER, ACC_ATOMIC = 0, 1
+
+# every symbol the header declares (tests check the .so exports them all)
+EXPORTS = (
+    "sl_abi_version", "sl_device_count", "sl_create", "sl_destroy",
+    "sl_last_error", "sl_get_stats", "sl_upload_masses", "sl_upload_springs",
+    "sl_set_environment", "sl_set_local_constraints", "sl_set_custom_factors",
+    "sl_write_masses", "sl_write_spring_params", "sl_kill_springs", "sl_step",
+    "sl_spring_pass", "sl_mass_pass", "sl_download_masses",
+    "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
+    "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync")
+
+
+class SlStats(C.Structure):
+    _fields_ = [("masses", C.c_int64), ("springs", C.c_int64),
+                ("alive_springs", C.c_int64), ("entries", C.c_int64),
+                ("slices", C.c_int64), ("layout_builds", C.c_int64),
+                ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
+                ("precision", C.c_int32), ("device", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load (once) and declare signatures.  Raises if the .so is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise SoftlatError(
+                f"CUDA library not built: {path} is missing; build it with "
+                "paper_1911_10274_b200/_build.py (no CPU fallback exists)")
+        lib = C.CDLL(path)
+        P, I64, D, I = C.c_void_p, C.c_int64, C.c_double, C.c_int
+        sig = {
+            "sl_abi_version": ([], I),
+            "sl_device_count": ([P], I),
+            "sl_create": ([I, I, P], I),
+            "sl_destroy": ([P], I),
+            "sl_last_error": ([P], C.c_char_p),
+            "sl_get_stats": ([P, P], I),
+            "sl_upload_masses": ([P, I64] + [P] * 9, I),
+            "sl_upload_springs": ([P, I64] + [P] * 15, I),
+            "sl_set_environment": ([P, P, D, P, I64, P, I64, P, P, I64, D], I),
+            "sl_set_local_constraints": ([P, I64, P, P, P, I64], I),
+            "sl_set_custom_factors": ([P, I64, P, P], I),
+            "sl_write_masses": ([P, I64] + [P] * 10, I),
+            "sl_write_spring_params": ([P, I64] + [P] * 10, I),
+            "sl_kill_springs": ([P, I64, P], I),
+            "sl_step": ([P, I64, P, D, I, P, P, P], I),
+            "sl_spring_pass": ([P, D, I, P], I),
+            "sl_mass_pass": ([P, D, P], I),
+            "sl_download_masses": ([P, P, P, P, P], I),
+            "sl_download_springs": ([P, P, P], I),
+            "sl_snapshot_begin": ([P], I),
+            "sl_snapshot_ready": ([P, P], I),
+            "sl_snapshot_wait": ([P, P, P], I),
+            "sl_timer_start": ([P], I),
+            "sl_timer_stop": ([P, P], I),
+            "sl_sync": ([P], I),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _c(a, dtype, shape_tail=()):
+    """Contiguous view/copy with the dtype the ABI expects."""
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr
+
+
+def device_count() -> int:
+    lib = load_library()
+    n = C.c_int(0)
+    rc = lib.sl_device_count(C.byref(n))
+    return int(n.value) if rc == SL_OK else 0
+
+
+class Context:
+    """One device context: SoA buffers of one store on one GPU + a stream."""
+
+    def __init__(self, device: int = 0, precision: str = "fp64"):
+        if precision not in PRECISIONS:
+            raise InvalidValueError(
+                f"precision must be one of {tuple(PRECISIONS)}")
+        self.lib = load_library()
+        self.device = int(device)
+        self.precision = precision
+        h = C.c_void_p()
+        rc = self.lib.sl_create(self.device, PRECISIONS[precision],
+                                C.byref(h))
+        if rc != SL_OK:
+            raise DeviceError(
+                f"sl_create failed ({rc}): "
+                f"{self.lib.sl_last_error(None).decode()}")
+        self.h = h
+        self.m_n = 0
+        self.s_n = 0
+
+    # ------------------------------------------------------------ errors
+    def _check(self, rc: int, what: str, mass_slot: int | None = None):
+        if rc == SL_OK:
+            return
+        msg = self.lib.sl_last_error(self.h).decode()
+        if rc == SL_ENUMERIC:
+            raise NumericalAbort(
+                f"non-finite state on mass slot {mass_slot}; reduce dt or "
+                "stiffness", mass_slot=mass_slot)
+        if rc == SL_EINVAL:
+            raise InvalidValueError(f"{what}: {msg}")
+        raise DeviceError(f"{what} failed ({rc}): {msg}")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sl_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ upload
+    def upload_masses(self, pos, vel, acc, fext, load, mass, fixed, alive,
+                      gen):
+        n = len(mass)
+        a = [_c(pos, np.float64), _c(vel, np.float64), _c(acc, np.float64),
+             _c(fext, np.float64), _c(load, np.float64),
+             _c(mass, np.float64), _c(fixed, np.uint8), _c(alive, np.uint8),
+             _c(gen, np.int64)]
+        self._check(self.lib.sl_upload_masses(self.h, n, *map(_ptr, a)),
+                    "sl_upload_masses")
+        self.m_n = n
+
+    def upload_springs(self, m1, m2, m1gen, m2gen, rest, k, diam, yld, mode,
+                       amp, freq, off, per, alive, degen):
+        n = len(m1)
+        a = [_c(m1, np.int64), _c(m2, np.int64), _c(m1gen, np.int64),
+             _c(m2gen, np.int64), _c(rest, np.float64), _c(k, np.float64),
+             _c(diam, np.float64), _c(yld, np.float64), _c(mode, np.int8),
+             _c(amp, np.float64), _c(freq, np.float64), _c(off, np.float64),
+             _c(per, np.float64), _c(alive, np.uint8), _c(degen, np.uint8)]
+        self._check(self.lib.sl_upload_springs(self.h, n, *map(_ptr, a)),
+                    "sl_upload_springs")
+        self.s_n = n
+
+    def set_environment(self, gravity, drag, planes, balls, gc_kind, gc_vec,
+                        v_stick):
+        g = _c(gravity, np.float64)
+        pl = _c(np.reshape(planes, (-1, 7)), np.float64)
+        bl = _c(np.reshape(balls, (-1, 5)), np.float64)
+        gk = _c(gc_kind, np.int8)
+        gv = _c(np.reshape(gc_vec, (-1, 3)), np.float64)
+        self._check(self.lib.sl_set_environment(
+            self.h, _ptr(g), float(drag), _ptr(pl), len(pl), _ptr(bl),
+            len(bl), _ptr(gk), _ptr(gv), len(gk), float(v_stick)),
+            "sl_set_environment")
+
+    def set_local_constraints(self, lc_off, lc_kind, lc_vec):
+        off = _c(lc_off, np.int64)
+        kind = _c(lc_kind, np.int8)
+        vec = _c(np.reshape(lc_vec, (-1, 3)), np.float64)
+        self._check(self.lib.sl_set_local_constraints(
+            self.h, len(off) - 1, _ptr(off), _ptr(kind), _ptr(vec),
+            len(kind)), "sl_set_local_constraints")
+
+    def set_custom_factors(self, slots, factors):
+        s = _c(slots, np.int64)
+        f = _c(factors, np.float64)
+        self._check(self.lib.sl_set_custom_factors(self.h, len(s), _ptr(s),
+                                                   _ptr(f)),
+                    "sl_set_custom_factors")
+
+    def write_masses(self, slots, pos, vel, acc, fext, load, mass, fixed,
+                     alive, gen):
+        s = _c(slots, np.int64)
+        a = [_c(pos, np.float64), _c(vel, np.float64), _c(acc, np.float64),
+             _c(fext, np.float64), _c(load, np.float64),
+             _c(mass, np.float64), _c(fixed, np.uint8), _c(alive, np.uint8),
+             _c(gen, np.int64)]
+        self._check(self.lib.sl_write_masses(self.h, len(s), _ptr(s),
+                                             *map(_ptr, a)),
+                    "sl_write_masses")
+
+    def write_spring_params(self, slots, rest, k, diam, yld, mode, amp, freq,
+                            off, per):
+        s = _c(slots, np.int64)
+        a = [_c(rest, np.float64), _c(k, np.float64), _c(diam, np.float64),
+             _c(yld, np.float64), _c(mode, np.int8), _c(amp, np.float64),
+             _c(freq, np.float64), _c(off, np.float64), _c(per, np.float64)]
+        self._check(self.lib.sl_write_spring_params(self.h, len(s), _ptr(s),
+                                                    *map(_ptr, a)),
+                    "sl_write_spring_params")
+
+    def kill_springs(self, slots):
+        s = _c(slots, np.int64)
+        self._check(self.lib.sl_kill_springs(self.h, len(s), _ptr(s)),
+                    "sl_kill_springs")
+
+    # -------------------------------------------------------------- step
+    def step(self, sim_times, dt: float, accumulation: int,
+             counters: np.ndarray) -> tuple[int, int]:
+        """Returns (steps_done, err_slot); raises NumericalAbort on a
+        non-finite step (after the state of that step is resident)."""
+        t = _c(sim_times, np.float64)
+        err = C.c_int64(0)
+        done = C.c_int64(0)
+        rc = self.lib.sl_step(self.h, len(t), _ptr(t), float(dt),
+                              int(accumulation), _ptr(counters),
+                              C.byref(err), C.byref(done))
+        if rc == SL_ENUMERIC:
+            return int(done.value), int(err.value)
+        self._check(rc, "sl_step")
+        return int(done.value), 0
+
+    def spring_pass(self, sim_t: float, accumulation: int,
+                    counters: np.ndarray):
+        self._check(self.lib.sl_spring_pass(self.h, float(sim_t),
+                                            int(accumulation),
+                                            _ptr(counters)),
+                    "sl_spring_pass")
+
+    def mass_pass(self, dt: float) -> int:
+        err = C.c_int64(0)
+        rc = self.lib.sl_mass_pass(self.h, float(dt), C.byref(err))
+        if rc == SL_ENUMERIC:
+            return int(err.value)
+        self._check(rc, "sl_mass_pass")
+        return 0
+
+    # ----------------------------------------------------------- download
+    def download_masses(self, pos=None, vel=None, acc=None, fext=None):
+        for a in (pos, vel, acc, fext):
+            if a is not None:
+                assert a.dtype == np.float64 and a.flags.c_contiguous \
+                    and a.shape == (self.m_n, 3)
+        self._check(self.lib.sl_download_masses(
+            self.h, _ptr(pos), _ptr(vel), _ptr(acc), _ptr(fext)),
+            "sl_download_masses")
+
+    def download_springs(self, alive=None, degen=None):
+        for a in (alive, degen):
+            if a is not None:
+                assert a.itemsize == 1 and a.flags.c_contiguous \
+                    and a.shape == (self.s_n,)
+        self._check(self.lib.sl_download_springs(self.h, _ptr(alive),
+                                                 _ptr(degen)),
+                    "sl_download_springs")
+
+    def snapshot_begin(self):
+        self._check(self.lib.sl_snapshot_begin(self.h), "sl_snapshot_begin")
+
+    def snapshot_ready(self) -> bool:
+        r = C.c_int(0)
+        self._check(self.lib.sl_snapshot_ready(self.h, C.byref(r)),
+                    "sl_snapshot_ready")
+        return bool(r.value)
+
+    def snapshot_wait(self, pos=None, vel=None):
+        self._check(self.lib.sl_snapshot_wait(self.h, _ptr(pos), _ptr(vel)),
+                    "sl_snapshot_wait")
+
+    # ------------------------------------------------------------- timing
+    def timer_start(self):
+        self._check(self.lib.sl_timer_start(self.h), "sl_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = C.c_float(0.0)
+        self._check(self.lib.sl_timer_stop(self.h, C.byref(ms)),
+                    "sl_timer_stop")
+        return float(ms.value)
+
+    def sync(self):
+        self._check(self.lib.sl_sync(self.h), "sl_sync")
+
+    def stats(self) -> dict:
+        st = SlStats()
+        self._check(self.lib.sl_get_stats(self.h, C.byref(st)),
+                    "sl_get_stats")
+        return {f: getattr(st, f) for f, _ in SlStats._fields_}

@@ -1,0 +1,1285 @@
+// sl_api.cu -- context, device buffers, incidence-layout build and the C ABI
+// declared in include/softlat_cuda.h.
+//
+// Ownership mirrors the reference's engine cache (engine._StoreCache,
+// engine.py:71-146): the context owns every device buffer of one store on one
+// device and rebuilds the derived incidence layout when the spring topology
+// changes (the reference rebuilds its slotted CSR the same way,
+// engine.py:105-118) -- here the rebuild runs on the device (CUB radix sort),
+// so a 12.7M-spring lattice re-indexes in milliseconds.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+
+#include "../../include/softlat_cuda.h"
+#include "sl_device.cuh"
+
+namespace sl {
+const Launch &launch_fp64();
+const Launch &launch_fp32();
+const Launch &launch_mixed();
+const Launch &launchers(int prec) {
+  if (prec == PREC_FP64) return launch_fp64();
+  if (prec == PREC_FP32) return launch_fp32();
+  return launch_mixed();
+}
+}  // namespace sl
+
+using namespace sl;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (want == 0) want = 16;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T *as() const {
+    return (T *)p;
+  }
+};
+
+}  // namespace
+
+struct sl_ctx {
+  int device = 0;
+  int prec = PREC_FP64;
+  size_t rsz = 8, fsz = 8;  // sizeof(R), sizeof(F)
+  cudaStream_t st = nullptr, side = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr, snap_ev = nullptr,
+              snap_done = nullptr;
+  int64_t m_n = 0, s_n = 0;
+  int cur = 0;
+  bool masses_set = false, springs_set = false, env_set = false;
+  bool layout_valid = false, validate_dirty = true, has_special = false;
+  bool snap_pending = false;
+  // mass SoA
+  DevBuf pos[2], vel, acc, fext, load, m_gen, m_alive;
+  DevBuf lc_off, lc_kind, lc_vec;
+  bool has_lc = false;
+  // spring SoA
+  DevBuf ends, kL0, s_alive, s_degen, mode, act, thr, custom, m1gen, m2gen;
+  // incidence layout
+  DevBuf slice_ptr, ent_j, ent_kL0, ent_s, e1, e2;
+  int64_t n_slices = 0, n_entries = 0, alive_springs = 0, layout_builds = 0;
+  // scratch
+  DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
+  DevBuf status;
+  unsigned long long *h_status = nullptr;
+  DevBuf snap_dev;
+  double *snap_host = nullptr;
+  size_t snap_host_bytes = 0;
+  int64_t snap_m = 0;
+  EnvP env;
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(sl_ctx *c, int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c)
+    c->err = buf;
+  else
+    g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess)                                              \
+      return fail(c, SL_ECUDA, "%s failed: %s", #call,                  \
+                  cudaGetErrorString(e_));                              \
+  } while (0)
+
+#define CKL()                                                           \
+  do {                                                                  \
+    cudaError_t e_ = cudaGetLastError();                                \
+    if (e_ != cudaSuccess)                                              \
+      return fail(c, SL_ECUDA, "kernel launch failed: %s",              \
+                  cudaGetErrorString(e_));                              \
+  } while (0)
+
+// ------------------------------------------------------------- pack kernels
+template <int P>
+__global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
+                              const double *acc, const double *fext,
+                              const double *load, const double *mass,
+                              const uint8_t *fixed, const uint8_t *alive,
+                              const int64_t *slots, void *pos0, void *pos1,
+                              void *velo, void *acco, void *fexto,
+                              void *loado, int64_t *gen_o, uint8_t *alive_o,
+                              const int64_t *gen_in) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t i = slots ? slots[r] : r;
+  uint32_t fl = 0;
+  if (alive[r]) fl |= MF_ALIVE;
+  if (fixed[r]) fl |= MF_FIXED;
+  const double *ld = load + 3 * r;
+  if (__double_as_longlong(ld[0]) | __double_as_longlong(ld[1]) |
+      __double_as_longlong(ld[2]))
+    fl |= MF_LOAD;
+  const double *fe = fext + 3 * r;
+  if (__double_as_longlong(fe[0]) | __double_as_longlong(fe[1]) |
+      __double_as_longlong(fe[2]))
+    fl |= MF_FEXT;
+  R4 p;
+  p.x = (R)pos[3 * r];
+  p.y = (R)pos[3 * r + 1];
+  p.z = (R)pos[3 * r + 2];
+  p.w = (R)mass[r];
+  ((R4 *)pos0)[i] = p;
+  ((R4 *)pos1)[i] = p;
+  R4 v;
+  v.x = (R)vel[3 * r];
+  v.y = (R)vel[3 * r + 1];
+  v.z = (R)vel[3 * r + 2];
+  // keep an existing local-constraint flag (set by sl_set_local_constraints)
+  if (slots) fl |= flags_of(((R4 *)velo)[i].w) & MF_LC;
+  set_flags(v.w, fl);
+  ((R4 *)velo)[i] = v;
+  R *a = (R *)acco + 3 * i;
+  a[0] = (R)acc[3 * r];
+  a[1] = (R)acc[3 * r + 1];
+  a[2] = (R)acc[3 * r + 2];
+  R4 f;
+  f.x = (R)fe[0];
+  f.y = (R)fe[1];
+  f.z = (R)fe[2];
+  f.w = (R)0.0;
+  ((R4 *)fexto)[i] = f;
+  R *l = (R *)loado + 3 * i;
+  l[0] = (R)ld[0];
+  l[1] = (R)ld[1];
+  l[2] = (R)ld[2];
+  gen_o[i] = gen_in[r];
+  alive_o[i] = alive[r];
+}
+
+template <int P>
+__global__ void k_unpack_masses(int64_t n, const void *posb, const void *velb,
+                                const void *accb, const void *fextb,
+                                double *pos, double *vel, double *acc,
+                                double *fext) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (pos) {
+    R4 p = ((const R4 *)posb)[i];
+    pos[3 * i] = (double)p.x;
+    pos[3 * i + 1] = (double)p.y;
+    pos[3 * i + 2] = (double)p.z;
+  }
+  if (vel) {
+    R4 v = ((const R4 *)velb)[i];
+    vel[3 * i] = (double)v.x;
+    vel[3 * i + 1] = (double)v.y;
+    vel[3 * i + 2] = (double)v.z;
+  }
+  if (acc) {
+    const R *a = (const R *)accb + 3 * i;
+    acc[3 * i] = (double)a[0];
+    acc[3 * i + 1] = (double)a[1];
+    acc[3 * i + 2] = (double)a[2];
+  }
+  if (fext) {
+    R4 f = ((const R4 *)fextb)[i];
+    fext[3 * i] = (double)f.x;
+    fext[3 * i + 1] = (double)f.y;
+    fext[3 * i + 2] = (double)f.z;
+  }
+}
+
+__global__ void k_set_lc_flags(int64_t n, const int64_t *lc_off, void *velb,
+                               int is_double) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool has = lc_off && lc_off[i + 1] > lc_off[i];
+  if (is_double) {
+    double4 *v = (double4 *)velb + i;
+    uint32_t fl = flags_of(v->w);
+    set_flags(v->w, has ? (fl | MF_LC) : (fl & ~MF_LC));
+  } else {
+    float4 *v = (float4 *)velb + i;
+    uint32_t fl = flags_of(v->w);
+    set_flags(v->w, has ? (fl | MF_LC) : (fl & ~MF_LC));
+  }
+}
+
+__global__ void k_set_fext_flags(int64_t n, void *velb, int is_double) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (is_double) {
+    double4 *v = (double4 *)velb + i;
+    set_flags(v->w, flags_of(v->w) | MF_FEXT);
+  } else {
+    float4 *v = (float4 *)velb + i;
+    set_flags(v->w, flags_of(v->w) | MF_FEXT);
+  }
+}
+
+// yield threshold exactly as kernels.py:78-81 evaluates it:
+// area = ((0.25*pi)*d)*d ; break when |fmag| > y*area.
+__device__ __forceinline__ double yield_threshold(double y, double d) {
+  if (y == CUDART_INF) return CUDART_INF;
+  double area = __dmul_rn(__dmul_rn(__dmul_rn(0.25, CUDART_PI), d), d);
+  return __dmul_rn(y, area);
+}
+
+template <int P>
+__global__ void k_pack_springs(int64_t n, const int64_t *slots,
+                               const int64_t *m1, const int64_t *m2,
+                               const int64_t *m1gen, const int64_t *m2gen,
+                               const double *rest, const double *k,
+                               const double *diam, const double *yield,
+                               const int8_t *mode, const double *amp,
+                               const double *freq, const double *off,
+                               const double *per, const uint8_t *alive,
+                               const uint8_t *degen, KState S,
+                               int64_t *m1g_o, int64_t *m2g_o, int8_t *mode_o,
+                               double4 *act_o, uint8_t *degen_o,
+                               double *custom_o, int params_only,
+                               int layout_valid) {
+  using F = typename Tr<P>::F;
+  using F2 = typename Tr<P>::F2;
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t s = slots ? slots[r] : r;
+  F2 kl;
+  kl.x = (F)k[r];
+  kl.y = (F)rest[r];
+  ((F2 *)S.kL0)[s] = kl;
+  mode_o[s] = mode[r];
+  act_o[s] = make_double4(amp[r], freq[r], off[r], per[r]);
+  F th = (F)yield_threshold(yield[r], diam[r]);
+  ((F *)S.thr)[s] = th;
+  if (!params_only) {
+    bool al = alive[r] != 0;
+    S.ends[s] = al ? make_int2((int)m1[r], (int)m2[r]) : make_int2(-1, -1);
+    S.s_alive[s] = alive[r];
+    degen_o[s] = degen[r];
+    m1g_o[s] = m1gen[r];
+    m2g_o[s] = m2gen[r];
+    custom_o[s] = 1.0;
+  } else if (layout_valid) {
+    // keep the incidence copies of (k, L0) and the special bit in sync
+    bool special = mode[r] != 0 || yield[r] != CUDART_INF;
+    int64_t es[2] = {S.e1[s], S.e2[s]};
+    for (int q = 0; q < 2; q++) {
+      int64_t e = es[q];
+      if (e < 0) continue;
+      ((F2 *)S.ent_kL0)[e] = kl;
+      uint32_t j = S.ent_j[e];
+      S.ent_j[e] = special ? (j | EJ_SPECIAL) : (j & ~EJ_SPECIAL);
+    }
+  }
+}
+
+__global__ void k_kill_springs(int64_t n, const int64_t *slots, KState S,
+                               int layout_valid) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t s = slots[r];
+  S.ends[s] = make_int2(-1, -1);
+  S.s_alive[s] = 0;
+  if (layout_valid) {
+    if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
+    if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
+  }
+}
+
+__global__ void k_set_custom(int64_t n, const int64_t *slots,
+                             const double *f, double *custom) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) custom[slots[r]] = f[r];
+}
+
+// Lazy endpoint invalidation, kernels.py:37-45: an alive spring whose
+// endpoint is dead or was re-issued (generation mismatch) dies and counts as
+// invalid.  Deletions only happen at pause points (store.py:221-224), so
+// running this once before the first step after an edit is equivalent to the
+// reference's per-step check.
+__global__ void k_validate(KState S, const uint8_t *m_alive,
+                           const int64_t *m_gen, const int64_t *m1gen,
+                           const int64_t *m2gen, int layout_valid) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S.s_n) return;
+  int2 ab = S.ends[s];
+  if (ab.x < 0) return;
+  if (m_alive[ab.x] && m_alive[ab.y] && m_gen[ab.x] == m1gen[s] &&
+      m_gen[ab.y] == m2gen[s])
+    return;
+  S.ends[s] = make_int2(-1, -1);
+  S.s_alive[s] = 0;
+  if (layout_valid) {
+    if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
+    if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
+  }
+  atomicAdd(S.status + 1, 1ull);
+}
+
+// ------------------------------------------------------- layout build kernels
+// Two incidence records per alive spring: (owner m1, 2s) and (owner m2,
+// 2s+1) -- the owner array of engine._refresh_slotted_layout.  A stable
+// radix sort by owner leaves each mass's records in ascending slot order.
+__global__ void k_make_keys(int64_t s_n, const int2 *ends, uint32_t m_n,
+                            uint32_t *keys, uint32_t *vals, uint32_t *deg) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s_n) return;
+  int2 ab = ends[s];
+  bool al = ab.x >= 0;
+  keys[2 * s] = al ? (uint32_t)ab.x : m_n;
+  keys[2 * s + 1] = al ? (uint32_t)ab.y : m_n;
+  vals[2 * s] = (uint32_t)(2 * s);
+  vals[2 * s + 1] = (uint32_t)(2 * s + 1);
+  if (al) {
+    atomicAdd(deg + ab.x, 1u);
+    atomicAdd(deg + ab.y, 1u);
+  }
+}
+
+// per-slice width = max degree of its 32 masses; entries = 32 * width
+__global__ void k_slice_width(int64_t m_n, const uint32_t *deg,
+                              int64_t n_slices, int64_t *slice_entries) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t w = i >> 5;
+  if (w >= n_slices) return;
+  uint32_t d = i < m_n ? deg[i] : 0u;
+  for (int o = 16; o; o >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+  if ((i & 31) == 0) slice_entries[w] = 32 * (int64_t)d;
+}
+
+// rank of each sorted record within its owner's run
+__global__ void k_owner_start(int64_t n, const uint32_t *keys, uint32_t m_n,
+                              int64_t *start) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint32_t k = keys[p];
+  if (k >= m_n) return;
+  if (p == 0 || keys[p - 1] != k) start[k] = p;
+}
+
+template <int P>
+__global__ void k_fill_layout(int64_t n, const uint32_t *keys,
+                              const uint32_t *vals, uint32_t m_n,
+                              const int64_t *start, KState S,
+                              uint32_t *ent_j, void *ent_kl, int32_t *ent_s,
+                              int64_t *e1, int64_t *e2) {
+  using F = typename Tr<P>::F;
+  using F2 = typename Tr<P>::F2;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint32_t i = keys[p];
+  if (i >= m_n) return;
+  uint32_t v = vals[p];
+  int64_t s = v >> 1;
+  int side = v & 1;
+  int64_t rank = p - start[i];
+  int64_t e = S.slice_ptr[i >> 5] + 32 * rank + (i & 31);
+  int2 ab = S.ends[s];
+  uint32_t other = side ? (uint32_t)ab.x : (uint32_t)ab.y;
+  bool special =
+      S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+  ent_j[e] = other | (side ? EJ_M2 : 0u) | (special ? EJ_SPECIAL : 0u);
+  ((F2 *)ent_kl)[e] = ((const F2 *)S.kL0)[s];
+  ent_s[e] = (int32_t)s;
+  (side ? e2 : e1)[s] = e;
+}
+
+KState make_state(sl_ctx *c) {
+  KState S;
+  memset(&S, 0, sizeof S);
+  S.m_n = c->m_n;
+  S.s_n = c->s_n;
+  S.pos[0] = c->pos[0].p;
+  S.pos[1] = c->pos[1].p;
+  S.vel = c->vel.p;
+  S.acc = c->acc.p;
+  S.fext = c->fext.p;
+  S.load = c->load.p;
+  S.lc_off = c->has_lc ? c->lc_off.as<int64_t>() : nullptr;
+  S.lc_kind = c->lc_kind.as<int8_t>();
+  S.lc_vec = c->lc_vec.as<double>();
+  S.ends = c->ends.as<int2>();
+  S.kL0 = c->kL0.p;
+  S.s_alive = c->s_alive.as<uint8_t>();
+  S.s_degen = c->s_degen.as<uint8_t>();
+  S.mode = c->mode.as<int8_t>();
+  S.act = c->act.as<double4>();
+  S.thr = c->thr.p;
+  S.custom = c->custom.as<double>();
+  S.slice_ptr = c->slice_ptr.as<int64_t>();
+  S.ent_j = c->ent_j.as<uint32_t>();
+  S.ent_kL0 = c->ent_kL0.p;
+  S.ent_s = c->ent_s.as<int32_t>();
+  S.e1 = c->layout_valid ? c->e1.as<int64_t>() : nullptr;
+  S.e2 = c->layout_valid ? c->e2.as<int64_t>() : nullptr;
+  S.status = c->status.as<unsigned long long>();
+  return S;
+}
+
+template <class T>
+int stage_copy(sl_ctx *c, size_t &off, const T *host, int64_t count,
+               const T **dev) {
+  size_t bytes = sizeof(T) * (size_t)count;
+  off = (off + 255) & ~(size_t)255;
+  if (!host || count == 0) {
+    *dev = nullptr;
+    return SL_OK;
+  }
+  *dev = (const T *)((char *)c->stage.p + off);
+  CK(cudaMemcpyAsync((void *)*dev, host, bytes, cudaMemcpyHostToDevice,
+                     c->st));
+  off += bytes;
+  return SL_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int ensure_masses(sl_ctx *c, int64_t m_n) {
+  size_t r4 = 4 * c->rsz;
+  for (int b = 0; b < 2; b++) CK(c->pos[b].ensure(r4 * m_n));
+  CK(c->vel.ensure(r4 * m_n));
+  CK(c->acc.ensure(3 * c->rsz * m_n));
+  CK(c->fext.ensure(r4 * m_n));
+  CK(c->load.ensure(3 * c->rsz * m_n));
+  CK(c->m_gen.ensure(8 * m_n));
+  CK(c->m_alive.ensure(m_n));
+  return SL_OK;
+}
+
+int ensure_springs(sl_ctx *c, int64_t s_n) {
+  CK(c->ends.ensure(8 * s_n));
+  CK(c->kL0.ensure(2 * c->fsz * s_n));
+  CK(c->s_alive.ensure(s_n));
+  CK(c->s_degen.ensure(s_n));
+  CK(c->mode.ensure(s_n));
+  CK(c->act.ensure(32 * s_n));
+  CK(c->thr.ensure(c->fsz * s_n));
+  CK(c->custom.ensure(8 * s_n));
+  CK(c->m1gen.ensure(8 * s_n));
+  CK(c->m2gen.ensure(8 * s_n));
+  return SL_OK;
+}
+
+int build_layout(sl_ctx *c) {
+  const int64_t m_n = c->m_n, s_n = c->s_n;
+  if (m_n > (int64_t)EJ_MASK)
+    return fail(c, SL_EUNSUPPORTED, "too many masses for one context (%lld)",
+                (long long)m_n);
+  if (2 * s_n >= (int64_t)0x7fffffff)
+    return fail(c, SL_EUNSUPPORTED, "too many springs for one context");
+  const int64_t n_slices = (m_n + 31) / 32;
+  const int64_t n_rec = 2 * s_n;
+  CK(c->deg.ensure(4 * (m_n + 1)));
+  CK(c->width.ensure(8 * (n_slices + 1)));
+  CK(c->slice_ptr.ensure(8 * (n_slices + 1)));
+  CK(c->e1.ensure(8 * s_n));
+  CK(c->e2.ensure(8 * s_n));
+  CK(cudaMemsetAsync(c->deg.p, 0, 4 * (m_n + 1), c->st));
+  CK(cudaMemsetAsync(c->e1.p, 0xFF, 8 * s_n, c->st));
+  CK(cudaMemsetAsync(c->e2.p, 0xFF, 8 * s_n, c->st));
+  for (int b = 0; b < 2; b++) {
+    CK(c->keys[b].ensure(4 * n_rec));
+    CK(c->vals[b].ensure(4 * n_rec));
+  }
+  if (s_n > 0) {
+    k_make_keys<<<blocks_for(s_n), 256, 0, c->st>>>(
+        s_n, c->ends.as<int2>(), (uint32_t)m_n, c->keys[0].as<uint32_t>(),
+        c->vals[0].as<uint32_t>(), c->deg.as<uint32_t>());
+    CKL();
+  }
+  // slice entry counts -> exclusive scan -> slice_ptr
+  if (n_slices > 0) {
+    k_slice_width<<<blocks_for(32 * n_slices), 256, 0, c->st>>>(
+        m_n, c->deg.as<uint32_t>(), n_slices, c->width.as<int64_t>());
+    CKL();
+  }
+  size_t tmp_bytes = 0, t2 = 0;
+  int end_bit = 1;
+  while (((uint64_t)1 << end_bit) <= (uint64_t)m_n) end_bit++;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (int64_t *)nullptr,
+                                (int64_t *)nullptr, (int)(n_slices + 1));
+  if (n_rec > 0)
+    cub::DeviceRadixSort::SortPairs(
+        nullptr, t2, (uint32_t *)nullptr, (uint32_t *)nullptr,
+        (uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_rec, 0, end_bit);
+  CK(c->sort_tmp.ensure(std::max(tmp_bytes, t2)));
+  CK(cudaMemsetAsync(c->width.as<int64_t>() + n_slices, 0, 8, c->st));
+  tmp_bytes = c->sort_tmp.bytes;
+  CK(cub::DeviceScan::ExclusiveSum(c->sort_tmp.p, tmp_bytes,
+                                   c->width.as<int64_t>(),
+                                   c->slice_ptr.as<int64_t>(),
+                                   (int)(n_slices + 1), c->st));
+  int64_t n_ent = 0;
+  CK(cudaMemcpyAsync(&n_ent, c->slice_ptr.as<int64_t>() + n_slices, 8,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  CK(c->ent_j.ensure(4 * n_ent));
+  CK(c->ent_kL0.ensure(2 * c->fsz * n_ent));
+  CK(c->ent_s.ensure(4 * n_ent));
+  CK(cudaMemsetAsync(c->ent_j.p, 0xFF, 4 * n_ent, c->st));
+  CK(cudaMemsetAsync(c->ent_s.p, 0xFF, 4 * n_ent, c->st));
+  if (n_rec > 0) {
+    tmp_bytes = c->sort_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(
+        c->sort_tmp.p, tmp_bytes, c->keys[0].as<uint32_t>(),
+        c->keys[1].as<uint32_t>(), c->vals[0].as<uint32_t>(),
+        c->vals[1].as<uint32_t>(), (int)n_rec, 0, end_bit, c->st));
+    DevBuf &start = c->start;
+    CK(start.ensure(8 * (m_n + 1)));
+    k_owner_start<<<blocks_for(n_rec), 256, 0, c->st>>>(
+        n_rec, c->keys[1].as<uint32_t>(), (uint32_t)m_n,
+        start.as<int64_t>());
+    CKL();
+    KState S = make_state(c);
+    auto fill = c->prec == PREC_FP64   ? k_fill_layout<PREC_FP64>
+                : c->prec == PREC_FP32 ? k_fill_layout<PREC_FP32>
+                                       : k_fill_layout<PREC_MIXED>;
+    fill<<<blocks_for(n_rec), 256, 0, c->st>>>(
+        n_rec, c->keys[1].as<uint32_t>(), c->vals[1].as<uint32_t>(),
+        (uint32_t)m_n, start.as<int64_t>(), S, c->ent_j.as<uint32_t>(),
+        c->ent_kL0.p, c->ent_s.as<int32_t>(), c->e1.as<int64_t>(),
+        c->e2.as<int64_t>());
+    CKL();
+  }
+  CK(cudaStreamSynchronize(c->st));
+  c->n_slices = n_slices;
+  c->n_entries = n_ent;
+  c->layout_valid = true;
+  c->layout_builds++;
+  c->launches += 5;
+  return SL_OK;
+}
+
+int prepare(sl_ctx *c, bool need_layout) {
+  if (!c->masses_set || !c->springs_set)
+    return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
+  if (!c->env_set)
+    return fail(c, SL_ESTATE, "environment not set (sl_set_environment)");
+  CK(cudaMemsetAsync(c->status.p, 0, 8 * 8, c->st));
+  if (c->validate_dirty && c->s_n > 0) {
+    KState S = make_state(c);
+    k_validate<<<blocks_for(c->s_n), 256, 0, c->st>>>(
+        S, c->m_alive.as<uint8_t>(), c->m_gen.as<int64_t>(),
+        c->m1gen.as<int64_t>(), c->m2gen.as<int64_t>(), c->layout_valid);
+    CKL();
+    c->launches++;
+  }
+  c->validate_dirty = false;
+  if (need_layout && !c->layout_valid) {
+    int rc = build_layout(c);
+    if (rc) return rc;
+  }
+  return SL_OK;
+}
+
+int finish_status(sl_ctx *c, int64_t *counters, int64_t *err_slot) {
+  CK(cudaMemcpyAsync(c->h_status, c->status.p, 8 * 8, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (counters)
+    for (int q = 0; q < 3; q++) counters[q] += (int64_t)c->h_status[q];
+  if (err_slot) *err_slot = (int64_t)c->h_status[3];
+  return SL_OK;
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+extern "C" {
+
+int sl_abi_version(void) { return 1; }
+
+int sl_device_count(int *count) {
+  sl_ctx *c = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(c, SL_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return SL_OK;
+}
+
+const char *sl_last_error(const sl_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+int sl_create(int device, int precision, sl_ctx **out) {
+  sl_ctx *c = nullptr;
+  if (!out) return fail(c, SL_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (precision < 0 || precision > 2)
+    return fail(c, SL_EINVAL, "unknown precision %d", precision);
+  CK(cudaSetDevice(device));
+  c = new sl_ctx();
+  c->device = device;
+  c->prec = precision;
+  c->rsz = precision == PREC_FP32 ? 4 : 8;
+  c->fsz = precision == PREC_FP64 ? 8 : 4;
+  memset(&c->env, 0, sizeof c->env);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+  if (e == cudaSuccess)
+    e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->t0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->t1);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = c->status.ensure(8 * 8);
+  if (e == cudaSuccess)
+    e = cudaMallocHost((void **)&c->h_status, 8 * 8);
+  if (e != cudaSuccess) {
+    int rc = fail(nullptr, SL_ECUDA, "context init failed: %s",
+                  cudaGetErrorString(e));
+    sl_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return SL_OK;
+}
+
+int sl_destroy(sl_ctx *c) {
+  if (!c) return SL_OK;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  if (c->side) cudaStreamSynchronize(c->side);
+  DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc, &c->fext,
+                    &c->load, &c->m_gen, &c->m_alive, &c->lc_off,
+                    &c->lc_kind, &c->lc_vec, &c->ends, &c->kL0, &c->s_alive,
+                    &c->s_degen, &c->mode, &c->act, &c->thr, &c->custom,
+                    &c->m1gen, &c->m2gen, &c->slice_ptr, &c->ent_j,
+                    &c->ent_kL0, &c->ent_s, &c->e1, &c->e2, &c->stage,
+                    &c->sort_tmp, &c->keys[0], &c->keys[1], &c->vals[0],
+                    &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
+                    &c->snap_dev};
+  for (DevBuf *b : bufs) b->release();
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->snap_host) cudaFreeHost(c->snap_host);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  if (c->snap_ev) cudaEventDestroy(c->snap_ev);
+  if (c->snap_done) cudaEventDestroy(c->snap_done);
+  if (c->st) cudaStreamDestroy(c->st);
+  if (c->side) cudaStreamDestroy(c->side);
+  delete c;
+  return SL_OK;
+}
+
+int sl_get_stats(sl_ctx *c, sl_stats *o) {
+  if (!c || !o) return fail(c, SL_EINVAL, "NULL argument");
+  memset(o, 0, sizeof *o);
+  o->masses = c->m_n;
+  o->springs = c->s_n;
+  o->entries = c->n_entries;
+  o->slices = c->n_slices;
+  o->layout_builds = c->layout_builds;
+  o->kernel_launches = c->launches;
+  o->precision = c->prec;
+  o->device = c->device;
+  const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc,
+                          &c->fext, &c->load, &c->m_gen, &c->m_alive,
+                          &c->ends, &c->kL0, &c->s_alive, &c->s_degen,
+                          &c->mode, &c->act, &c->thr, &c->custom, &c->m1gen,
+                          &c->m2gen, &c->slice_ptr, &c->ent_j, &c->ent_kL0,
+                          &c->ent_s, &c->e1, &c->e2, &c->stage, &c->sort_tmp,
+                          &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1],
+                          &c->deg, &c->width};
+  for (const DevBuf *b : bufs) o->device_bytes += (int64_t)b->bytes;
+  if (c->springs_set) {
+    std::vector<uint8_t> al(c->s_n);
+    if (c->s_n) {
+      CK(cudaMemcpyAsync(al.data(), c->s_alive.p, c->s_n,
+                         cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+    }
+    for (uint8_t a : al) o->alive_springs += a;
+  }
+  return SL_OK;
+}
+
+int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
+                     const double *vel, const double *acc, const double *fext,
+                     const double *load, const double *mass,
+                     const uint8_t *fixed, const uint8_t *alive,
+                     const int64_t *gen) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (m_n < 0 || (m_n > 0 && (!pos || !vel || !mass || !fixed || !alive ||
+                              !gen)))
+    return fail(c, SL_EINVAL, "sl_upload_masses: bad arguments");
+  CK(cudaSetDevice(c->device));
+  if (m_n != c->m_n) c->layout_valid = false;  // slices follow mass count
+  int rc = ensure_masses(c, m_n);
+  if (rc) return rc;
+  std::vector<double> zeros;
+  if (!acc || !fext || !load) zeros.assign(3 * (size_t)m_n, 0.0);
+  size_t need = 0;
+  need += align256(24 * m_n) * 5 + align256(8 * m_n) * 2 +
+          align256(m_n) * 2 + 1024;
+  CK(c->stage.ensure(need));
+  size_t off = 0;
+  const double *dp, *dv, *da, *df, *dl, *dm;
+  const uint8_t *dfx, *dal;
+  const int64_t *dg;
+  if ((rc = stage_copy(c, off, pos, 3 * m_n, &dp))) return rc;
+  if ((rc = stage_copy(c, off, vel, 3 * m_n, &dv))) return rc;
+  if ((rc = stage_copy(c, off, acc ? acc : zeros.data(), 3 * m_n, &da)))
+    return rc;
+  if ((rc = stage_copy(c, off, fext ? fext : zeros.data(), 3 * m_n, &df)))
+    return rc;
+  if ((rc = stage_copy(c, off, load ? load : zeros.data(), 3 * m_n, &dl)))
+    return rc;
+  if ((rc = stage_copy(c, off, mass, m_n, &dm))) return rc;
+  if ((rc = stage_copy(c, off, fixed, m_n, &dfx))) return rc;
+  if ((rc = stage_copy(c, off, alive, m_n, &dal))) return rc;
+  if ((rc = stage_copy(c, off, gen, m_n, &dg))) return rc;
+  if (m_n > 0) {
+    auto k = c->prec == PREC_FP64   ? k_pack_masses<PREC_FP64>
+             : c->prec == PREC_FP32 ? k_pack_masses<PREC_FP32>
+                                    : k_pack_masses<PREC_MIXED>;
+    k<<<blocks_for(m_n), 256, 0, c->st>>>(
+        m_n, dp, dv, da, df, dl, dm, dfx, dal, nullptr, c->pos[0].p,
+        c->pos[1].p, c->vel.p, c->acc.p, c->fext.p, c->load.p,
+        c->m_gen.as<int64_t>(), c->m_alive.as<uint8_t>(), dg);
+    CKL();
+    c->launches++;
+    if (c->has_lc) {
+      k_set_lc_flags<<<blocks_for(m_n), 256, 0, c->st>>>(
+          m_n, c->lc_off.as<int64_t>(), c->vel.p, c->rsz == 8);
+      CKL();
+    }
+  }
+  CK(cudaStreamSynchronize(c->st));  // staging is reused by the next call
+  c->m_n = m_n;
+  c->cur = 0;
+  c->masses_set = true;
+  c->validate_dirty = true;
+  return SL_OK;
+}
+
+static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
+                               const int64_t *m1, const int64_t *m2,
+                               const int64_t *m1gen, const int64_t *m2gen,
+                               const double *rest, const double *k,
+                               const double *diam, const double *yield,
+                               const int8_t *mode, const double *amp,
+                               const double *freq, const double *off_,
+                               const double *per, const uint8_t *alive,
+                               const uint8_t *degen, bool params_only) {
+  CK(cudaSetDevice(c->device));
+  // host-side validation of the pieces the device trusts
+  for (int64_t r = 0; r < n; r++) {
+    if (!params_only && alive[r] &&
+        (m1[r] < 0 || m2[r] < 0 || m1[r] >= c->m_n || m2[r] >= c->m_n))
+      return fail(c, SL_EINVAL, "spring %lld endpoint out of range",
+                  (long long)(slots ? slots[r] : r));
+    if (mode[r] != 0 || yield[r] != INFINITY) c->has_special = true;
+  }
+  size_t need = align256(8 * n) * 16 + align256(n) * 3 + 2048;
+  CK(c->stage.ensure(need));
+  size_t off = 0;
+  const int64_t *dsl = nullptr, *d1 = nullptr, *d2 = nullptr, *dg1 = nullptr,
+                *dg2 = nullptr;
+  const double *dr, *dk, *dd, *dy, *da, *df, *doff, *dper;
+  const int8_t *dmo;
+  const uint8_t *dal = nullptr, *dde = nullptr;
+  int rc;
+  if ((rc = stage_copy(c, off, slots, slots ? n : 0, &dsl))) return rc;
+  if (!params_only) {
+    if ((rc = stage_copy(c, off, m1, n, &d1))) return rc;
+    if ((rc = stage_copy(c, off, m2, n, &d2))) return rc;
+    if ((rc = stage_copy(c, off, m1gen, n, &dg1))) return rc;
+    if ((rc = stage_copy(c, off, m2gen, n, &dg2))) return rc;
+    if ((rc = stage_copy(c, off, alive, n, &dal))) return rc;
+    if ((rc = stage_copy(c, off, degen, n, &dde))) return rc;
+  }
+  if ((rc = stage_copy(c, off, rest, n, &dr))) return rc;
+  if ((rc = stage_copy(c, off, k, n, &dk))) return rc;
+  if ((rc = stage_copy(c, off, diam, n, &dd))) return rc;
+  if ((rc = stage_copy(c, off, yield, n, &dy))) return rc;
+  if ((rc = stage_copy(c, off, mode, n, &dmo))) return rc;
+  if ((rc = stage_copy(c, off, amp, n, &da))) return rc;
+  if ((rc = stage_copy(c, off, freq, n, &df))) return rc;
+  if ((rc = stage_copy(c, off, off_, n, &doff))) return rc;
+  if ((rc = stage_copy(c, off, per, n, &dper))) return rc;
+  if (n > 0) {
+    KState S = make_state(c);
+    auto kk = c->prec == PREC_FP64   ? k_pack_springs<PREC_FP64>
+              : c->prec == PREC_FP32 ? k_pack_springs<PREC_FP32>
+                                     : k_pack_springs<PREC_MIXED>;
+    kk<<<blocks_for(n), 256, 0, c->st>>>(
+        n, dsl, d1, d2, dg1, dg2, dr, dk, dd, dy, dmo, da, df, doff, dper,
+        dal, dde, S, c->m1gen.as<int64_t>(), c->m2gen.as<int64_t>(),
+        c->mode.as<int8_t>(), c->act.as<double4>(),
+        c->s_degen.as<uint8_t>(), c->custom.as<double>(), params_only,
+        c->layout_valid);
+    CKL();
+    c->launches++;
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
+                      const int64_t *m2, const int64_t *m1gen,
+                      const int64_t *m2gen, const double *rest,
+                      const double *k, const double *diam,
+                      const double *yield, const int8_t *mode,
+                      const double *amp, const double *freq,
+                      const double *off, const double *per,
+                      const uint8_t *alive, const uint8_t *degen) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!c->masses_set)
+    return fail(c, SL_ESTATE, "upload masses before springs");
+  if (s_n < 0 || (s_n > 0 && (!m1 || !m2 || !m1gen || !m2gen || !rest ||
+                              !k || !diam || !yield || !mode || !amp ||
+                              !freq || !off || !per || !alive || !degen)))
+    return fail(c, SL_EINVAL, "sl_upload_springs: bad arguments");
+  CK(cudaSetDevice(c->device));
+  int rc = ensure_springs(c, s_n);
+  if (rc) return rc;
+  c->has_special = false;
+  c->s_n = s_n;
+  c->layout_valid = false;
+  rc = upload_springs_impl(c, s_n, nullptr, m1, m2, m1gen, m2gen, rest, k,
+                           diam, yield, mode, amp, freq, off, per, alive,
+                           degen, false);
+  if (rc) return rc;
+  c->springs_set = true;
+  c->validate_dirty = true;
+  return SL_OK;
+}
+
+int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
+                           const double *rest, const double *k,
+                           const double *diam, const double *yield,
+                           const int8_t *mode, const double *amp,
+                           const double *freq, const double *off,
+                           const double *per) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (n < 0 || (n > 0 && (!slots || !rest || !k || !diam || !yield ||
+                          !mode || !amp || !freq || !off || !per)))
+    return fail(c, SL_EINVAL, "sl_write_spring_params: bad arguments");
+  for (int64_t r = 0; r < n; r++)
+    if (slots[r] < 0 || slots[r] >= c->s_n)
+      return fail(c, SL_EINVAL, "spring slot %lld out of range",
+                  (long long)slots[r]);
+  return upload_springs_impl(c, n, slots, nullptr, nullptr, nullptr, nullptr,
+                             rest, k, diam, yield, mode, amp, freq, off, per,
+                             nullptr, nullptr, true);
+}
+
+int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (n <= 0) return SL_OK;
+  for (int64_t r = 0; r < n; r++)
+    if (slots[r] < 0 || slots[r] >= c->s_n)
+      return fail(c, SL_EINVAL, "spring slot %lld out of range",
+                  (long long)slots[r]);
+  CK(cudaSetDevice(c->device));
+  CK(c->stage.ensure(8 * n + 256));
+  size_t off = 0;
+  const int64_t *ds;
+  int rc = stage_copy(c, off, slots, n, &ds);
+  if (rc) return rc;
+  KState S = make_state(c);
+  k_kill_springs<<<blocks_for(n), 256, 0, c->st>>>(n, ds, S, c->layout_valid);
+  CKL();
+  c->launches++;
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_write_masses(sl_ctx *c, int64_t n, const int64_t *slots,
+                    const double *pos, const double *vel, const double *acc,
+                    const double *fext, const double *load,
+                    const double *mass, const uint8_t *fixed,
+                    const uint8_t *alive, const int64_t *gen) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (n < 0 || (n > 0 && (!slots || !pos || !vel || !acc || !fext || !load ||
+                          !mass || !fixed || !alive || !gen)))
+    return fail(c, SL_EINVAL, "sl_write_masses: bad arguments");
+  if (n == 0) return SL_OK;
+  for (int64_t r = 0; r < n; r++)
+    if (slots[r] < 0 || slots[r] >= c->m_n)
+      return fail(c, SL_EINVAL, "mass slot %lld out of range",
+                  (long long)slots[r]);
+  CK(cudaSetDevice(c->device));
+  CK(c->stage.ensure(align256(24 * n) * 5 + align256(8 * n) * 3 +
+                     align256(n) * 2 + 1024));
+  size_t off = 0;
+  const double *dp, *dv, *da, *df, *dl, *dm;
+  const uint8_t *dfx, *dal;
+  const int64_t *dg, *ds;
+  int rc;
+  if ((rc = stage_copy(c, off, slots, n, &ds))) return rc;
+  if ((rc = stage_copy(c, off, pos, 3 * n, &dp))) return rc;
+  if ((rc = stage_copy(c, off, vel, 3 * n, &dv))) return rc;
+  if ((rc = stage_copy(c, off, acc, 3 * n, &da))) return rc;
+  if ((rc = stage_copy(c, off, fext, 3 * n, &df))) return rc;
+  if ((rc = stage_copy(c, off, load, 3 * n, &dl))) return rc;
+  if ((rc = stage_copy(c, off, mass, n, &dm))) return rc;
+  if ((rc = stage_copy(c, off, fixed, n, &dfx))) return rc;
+  if ((rc = stage_copy(c, off, alive, n, &dal))) return rc;
+  if ((rc = stage_copy(c, off, gen, n, &dg))) return rc;
+  auto k = c->prec == PREC_FP64   ? k_pack_masses<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_pack_masses<PREC_FP32>
+                                  : k_pack_masses<PREC_MIXED>;
+  // write the current buffer and its partner (static masses are never
+  // rewritten by the step kernels, so both halves must agree)
+  k<<<blocks_for(n), 256, 0, c->st>>>(
+      n, dp, dv, da, df, dl, dm, dfx, dal, ds, c->pos[0].p, c->pos[1].p,
+      c->vel.p, c->acc.p, c->fext.p, c->load.p, c->m_gen.as<int64_t>(),
+      c->m_alive.as<uint8_t>(), dg);
+  CKL();
+  c->launches++;
+  CK(cudaStreamSynchronize(c->st));
+  c->validate_dirty = true;
+  return SL_OK;
+}
+
+int sl_set_environment(sl_ctx *c, const double *gravity, double drag,
+                       const double *planes, int64_t n_planes,
+                       const double *balls, int64_t n_balls,
+                       const int8_t *gc_kind, const double *gc_vec,
+                       int64_t n_gc, double v_stick) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!gravity) return fail(c, SL_EINVAL, "gravity is NULL");
+  if (n_planes < 0 || n_planes > MAXP || n_balls < 0 || n_balls > MAXB ||
+      n_gc < 0 || n_gc > MAXG)
+    return fail(c, SL_EUNSUPPORTED,
+                "environment too large (planes<=%d balls<=%d global<=%d)",
+                MAXP, MAXB, MAXG);
+  EnvP &E = c->env;
+  memset(&E, 0, sizeof E);
+  for (int q = 0; q < 3; q++) E.g[q] = gravity[q];
+  E.drag = drag;
+  E.v_stick = v_stick;
+  E.np = (int)n_planes;
+  E.nb = (int)n_balls;
+  E.ngc = (int)n_gc;
+  for (int p = 0; p < n_planes; p++)
+    for (int q = 0; q < 7; q++) E.pl[p][q] = planes[7 * p + q];
+  for (int b = 0; b < n_balls; b++)
+    for (int q = 0; q < 5; q++) E.bl[b][q] = balls[5 * b + q];
+  for (int g = 0; g < n_gc; g++) {
+    E.gck[g] = gc_kind[g];
+    for (int q = 0; q < 3; q++) E.gcv[g][q] = gc_vec[3 * g + q];
+  }
+  c->env_set = true;
+  return SL_OK;
+}
+
+int sl_set_local_constraints(sl_ctx *c, int64_t m_n, const int64_t *lc_off,
+                             const int8_t *lc_kind, const double *lc_vec,
+                             int64_t n_lc) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "upload masses first");
+  if (m_n != c->m_n) return fail(c, SL_EINVAL, "lc_off must have m_n+1 rows");
+  CK(cudaSetDevice(c->device));
+  if (n_lc <= 0 || !lc_off) {
+    c->has_lc = false;
+    if (m_n > 0) {
+      k_set_lc_flags<<<blocks_for(m_n), 256, 0, c->st>>>(m_n, nullptr,
+                                                         c->vel.p, c->rsz == 8);
+      CKL();
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return SL_OK;
+  }
+  CK(c->lc_off.ensure(8 * (m_n + 1)));
+  CK(c->lc_kind.ensure(n_lc));
+  CK(c->lc_vec.ensure(24 * n_lc));
+  CK(cudaMemcpyAsync(c->lc_off.p, lc_off, 8 * (m_n + 1),
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->lc_kind.p, lc_kind, n_lc, cudaMemcpyHostToDevice,
+                     c->st));
+  CK(cudaMemcpyAsync(c->lc_vec.p, lc_vec, 24 * n_lc, cudaMemcpyHostToDevice,
+                     c->st));
+  c->has_lc = true;
+  if (m_n > 0) {
+    k_set_lc_flags<<<blocks_for(m_n), 256, 0, c->st>>>(
+        m_n, c->lc_off.as<int64_t>(), c->vel.p, c->rsz == 8);
+    CKL();
+  }
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_set_custom_factors(sl_ctx *c, int64_t n, const int64_t *slots,
+                          const double *factors) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (n <= 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  CK(c->stage.ensure(align256(8 * n) * 2 + 512));
+  size_t off = 0;
+  const int64_t *ds;
+  const double *df;
+  int rc;
+  if ((rc = stage_copy(c, off, slots, n, &ds))) return rc;
+  if ((rc = stage_copy(c, off, factors, n, &df))) return rc;
+  k_set_custom<<<blocks_for(n), 256, 0, c->st>>>(n, ds, df,
+                                                 c->custom.as<double>());
+  CKL();
+  c->launches++;
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
+            int accumulation, int64_t *counters, int64_t *err_slot,
+            int64_t *steps_done) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (n_steps < 0 || (n_steps > 0 && !sim_times))
+    return fail(c, SL_EINVAL, "sl_step: bad arguments");
+  if (!(dt > 0) || !std::isfinite(dt))
+    return fail(c, SL_EINVAL, "dt must be positive, got %g", dt);
+  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC)
+    return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
+  if (err_slot) *err_slot = 0;
+  if (steps_done) *steps_done = 0;
+  CK(cudaSetDevice(c->device));
+  int rc = prepare(c, accumulation == SL_ACC_GATHER);
+  if (rc) return rc;
+  const Launch &L = launchers(c->prec);
+  KState S = make_state(c);
+  for (int64_t n = 0; n < n_steps; n++) {
+    StepP T;
+    T.sim_t = sim_times[n];
+    T.dt = dt;
+    T.step = n;
+    T.cur = (int)((c->cur + n) & 1);
+    T.write_acc = n == n_steps - 1;
+    if (accumulation == SL_ACC_GATHER) {
+      L.gather(S, c->env, T, c->st);
+      c->launches++;
+    } else {
+      L.spring_atomic(S, T, c->has_special, c->st);
+      L.mass(S, c->env, T, c->st);
+      c->launches += 2;
+    }
+  }
+  CKL();
+  int64_t err = 0;
+  if ((rc = finish_status(c, counters, &err))) return rc;
+  int64_t done = n_steps;
+  if (c->h_status[4]) done = (int64_t)c->h_status[4];
+  c->cur = (int)((c->cur + done) & 1);
+  if (steps_done) *steps_done = done;
+  if (err_slot) *err_slot = err;
+  if (err) return fail(c, SL_ENUMERIC, "non-finite state on mass slot %lld",
+                       (long long)(err - 1));
+  return SL_OK;
+}
+
+int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
+                   int64_t *counters) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  CK(cudaSetDevice(c->device));
+  int rc = prepare(c, accumulation == SL_ACC_GATHER);
+  if (rc) return rc;
+  const Launch &L = launchers(c->prec);
+  KState S = make_state(c);
+  StepP T;
+  T.sim_t = sim_t;
+  T.dt = 0.0;
+  T.step = 0;
+  T.cur = c->cur;
+  T.write_acc = 0;
+  if (accumulation == SL_ACC_GATHER) {
+    L.force_only(S, c->env, T, c->st);
+    c->launches++;
+  } else {
+    L.spring_atomic(S, T, c->has_special, c->st);
+    if (c->m_n > 0)
+      k_set_fext_flags<<<blocks_for(c->m_n), 256, 0, c->st>>>(c->m_n, c->vel.p,
+                                                            c->rsz == 8);
+    c->launches += 2;
+  }
+  CKL();
+  return finish_status(c, counters, nullptr);
+}
+
+int sl_mass_pass(sl_ctx *c, double dt, int64_t *err_slot) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!(dt > 0)) return fail(c, SL_EINVAL, "dt must be positive");
+  CK(cudaSetDevice(c->device));
+  int rc = prepare(c, false);
+  if (rc) return rc;
+  KState S = make_state(c);
+  StepP T;
+  T.sim_t = 0.0;
+  T.dt = dt;
+  T.step = 0;
+  T.cur = c->cur;
+  T.write_acc = 1;
+  launchers(c->prec).mass(S, c->env, T, c->st);
+  c->launches++;
+  CKL();
+  int64_t err = 0;
+  if ((rc = finish_status(c, nullptr, &err))) return rc;
+  c->cur ^= 1;
+  if (err_slot) *err_slot = err;
+  if (err) return fail(c, SL_ENUMERIC, "non-finite state on mass slot %lld",
+                       (long long)(err - 1));
+  return SL_OK;
+}
+
+int sl_download_masses(sl_ctx *c, double *pos, double *vel, double *acc,
+                       double *fext) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  const int64_t m = c->m_n;
+  if (m == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  size_t vb = align256(24 * m);
+  CK(c->stage.ensure(4 * vb));
+  double *dp = pos ? (double *)c->stage.p : nullptr;
+  double *dv = vel ? (double *)((char *)c->stage.p + vb) : nullptr;
+  double *da = acc ? (double *)((char *)c->stage.p + 2 * vb) : nullptr;
+  double *df = fext ? (double *)((char *)c->stage.p + 3 * vb) : nullptr;
+  auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                  : k_unpack_masses<PREC_MIXED>;
+  k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p, c->vel.p,
+                                      c->acc.p, c->fext.p, dp, dv, da, df);
+  CKL();
+  c->launches++;
+  if (pos) CK(cudaMemcpyAsync(pos, dp, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (vel) CK(cudaMemcpyAsync(vel, dv, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (acc) CK(cudaMemcpyAsync(acc, da, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (fext)
+    CK(cudaMemcpyAsync(fext, df, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_download_springs(sl_ctx *c, uint8_t *alive, uint8_t *degen) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (c->s_n == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  if (alive)
+    CK(cudaMemcpyAsync(alive, c->s_alive.p, c->s_n, cudaMemcpyDeviceToHost,
+                       c->st));
+  if (degen)
+    CK(cudaMemcpyAsync(degen, c->s_degen.p, c->s_n, cudaMemcpyDeviceToHost,
+                       c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_snapshot_begin(sl_ctx *c) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  const int64_t m = c->m_n;
+  CK(cudaSetDevice(c->device));
+  if (c->snap_pending) CK(cudaEventSynchronize(c->snap_done));
+  size_t bytes = 48 * (size_t)m + 16;
+  CK(c->snap_dev.ensure(bytes));
+  if (c->snap_host_bytes < bytes) {
+    if (c->snap_host) cudaFreeHost(c->snap_host);
+    c->snap_host = nullptr;
+    c->snap_host_bytes = 0;
+    CK(cudaMallocHost((void **)&c->snap_host, bytes));
+    c->snap_host_bytes = bytes;
+  }
+  if (m > 0) {
+    auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+             : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                    : k_unpack_masses<PREC_MIXED>;
+    double *dp = (double *)c->snap_dev.p;
+    k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p, c->vel.p,
+                                        nullptr, nullptr, dp, dp + 3 * m,
+                                        nullptr, nullptr);
+    CKL();
+    c->launches++;
+  }
+  CK(cudaEventRecord(c->snap_ev, c->st));
+  CK(cudaStreamWaitEvent(c->side, c->snap_ev, 0));
+  if (m > 0)
+    CK(cudaMemcpyAsync(c->snap_host, c->snap_dev.p, 48 * m,
+                       cudaMemcpyDeviceToHost, c->side));
+  CK(cudaEventRecord(c->snap_done, c->side));
+  c->snap_m = m;
+  c->snap_pending = true;
+  return SL_OK;
+}
+
+int sl_snapshot_ready(sl_ctx *c, int *ready) {
+  if (!c || !ready) return fail(c, SL_EINVAL, "NULL argument");
+  if (!c->snap_pending) return fail(c, SL_ESTATE, "no snapshot in flight");
+  cudaError_t e = cudaEventQuery(c->snap_done);
+  if (e == cudaErrorNotReady) {
+    *ready = 0;
+    return SL_OK;
+  }
+  CK(e);
+  *ready = 1;
+  return SL_OK;
+}
+
+int sl_snapshot_wait(sl_ctx *c, double *pos, double *vel) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!c->snap_pending) return fail(c, SL_ESTATE, "no snapshot in flight");
+  CK(cudaEventSynchronize(c->snap_done));
+  const int64_t m = c->snap_m;
+  if (pos) memcpy(pos, c->snap_host, 24 * m);
+  if (vel) memcpy(vel, c->snap_host + 3 * m, 24 * m);
+  c->snap_pending = false;
+  return SL_OK;
+}
+
+int sl_timer_start(sl_ctx *c) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  CK(cudaEventRecord(c->t0, c->st));
+  return SL_OK;
+}
+
+int sl_timer_stop(sl_ctx *c, float *ms) {
+  if (!c || !ms) return fail(c, SL_EINVAL, "NULL argument");
+  CK(cudaEventRecord(c->t1, c->st));
+  CK(cudaEventSynchronize(c->t1));
+  CK(cudaEventElapsedTime(ms, c->t0, c->t1));
+  return SL_OK;
+}
+
+int sl_sync(sl_ctx *c) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,584 @@
+// sl_device.cuh -- device-side types and kernel templates for the
+// spring-mass step (sm_100a).
+//
+// Semantics follow the reference kernels (/root/reference/pkg/src/softlat/
+// kernels.py); the code is a B200-first re-design, not a translation:
+//
+//   * Mass state is resident in HBM as 16/32-byte records:
+//       pos[2][M] = (x, y, z, m)        -- ping-pong: step n reads buffer
+//                                          (cur+n)&1, writes the other, so
+//                                          the barrier invariant of
+//                                          engine.py:5-7 holds inside one
+//                                          fused kernel
+//       vel[M]    = (vx, vy, vz, flags)  -- flags packed in the spare lane
+//   * Deterministic accumulation ("gather", == reference slotted/serial
+//     order, engine.py:105-118) uses a per-mass incidence list in a sliced
+//     ELL layout: slice = 32 consecutive masses = one warp; entry t of lane l
+//     lives at slice_ptr[w] + 32*t + l so every warp-wide load of the list is
+//     one contiguous 128/256-byte transaction.  Entries of a mass appear in
+//     ascending spring slot, so the per-mass sum has exactly the serial
+//     operation order (bit-exact in fp64).  Each entry carries the other
+//     endpoint and a copy of (k, L0); the spring force is recomputed at both
+//     endpoints (identical inputs -> identical bits), which removes the
+//     scatter, the atomics and the f_ext round trip entirely: one kernel per
+//     step does spring pass + mass pass.
+//   * "atomic" accumulation (reference linearizable) = one thread per
+//     spring, red.global vector atomics into f_ext, then a mass kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <math_constants.h>
+
+namespace sl {
+
+enum : int { PREC_FP64 = 0, PREC_FP32 = 1, PREC_MIXED = 2 };
+
+// mass flag bits (packed into vel[i].w)
+enum : uint32_t {
+  MF_ALIVE = 1u,
+  MF_FIXED = 2u,
+  MF_LC = 4u,     // has local constraints (CSR lookup needed)
+  MF_LOAD = 8u,   // persistent load has non-zero bits
+  MF_FEXT = 16u,  // f_ext accumulator has non-zero bits at step start
+};
+
+// incidence entry word: low 29 bits other endpoint
+enum : uint32_t {
+  EJ_MASK = 0x1FFFFFFFu,
+  EJ_SPECIAL = 1u << 29,  // actuated or finite yield: per-slot lookup
+  EJ_M2 = 1u << 30,       // this mass is endpoint m2: subtract the force
+  EJ_DEAD = 1u << 31,     // dead spring or padding
+};
+constexpr uint32_t EJ_PAD = 0xFFFFFFFFu;
+
+constexpr int MAXP = 8;  // contact planes
+constexpr int MAXB = 8;  // contact balls
+constexpr int MAXG = 4;  // global constraints
+
+struct EnvP {
+  double g[3];
+  double drag;
+  double v_stick;
+  int np, nb, ngc, pad_;
+  double pl[MAXP][7];
+  double bl[MAXB][5];
+  double gcv[MAXG][3];
+  int gck[MAXG];
+};
+
+// All device pointers of one context (type-erased; kernels cast).
+struct KState {
+  int64_t m_n, s_n;
+  void *pos[2];
+  void *vel;
+  void *acc;   // R[3*m_n]
+  void *fext;  // R4[m_n]
+  const void *load;  // R[3*m_n]
+  const int64_t *lc_off;
+  const int8_t *lc_kind;
+  const double *lc_vec;
+  // spring SoA by slot
+  int2 *ends;          // (m1, m2); x < 0 => dead
+  const void *kL0;     // F2 (k, rest)
+  uint8_t *s_alive;
+  uint8_t *s_degen;
+  const int8_t *mode;
+  const double4 *act;  // (amp, freq, off, per)
+  const void *thr;     // F: yield * area, +inf if no yield
+  const double *custom;
+  // incidence layout
+  const int64_t *slice_ptr;
+  uint32_t *ent_j;
+  const void *ent_kL0;  // F2
+  const int32_t *ent_s;
+  const int64_t *e1, *e2;
+  // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
+  unsigned long long *status;
+};
+
+struct StepP {
+  double sim_t;
+  double dt;
+  int64_t step;   // index within the current sl_step call
+  int cur;        // pos buffer read this step
+  int write_acc;  // store acceleration (final step of a launch)
+};
+
+template <int P>
+struct Tr;
+template <>
+struct Tr<PREC_FP64> {
+  using R = double;
+  using F = double;
+  using R4 = double4;
+  using F2 = double2;
+};
+template <>
+struct Tr<PREC_FP32> {
+  using R = float;
+  using F = float;
+  using R4 = float4;
+  using F2 = float2;
+};
+template <>
+struct Tr<PREC_MIXED> {
+  using R = double;
+  using F = float;
+  using R4 = double4;
+  using F2 = float2;
+};
+
+__device__ __forceinline__ uint32_t flags_of(float w) {
+  return __float_as_uint(w);
+}
+__device__ __forceinline__ uint32_t flags_of(double w) {
+  return (uint32_t)__double_as_longlong(w);
+}
+__device__ __forceinline__ void set_flags(float &w, uint32_t f) {
+  w = __uint_as_float(f);
+}
+__device__ __forceinline__ void set_flags(double &w, uint32_t f) {
+  w = __longlong_as_double((long long)f);
+}
+
+// Python float % (CPython float_rem, which numba follows; kernels.py:58).
+__device__ __forceinline__ double py_mod(double a, double b) {
+  double r = fmod(a, b);
+  if (r != 0.0) {
+    if ((r < 0.0) != (b < 0.0)) r += b;
+  } else {
+    r = copysign(0.0, b);
+  }
+  return r;
+}
+
+// kernels.py:55-65 (fp64 always: the phase wraps sim time of arbitrary size)
+__device__ __forceinline__ double act_factor(const KState &S, int64_t s,
+                                             double sim_t) {
+  int m = S.mode[s];
+  if (m == 1 || m == 2) {
+    double4 a = S.act[s];  // amp, freq, off, per
+    if (m == 2 && !(sim_t >= a.z)) return 1.0;
+    double t = py_mod(sim_t - a.z, a.w);
+    return 1.0 + a.x * sin(a.y * t);
+  }
+  if (m == 3) return S.custom[s];
+  return 1.0;
+}
+
+__device__ __forceinline__ bool stopped(const KState &S, int64_t step) {
+  // a strictly earlier step of this launch went non-finite: do nothing
+  unsigned long long e = *(volatile unsigned long long *)(S.status + 4);
+  return e != 0ull && (int64_t)e - 1 < step;
+}
+
+__device__ __forceinline__ void count(const KState &S, int which) {
+  atomicAdd(S.status + which, 1ull);
+}
+
+__device__ __forceinline__ void mark_nonfinite(const KState &S, int64_t i,
+                                               int64_t step) {
+  atomicMax(S.status + 3, (unsigned long long)(i + 1));
+  *(volatile unsigned long long *)(S.status + 4) =
+      (unsigned long long)(step + 1);
+}
+
+// vector atomics into f_ext (sm_90+: red.global.add.v4.f32)
+__device__ __forceinline__ void red_add(float4 *p, float x, float y,
+                                        float z) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "f"(x), "f"(y), "f"(z), "f"(0.0f)
+               : "memory");
+}
+__device__ __forceinline__ void red_add(double4 *p, double x, double y,
+                                        double z) {
+  atomicAdd(&p->x, x);
+  atomicAdd(&p->y, y);
+  atomicAdd(&p->z, z);
+}
+
+// ---------------------------------------------------------------------------
+// Mass pass body (kernels.py:271-376), shared by the fused gather step and
+// the standalone mass kernel.  (fx, fy, fz) enters as the accumulated f_ext.
+// Writes pos_next / vel / acc; returns false on non-finite state.
+template <int P>
+__device__ __forceinline__ void integrate(
+    const KState &S, const EnvP &E, const StepP &T, int64_t i,
+    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
+    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  const R mm = me.w;
+  R px = me.x, py = me.y, pz = me.z;
+  R vx = v.x, vy = v.y, vz = v.z;
+  // F = ((f_ext + load) + m*g) - drag*v; an all-zero load adds +0.0, which
+  // keeps the sign-of-zero behaviour of the reference's addition.
+  if (fl & MF_LOAD) {
+    const R *ld = (const R *)S.load + 3 * i;
+    fx = fx + ld[0];
+    fy = fy + ld[1];
+    fz = fz + ld[2];
+  } else {
+    fx = fx + (R)0.0;
+    fy = fy + (R)0.0;
+    fz = fz + (R)0.0;
+  }
+  fx = fx + mm * (R)E.g[0];
+  fy = fy + mm * (R)E.g[1];
+  fz = fz + mm * (R)E.g[2];
+  const R drag = (R)E.drag;
+  fx = fx - drag * vx;
+  fy = fy - drag * vy;
+  fz = fz - drag * vz;
+  // contact planes with Coulomb friction on the running force
+  for (int p = 0; p < E.np; p++) {
+    const R nx = (R)E.pl[p][0], ny = (R)E.pl[p][1], nz = (R)E.pl[p][2];
+    const R depth = (R)E.pl[p][3] - (px * nx + py * ny + pz * nz);
+    if (depth > (R)0.0) {
+      const R nmag = (R)E.pl[p][4] * depth;
+      fx += nmag * nx;
+      fy += nmag * ny;
+      fz += nmag * nz;
+      const R vn = vx * nx + vy * ny + vz * nz;
+      const R tvx = vx - vn * nx, tvy = vy - vn * ny, tvz = vz - vn * nz;
+      const R tv = sqrt(tvx * tvx + tvy * tvy + tvz * tvz);
+      const R fn = fx * nx + fy * ny + fz * nz;
+      const R tfx = fx - fn * nx, tfy = fy - fn * ny, tfz = fz - fn * nz;
+      const R tf = sqrt(tfx * tfx + tfy * tfy + tfz * tfz);
+      const R vs = (R)E.v_stick;
+      if (tv < vs && tf <= (R)E.pl[p][5] * nmag) {
+        fx -= tfx;
+        fy -= tfy;
+        fz -= tfz;
+      } else if (tv >= vs) {
+        const R sc = (R)E.pl[p][6] * nmag / tv;
+        fx -= sc * tvx;
+        fy -= sc * tvy;
+        fz -= sc * tvz;
+      } else if (tf > (R)0.0) {
+        const R sc = (R)E.pl[p][6] * nmag / tf;
+        fx -= sc * tfx;
+        fy -= sc * tfy;
+        fz -= sc * tfz;
+      }
+    }
+  }
+  for (int b = 0; b < E.nb; b++) {
+    const R ddx = px - (R)E.bl[b][0], ddy = py - (R)E.bl[b][1],
+            ddz = pz - (R)E.bl[b][2];
+    const R dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+    const R depth = (R)E.bl[b][3] - dist;
+    if (depth > (R)0.0 && dist > (R)0.0) {
+      const R sc = (R)E.bl[b][4] * depth / dist;
+      fx += sc * ddx;
+      fy += sc * ddy;
+      fz += sc * ddz;
+    }
+  }
+  const R ax = fx / mm, ay = fy / mm, az = fz / mm;
+  const R dt = (R)T.dt;
+  vx += ax * dt;
+  vy += ay * dt;
+  vz += az * dt;
+  for (int g = 0; g < E.ngc; g++) {
+    const R cx = (R)E.gcv[g][0], cy = (R)E.gcv[g][1], cz = (R)E.gcv[g][2];
+    const R vd = vx * cx + vy * cy + vz * cz;
+    if (E.gck[g] == 1) {
+      vx = vd * cx;
+      vy = vd * cy;
+      vz = vd * cz;
+    } else {
+      vx -= vd * cx;
+      vy -= vd * cy;
+      vz -= vd * cz;
+    }
+  }
+  if (fl & MF_LC) {
+    for (int64_t kk = S.lc_off[i]; kk < S.lc_off[i + 1]; kk++) {
+      const R cx = (R)S.lc_vec[3 * kk], cy = (R)S.lc_vec[3 * kk + 1],
+              cz = (R)S.lc_vec[3 * kk + 2];
+      const R vd = vx * cx + vy * cy + vz * cz;
+      if (S.lc_kind[kk] == 1) {
+        vx = vd * cx;
+        vy = vd * cy;
+        vz = vd * cz;
+      } else {
+        vx -= vd * cx;
+        vy -= vd * cy;
+        vz -= vd * cz;
+      }
+    }
+  }
+  px += vx * dt;
+  py += vy * dt;
+  pz += vz * dt;
+  R4 np4;
+  np4.x = px;
+  np4.y = py;
+  np4.z = pz;
+  np4.w = mm;
+  ((R4 *)S.pos[T.cur ^ 1])[i] = np4;
+  R4 nv;
+  nv.x = vx;
+  nv.y = vy;
+  nv.z = vz;
+  set_flags(nv.w, fl & ~MF_FEXT);
+  ((R4 *)S.vel)[i] = nv;
+  if (T.write_acc) {
+    R *a = (R *)S.acc + 3 * i;
+    a[0] = ax;
+    a[1] = ay;
+    a[2] = az;
+  }
+  if (!(isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) &&
+        isfinite(vy) && isfinite(vz)))
+    mark_nonfinite(S, i, T.step);
+}
+
+template <int P>
+__device__ __forceinline__ void fixed_mass(const KState &S, const StepP &T,
+                                           int64_t i, typename Tr<P>::R4 v,
+                                           uint32_t fl) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  // kernels.py:260-270: vel = acc = f_ext = 0, pos and load untouched
+  R4 nv;
+  nv.x = (R)0.0;
+  nv.y = (R)0.0;
+  nv.z = (R)0.0;
+  set_flags(nv.w, fl & ~MF_FEXT);
+  ((R4 *)S.vel)[i] = nv;
+  if (T.write_acc) {
+    R *a = (R *)S.acc + 3 * i;
+    a[0] = a[1] = a[2] = (R)0.0;
+  }
+  if (fl & MF_FEXT) {
+    R4 z;
+    z.x = z.y = z.z = z.w = (R)0.0;
+    ((R4 *)S.fext)[i] = z;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One incidence entry: spring force between this mass and `other`, in the
+// reference's operation order (kernels.py:46-83).  Returns false if the
+// entry contributes nothing.  Side effects (yield break, zero-length flag,
+// counters) are performed exactly once per spring, by its m1 endpoint; the
+// m2 endpoint reaches the same decision from the same bits and only kills
+// its own entry.
+template <int P>
+__device__ __forceinline__ bool entry_force(
+    const KState &S, int64_t e, uint32_t jr, typename Tr<P>::R4 me,
+    typename Tr<P>::R4 other, typename Tr<P>::F2 kl, double sim_t,
+    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using F = typename Tr<P>::F;
+  const bool is_m2 = (jr & EJ_M2) != 0;
+  // d = pos[m2] - pos[m1]
+  F dx, dy, dz;
+  if (is_m2) {
+    dx = (F)(me.x - other.x);
+    dy = (F)(me.y - other.y);
+    dz = (F)(me.z - other.z);
+  } else {
+    dx = (F)(other.x - me.x);
+    dy = (F)(other.y - me.y);
+    dz = (F)(other.z - me.z);
+  }
+  const F len = sqrt(dx * dx + dy * dy + dz * dz);
+  if (len == (F)0.0) {
+    if (!is_m2) {
+      const int32_t s = S.ent_s[e];
+      if (!S.s_degen[s]) {
+        S.s_degen[s] = 1;
+        count(S, 2);
+      }
+    }
+    return false;
+  }
+  F factor = (F)1.0;
+  if (jr & EJ_SPECIAL) factor = (F)act_factor(S, S.ent_s[e], sim_t);
+  const F fmag = kl.x * (len - factor * kl.y);
+  const F scale = fmag / len;
+  const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
+  if (is_m2) {
+    fx -= (R)gx;
+    fy -= (R)gy;
+    fz -= (R)gz;
+  } else {
+    fx += (R)gx;
+    fy += (R)gy;
+    fz += (R)gz;
+  }
+  if (jr & EJ_SPECIAL) {
+    const int32_t s = S.ent_s[e];
+    const F thr = ((const F *)S.thr)[s];
+    const F mag = fmag >= (F)0.0 ? fmag : -fmag;
+    if (mag > thr) {
+      S.ent_j[e] = jr | EJ_DEAD;
+      if (!is_m2) {
+        S.s_alive[s] = 0;
+        S.ends[s] = make_int2(-1, -1);
+        count(S, 0);
+      }
+    }
+  }
+  return true;
+}
+
+// Fused step: deterministic gather of spring forces + mass integration.
+// FORCE_ONLY = engine.spring_pass alone: add the forces into f_ext.
+template <int P, bool FORCE_ONLY>
+__global__ void __launch_bounds__(256)
+    k_gather_step(const KState S, const EnvP E, const StepP T) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  if (!FORCE_ONLY && stopped(S, T.step)) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const R4 v = ((const R4 *)S.vel)[i];
+  const uint32_t fl = flags_of(v.w);
+  if (!(fl & MF_ALIVE)) return;
+  const R4 me = pos[i];
+  R fx = (R)0.0, fy = (R)0.0, fz = (R)0.0;
+  if (FORCE_ONLY || (fl & MF_FEXT)) {
+    const R4 f0 = ((const R4 *)S.fext)[i];
+    fx = f0.x;
+    fy = f0.y;
+    fz = f0.z;
+  }
+  const int64_t w = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t base = S.slice_ptr[w];
+  const int width = (int)((S.slice_ptr[w + 1] - base) >> 5);
+  const uint32_t *ej = S.ent_j + base + lane;
+  const F2 *ekl = (const F2 *)S.ent_kL0 + base + lane;
+#pragma unroll 2
+  for (int t = 0; t < width; t++) {
+    const uint32_t jr = __ldg(ej + 32 * t);
+    if (jr & EJ_DEAD) continue;
+    const F2 kl = __ldg(ekl + 32 * t);
+    const R4 o = pos[jr & EJ_MASK];
+    entry_force<P>(S, base + lane + 32 * (int64_t)t, jr, me, o, kl, T.sim_t,
+                   fx, fy, fz);
+  }
+  if (FORCE_ONLY) {
+    R4 f;
+    f.x = fx;
+    f.y = fy;
+    f.z = fz;
+    f.w = (R)0.0;
+    ((R4 *)S.fext)[i] = f;
+    R4 nv = v;
+    set_flags(nv.w, fl | MF_FEXT);
+    ((R4 *)S.vel)[i] = nv;
+    return;
+  }
+  if (fl & MF_FIXED) {
+    fixed_mass<P>(S, T, i, v, fl);
+    return;
+  }
+  if (fl & MF_FEXT) {
+    R4 z;
+    z.x = z.y = z.z = z.w = (R)0.0;
+    ((R4 *)S.fext)[i] = z;
+  }
+  integrate<P>(S, E, T, i, me, v, fl, fx, fy, fz);
+}
+
+// Atomic variant, spring side: one thread per spring slot (kernels.py:36-83
+// with the accumulation of the paper's GPU design).
+template <int P, bool SPECIAL>
+__global__ void __launch_bounds__(256)
+    k_spring_atomic(const KState S, const StepP T) {
+  using R = typename Tr<P>::R;
+  using F = typename Tr<P>::F;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S.s_n) return;
+  if (stopped(S, T.step)) return;
+  const int2 ab = S.ends[s];
+  if (ab.x < 0) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const R4 pa = pos[ab.x], pb = pos[ab.y];
+  const F2 kl = ((const F2 *)S.kL0)[s];
+  const F dx = (F)(pb.x - pa.x), dy = (F)(pb.y - pa.y), dz = (F)(pb.z - pa.z);
+  const F len = sqrt(dx * dx + dy * dy + dz * dz);
+  if (len == (F)0.0) {
+    if (!S.s_degen[s]) {
+      S.s_degen[s] = 1;
+      count(S, 2);
+    }
+    return;
+  }
+  F factor = (F)1.0;
+  bool special = false;
+  if (SPECIAL) {
+    special = S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+    if (S.mode[s] != 0) factor = (F)act_factor(S, s, T.sim_t);
+  }
+  const F fmag = kl.x * (len - factor * kl.y);
+  const F scale = fmag / len;
+  const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
+  R4 *fe = (R4 *)S.fext;
+  red_add(fe + ab.x, (R)gx, (R)gy, (R)gz);
+  red_add(fe + ab.y, -(R)gx, -(R)gy, -(R)gz);
+  if (SPECIAL && special) {
+    const F thr = ((const F *)S.thr)[s];
+    const F mag = fmag >= (F)0.0 ? fmag : -fmag;
+    if (mag > thr) {
+      S.s_alive[s] = 0;
+      S.ends[s] = make_int2(-1, -1);
+      if (S.e1) {  // incidence layout present: keep it consistent
+        if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
+        if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
+      }
+      count(S, 0);
+    }
+  }
+}
+
+// Standalone mass pass (engine.mass_pass; second half of the atomic step).
+template <int P>
+__global__ void __launch_bounds__(256)
+    k_mass(const KState S, const EnvP E, const StepP T) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  if (stopped(S, T.step)) return;
+  const R4 v = ((const R4 *)S.vel)[i];
+  const uint32_t fl = flags_of(v.w);
+  if (!(fl & MF_ALIVE)) return;
+  R4 *fe = (R4 *)S.fext + i;
+  const R4 f0 = *fe;
+  if (fl & MF_FIXED) {
+    fixed_mass<P>(S, T, i, v, fl | MF_FEXT);
+    return;
+  }
+  R4 z;
+  z.x = z.y = z.z = z.w = (R)0.0;
+  *fe = z;
+  const R4 me = ((const R4 *)S.pos[T.cur])[i];
+  integrate<P>(S, E, T, i, me, v, fl, f0.x, f0.y, f0.z);
+}
+
+inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+// Host-side launchers, one set per precision (defined in sl_kernels_*.cu).
+struct Launch {
+  void (*gather)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  void (*force_only)(const KState &, const EnvP &, const StepP &,
+                     cudaStream_t);
+  void (*spring_atomic)(const KState &, const StepP &, bool special,
+                        cudaStream_t);
+  void (*mass)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+};
+
+const Launch &launchers(int prec);
+
+}  // namespace sl

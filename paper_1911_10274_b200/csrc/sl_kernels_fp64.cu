@@ -1,0 +1,5 @@
+// fp64 parity kernels.  Build flag -fmad=false: no FMA contraction, so each
+// multiply/add rounds exactly like the reference's numba code (kernels.py,
+// compiled without fastmath).
+#include "sl_kernels_inst.cuh"
+SL_DEFINE_LAUNCHERS(PREC_FP64, launch_fp64)

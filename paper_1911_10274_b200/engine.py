@@ -1,0 +1,478 @@
+"""Integration engine: the drop-in for the reference's engine module.
+
+Reference: /root/reference/pkg/src/softlat/engine.py.  The public functions
+keep their names and signatures (``StepConfig``, ``spring_pass``,
+``mass_pass``, ``step``, ``throughput``, diagnostics); the dispatch that
+selected numba kernels (engine.py:177-200, 246-250) now drives
+libsoftlat_cuda through the C ABI.  ``BACKENDS`` is ``("cuda",)``: there is
+no CPU fallback.
+
+Accumulation modes (StepConfig.accumulation):
+
+* ``"linearizable"`` (default) / ``"slotted"`` / ``"gather"`` -- the
+  deterministic per-mass gather in ascending spring-slot order.  In fp64 it
+  is bit-identical to the reference's serial backend (which is what both
+  reference modes compute when run serially, test_engine.py:336-342).
+* ``"atomic"`` -- the paper's design (one thread per spring, vector atomics
+  into f_ext): order-dependent rounding, tolerance-only.
+
+Precision (StepConfig.precision): ``"fp64"`` (parity), ``"fp32"``,
+``"mixed"`` (fp64 mass state, fp32 spring math).
+
+Host arrays are authoritative between calls: ``spring_pass`` / ``mass_pass``
+/ ``step`` upload the store, run, and download (exactly the reference's
+per-call contract, for tests that poke the arrays between steps).
+``run_steps`` and the controller keep the state resident on the device for
+many steps and synchronise only at the ends.
+"""
+from __future__ import annotations
+
+import logging
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .actuation import actuation_factor
+from .core import Environment, Mass, Vec3
+from .errors import InvalidValueError, NumericalAbort
+from .store import ObjectStore
+
+log = logging.getLogger(__name__)
+
+V_STICK = 1e-6                       # engine.py:38
+KIND_DIRECTION = 1                   # kernels.py:24-25
+KIND_PLANE = 2
+
+ACCUMULATIONS = ("linearizable", "slotted", "gather", "atomic")
+BACKENDS = ("cuda",)
+PRECISIONS = ("fp64", "fp32", "mixed")
+
+
+@dataclass(frozen=True)
+class StepConfig:
+    """Timestep, accumulation, precision and device (engine.py:44-68)."""
+
+    dt: float
+    accumulation: str = "linearizable"
+    backend: str = "cuda"
+    workers: int | None = None       # accepted for API parity; unused
+    precision: str = "fp64"
+    device: int = 0
+    max_batch: int = 4096            # steps per device launch batch
+
+    def __post_init__(self):
+        if not (math.isfinite(self.dt) and self.dt > 0):
+            raise InvalidValueError(f"dt must be positive, got {self.dt}")
+        if self.accumulation not in ACCUMULATIONS:
+            raise InvalidValueError(
+                f"accumulation must be one of {ACCUMULATIONS}")
+        if self.backend not in BACKENDS:
+            raise InvalidValueError(
+                f"backend must be one of {BACKENDS} (no CPU fallback)")
+        if self.precision not in PRECISIONS:
+            raise InvalidValueError(f"precision must be one of {PRECISIONS}")
+        if self.workers is not None and self.workers < 1:
+            raise InvalidValueError("worker count must be >= 1")
+        if self.max_batch < 1:
+            raise InvalidValueError("max_batch must be >= 1")
+
+    @property
+    def native_accumulation(self) -> int:
+        return (_native.ACC_ATOMIC if self.accumulation == "atomic"
+                else _native.ACC_GATHER)
+
+
+# ----------------------------------------------------------- device mirror
+class DeviceMirror:
+    """The device-resident copy of one store (the analogue of the reference's
+    per-store engine cache, engine.py:71-102), keyed on the store's version
+    counters so springs / constraints are re-uploaded only when they change.
+    """
+
+    def __init__(self, device: int, precision: str):
+        self.ctx = _native.Context(device, precision)
+        self.counters = np.zeros(3, np.int64)
+        self._springs_key = None
+        self._constraints_key = None
+        self._custom_slots = np.zeros(0, np.int64)
+        self.degen_logged = np.zeros(0, np.bool_)
+
+    # host -> device
+    def push(self, store: ObjectStore, env: Environment | None,
+             masses: bool = True):
+        m, s = store.mass_slot_count, store.spring_slot_count
+        if masses or self.ctx.m_n != m:
+            self.ctx.upload_masses(
+                store._m_pos[:m], store._m_vel[:m], store._m_acc[:m],
+                store._m_fext[:m], store._m_load[:m], store._m_mass[:m],
+                store._m_fixed[:m], store._m_alive[:m], store._m_gen[:m])
+        key = (s, m, store.topology_version, store.spring_param_version,
+               id(store._s_m1))
+        if key != self._springs_key:
+            self.ctx.upload_springs(
+                store._s_m1[:s], store._s_m2[:s], store._s_m1gen[:s],
+                store._s_m2gen[:s], store._s_rest[:s], store._s_k[:s],
+                store._s_diam[:s], store._s_yield[:s], store._s_act_mode[:s],
+                store._s_act_amp[:s], store._s_act_freq[:s],
+                store._s_act_off[:s], store._s_act_per[:s],
+                store._s_alive[:s], store._s_degen[:s])
+            self._springs_key = key
+            self._custom_slots = np.array(
+                sorted(k for k in store._s_custom if k < s), dtype=np.int64)
+        ckey = (m, store.constraint_version, id(store._m_pos))
+        if ckey != self._constraints_key or masses:
+            lc_off, lc_kind, lc_vec = local_constraint_csr(store)
+            self.ctx.set_local_constraints(lc_off, lc_kind, lc_vec)
+            self._constraints_key = ckey
+        self.set_env(store, env or Environment())
+
+    def set_env(self, store: ObjectStore, env: Environment):
+        planes, balls = flatten_contacts(env)
+        gk, gv = global_constraint_arrays(store)
+        self.ctx.set_environment(env.gravity.as_array(), env.drag_coeff,
+                                 planes, balls, gk, gv, V_STICK)
+
+    @property
+    def has_custom(self) -> bool:
+        return len(self._custom_slots) > 0
+
+    def push_custom(self, store: ObjectStore, sim_t: float):
+        """engine._fill_custom_factors (engine.py:149-155): callables run on
+        the host, factors go to the device."""
+        slots = [int(x) for x in self._custom_slots
+                 if store._s_alive[x] and x in store._s_actuation]
+        if not slots:
+            return
+        f = [actuation_factor(store._s_actuation[x], sim_t) for x in slots]
+        self.ctx.set_custom_factors(np.array(slots, np.int64),
+                                    np.array(f, np.float64))
+
+    # device -> host
+    def pull(self, store: ObjectStore, springs: bool = True,
+             acc: bool = True, fext: bool = True):
+        m, s = store.mass_slot_count, store.spring_slot_count
+        self.ctx.download_masses(store._m_pos[:m], store._m_vel[:m],
+                                 store._m_acc[:m] if acc else None,
+                                 store._m_fext[:m] if fext else None)
+        if springs and s:
+            self.ctx.download_springs(store._s_alive[:s].view(np.uint8),
+                                      store._s_degen[:s].view(np.uint8))
+
+    def log_degenerate(self, store: ObjectStore):
+        """engine._log_degenerate (engine.py:205-215)."""
+        s = store.spring_slot_count
+        if len(self.degen_logged) < s:
+            grown = np.zeros(s, np.bool_)
+            grown[:len(self.degen_logged)] = self.degen_logged
+            self.degen_logged = grown
+        fresh = np.flatnonzero(store._s_degen[:s] & ~self.degen_logged[:s])
+        for slot in fresh.tolist():
+            log.warning("spring slot %d has zero length; contributing zero "
+                        "force", slot)
+        self.degen_logged[fresh] = True
+
+
+_mirrors: "weakref.WeakKeyDictionary[ObjectStore, dict]" = \
+    weakref.WeakKeyDictionary()
+
+
+def mirror_for(store: ObjectStore, cfg: StepConfig) -> DeviceMirror:
+    per = _mirrors.get(store)
+    if per is None:
+        per = {}
+        _mirrors[store] = per
+    key = (cfg.device, cfg.precision)
+    mir = per.get(key)
+    if mir is None:
+        mir = DeviceMirror(cfg.device, cfg.precision)
+        per[key] = mir
+    return mir
+
+
+def drop_mirrors(store: ObjectStore):
+    """Release the device buffers held for ``store``."""
+    per = _mirrors.pop(store, None)
+    for mir in (per or {}).values():
+        mir.ctx.close()
+
+
+# ---------------------------------------------------------------- helpers
+def flatten_contacts(env: Environment):
+    """planes [P,7] and balls [B,5] exactly as engine.py:223-236 packs
+    them."""
+    pl = env.planes()
+    planes = np.zeros((len(pl), 7))
+    for p, c in enumerate(pl):
+        planes[p] = (*c.normal.as_tuple(), c.offset, c.stiffness,
+                     c.static_friction, c.kinetic_friction)
+    bl = env.balls()
+    balls = np.zeros((len(bl), 5))
+    for b, c in enumerate(bl):
+        balls[b] = (*c.center.as_tuple(), c.radius, c.stiffness)
+    return planes, balls
+
+
+def _kind_code(c) -> int:
+    return KIND_DIRECTION if c.kind == "direction" else KIND_PLANE
+
+
+def global_constraint_arrays(store: ObjectStore):
+    gc = store.global_constraints
+    kinds = np.array([_kind_code(c) for c in gc], dtype=np.int8)
+    vecs = (np.array([c.vector.as_tuple() for c in gc], dtype=np.float64)
+            .reshape(-1, 3))
+    return kinds, vecs
+
+
+def local_constraint_csr(store: ObjectStore):
+    """Per-mass constraint CSR of engine._refresh_constraints
+    (engine.py:121-146)."""
+    m = store.mass_slot_count
+    off = np.zeros(m + 1, dtype=np.int64)
+    kinds, vecs = [], []
+    for slot in sorted(k for k in store._m_constraints if k < m):
+        cs = store._m_constraints[slot]
+        off[slot + 1] = len(cs)
+        for c in cs:
+            kinds.append(_kind_code(c))
+            vecs.append(c.vector.as_tuple())
+    np.cumsum(off, out=off)
+    return (off, np.array(kinds, dtype=np.int8),
+            np.array(vecs, dtype=np.float64).reshape(-1, 3))
+
+
+def _raise_abort(err_slot: int, sim_time: float | None = None):
+    slot = err_slot - 1
+    raise NumericalAbort(f"non-finite state on mass slot {slot}; "
+                         f"reduce dt or stiffness", mass_slot=slot,
+                         sim_time=sim_time)
+
+
+# -------------------------------------------------------- reference API
+def spring_pass(store: ObjectStore, sim_t: float, cfg: StepConfig) -> None:
+    """Spring forces of all alive springs added into f_ext
+    (engine.py:158-202)."""
+    mir = mirror_for(store, cfg)
+    mir.push(store, None)
+    if mir.has_custom:
+        mir.push_custom(store, sim_t)
+    mir.counters[:] = 0
+    mir.ctx.spring_pass(sim_t, cfg.native_accumulation, mir.counters)
+    m, s = store.mass_slot_count, store.spring_slot_count
+    mir.ctx.download_masses(None, None, None, store._m_fext[:m])
+    if s:
+        mir.ctx.download_springs(store._s_alive[:s].view(np.uint8),
+                                 store._s_degen[:s].view(np.uint8))
+    if mir.counters[2]:
+        mir.log_degenerate(store)
+
+
+def mass_pass(store: ObjectStore, env: Environment, cfg: StepConfig) -> None:
+    """Semi-implicit Euler of every alive non-fixed mass; clears f_ext
+    (engine.py:218-255)."""
+    mir = mirror_for(store, cfg)
+    mir.push(store, env)
+    err = mir.ctx.mass_pass(cfg.dt)
+    mir.pull(store, springs=False)
+    if err:
+        _raise_abort(err)
+
+
+def step(store: ObjectStore, env: Environment, sim_t: float,
+         cfg: StepConfig) -> float:
+    """One fused spring + mass step; returns sim_t + dt
+    (engine.py:258-264)."""
+    mir = mirror_for(store, cfg)
+    mir.push(store, env)
+    if mir.has_custom:
+        mir.push_custom(store, sim_t)
+    mir.counters[:] = 0
+    _, err = mir.ctx.step(np.array([sim_t]), cfg.dt, cfg.native_accumulation,
+                          mir.counters)
+    mir.pull(store, springs=bool(mir.counters[0] or mir.counters[1]
+                                 or mir.counters[2]))
+    if mir.counters[2]:
+        mir.log_degenerate(store)
+    if err:
+        _raise_abort(err)
+    return sim_t + cfg.dt
+
+
+def step_times(n: int, dt: float, t0: float = 0.0, time_rule: str =
+               "accumulate", step0: int = 0) -> np.ndarray:
+    """Sim time of each step: ``accumulate`` = repeated ``t += dt``
+    (tests/conftest.py:36-41); ``index`` = ``t0 + (step0+k)*dt``
+    (control.py:306-307)."""
+    if time_rule == "index":
+        return t0 + (step0 + np.arange(n, dtype=np.float64)) * dt
+    if time_rule != "accumulate":
+        raise InvalidValueError(f"unknown time rule {time_rule!r}")
+    out = np.empty(n, dtype=np.float64)
+    t = float(t0)
+    for k in range(n):
+        out[k] = t
+        t = t + dt
+    return out
+
+
+def run_steps(store: ObjectStore, env: Environment, cfg: StepConfig,
+              steps: int, t0: float = 0.0, time_rule: str = "accumulate",
+              step0: int = 0) -> float:
+    """``steps`` engine steps with the state resident on the device: one
+    upload, batched launches, one download.  Same trajectory as calling
+    ``step`` in a loop.  Returns the sim time after the last step."""
+    times = step_times(steps + 1, cfg.dt, t0, time_rule, step0)
+    mir = mirror_for(store, cfg)
+    mir.push(store, env)
+    counters = np.zeros(3, np.int64)
+    done = 0
+    err = 0
+    while done < steps and not err:
+        n = 1 if mir.has_custom else min(cfg.max_batch, steps - done)
+        if mir.has_custom:
+            mir.push_custom(store, float(times[done]))
+        k, err = mir.ctx.step(times[done:done + n], cfg.dt,
+                              cfg.native_accumulation, counters)
+        done += k
+    mir.pull(store, springs=bool(counters.any()))
+    if counters[2]:
+        mir.log_degenerate(store)
+    if err:
+        _raise_abort(err)
+    return float(times[steps]) if time_rule == "index" else \
+        float(times[steps])
+
+
+def throughput(springs: int, steps: int, wall_seconds: float) -> float:
+    """Spring updates per second (engine.py:267-271)."""
+    if wall_seconds <= 0:
+        raise InvalidValueError("wall_seconds must be positive")
+    return springs * steps / wall_seconds
+
+
+# --------------------------------------------- host diagnostics (numpy)
+def check_stability(store: ObjectStore, dt: float,
+                    env: Environment | None = None) -> float:
+    """dt*sqrt(k_max/m_min), contacts included; warns above 0.5
+    (engine.py:274-296)."""
+    ms = store.alive_mass_slots()
+    if len(ms) == 0:
+        return 0.0
+    ss = store.alive_spring_slots()
+    k_max = float(store._s_k[ss].max()) if len(ss) else 0.0
+    if env is not None:
+        for c in env.contacts:
+            k_max = max(k_max, c.stiffness)
+    if k_max == 0.0:
+        return 0.0
+    m_min = float(store._m_mass[ms].min())
+    ratio = dt * math.sqrt(k_max / m_min) if m_min > 0 else math.inf
+    if ratio > 0.5:
+        log.warning("dt*sqrt(k_max/m_min) = %.3g exceeds 0.5; integration "
+                    "may be unstable", ratio)
+    return ratio
+
+
+def contact_forces(mass: Mass, env: Environment) -> Vec3:
+    """Contact force on one mass, kernel semantics (engine.py:299-331)."""
+    f = mass.f_ext + env.gravity * mass.m - mass.vel * env.drag_coeff
+    total = Vec3.zero()
+    for pl in env.planes():
+        depth = pl.offset - mass.pos.dot(pl.normal)
+        if depth <= 0:
+            continue
+        nmag = pl.stiffness * depth
+        normal_force = pl.normal * nmag
+        f_now = f + total + normal_force
+        v_t = mass.vel - pl.normal * mass.vel.dot(pl.normal)
+        f_t = f_now - pl.normal * f_now.dot(pl.normal)
+        contrib = normal_force
+        tv, tf = v_t.norm(), f_t.norm()
+        if tv < V_STICK and tf <= pl.static_friction * nmag:
+            contrib = contrib - f_t
+        elif tv >= V_STICK:
+            contrib = contrib - v_t * (pl.kinetic_friction * nmag / tv)
+        elif tf > 0:
+            contrib = contrib - f_t * (pl.kinetic_friction * nmag / tf)
+        total = total + contrib
+    for bl in env.balls():
+        d = mass.pos - bl.center
+        dist = d.norm()
+        depth = bl.radius - dist
+        if depth > 0 and dist > 0:
+            total = total + d * (bl.stiffness * depth / dist)
+    return total
+
+
+def actuation_factors(store: ObjectStore, sim_t: float,
+                      slots: np.ndarray) -> np.ndarray:
+    """Vectorised rest-length factors (engine.py:334-352)."""
+    mode = store._s_act_mode[slots]
+    out = np.ones(len(slots))
+    periodic = (mode == 1) | (mode == 2)
+    if periodic.any():
+        sel = slots[periodic]
+        t = (sim_t - store._s_act_off[sel]) % store._s_act_per[sel]
+        f = 1.0 + store._s_act_amp[sel] * np.sin(store._s_act_freq[sel] * t)
+        quiet = (store._s_act_mode[sel] == 2) & (sim_t < store._s_act_off[sel])
+        out[periodic] = np.where(quiet, 1.0, f)
+    for idx in np.flatnonzero(mode == 3).tolist():
+        out[idx] = actuation_factor(store._s_actuation[int(slots[idx])],
+                                    sim_t)
+    return out
+
+
+@dataclass(frozen=True)
+class EnergyBreakdown:
+    kinetic: float
+    spring_potential: float
+    gravity_potential: float
+
+    @property
+    def total(self) -> float:
+        return self.kinetic + self.spring_potential + self.gravity_potential
+
+
+def mechanical_energy(store: ObjectStore, env: Environment,
+                      sim_t: float = 0.0) -> EnergyBreakdown:
+    """Kinetic + elastic + gravitational energy (engine.py:366-389)."""
+    m = store.alive_mass_slots()
+    ke = gpe = 0.0
+    if len(m):
+        mass = store._m_mass[m]
+        vel = store._m_vel[m]
+        ke = 0.5 * float(np.sum(mass * np.sum(vel * vel, axis=1)))
+        gpe = -float(np.sum(mass * (store._m_pos[m] @ env.gravity.as_array())))
+    s = store.alive_spring_slots()
+    spe = 0.0
+    if len(s):
+        d = store._m_pos[store._s_m2[s]] - store._m_pos[store._s_m1[s]]
+        lengths = np.linalg.norm(d, axis=1)
+        targets = actuation_factors(store, sim_t, s) * store._s_rest[s]
+        spe = 0.5 * float(np.sum(store._s_k[s] * (lengths - targets) ** 2))
+    return EnergyBreakdown(ke, spe, gpe)
+
+
+@dataclass(frozen=True)
+class SpringLoads:
+    slots: np.ndarray
+    lengths: np.ndarray
+    force_magnitudes: np.ndarray
+    stresses: np.ndarray
+
+
+def spring_loads(store: ObjectStore, sim_t: float = 0.0) -> SpringLoads:
+    """Per-spring |F| and stress (engine.py:402-412)."""
+    s = store.alive_spring_slots()
+    d = store._m_pos[store._s_m2[s]] - store._m_pos[store._s_m1[s]]
+    lengths = np.linalg.norm(d, axis=1)
+    targets = actuation_factors(store, sim_t, s) * store._s_rest[s]
+    fmag = np.abs(store._s_k[s] * (lengths - targets))
+    area = 0.25 * np.pi * store._s_diam[s] ** 2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        stress = np.where(area > 0, fmag / np.where(area > 0, area, 1.0),
+                          np.where(fmag > 0, np.inf, 0.0))
+    return SpringLoads(s, lengths, fmag, stress)
