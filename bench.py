@@ -84,10 +84,10 @@ def store_case(st, env):
             ("m_pos", "m_vel", "m_acc", "m_fext", "m_load", "m_mass",
              "m_fixed", "m_alive", "m_gen")}
     for k in ("s_m1", "s_m2", "s_m1gen", "s_m2gen", "s_rest", "s_k",
-              "s_diam", "s_yield", "s_amp", "s_freq", "s_off", "s_per",
-              "s_alive", "s_degen"):
+              "s_diam", "s_yield", "s_alive", "s_degen"):
         case[k] = getattr(st, "_" + k)[:s]
-    case["s_mode"] = st._s_act_mode[:s]
+    for k in ("mode", "amp", "freq", "off", "per"):
+        case["s_" + k] = getattr(st, "_s_act_" + k)[:s]
     planes, balls = engine.flatten_contacts(env)
     case.update(gravity=env.gravity.as_array(), drag=env.drag_coeff,
                 planes=planes, balls=balls)

@@ -113,6 +113,8 @@ struct Tr<PREC_FP64> {
   using F = double;
   using R4 = double4;
   using F2 = double2;
+  using M = double;  // force arithmetic
+  static constexpr int U = 4;  // gather batch (registers: 4 x 52 B)
 };
 template <>
 struct Tr<PREC_FP32> {
@@ -120,6 +122,8 @@ struct Tr<PREC_FP32> {
   using F = float;
   using R4 = float4;
   using F2 = float2;
+  using M = float;
+  static constexpr int U = 8;
 };
 template <>
 struct Tr<PREC_MIXED> {
@@ -127,6 +131,8 @@ struct Tr<PREC_MIXED> {
   using F = float;
   using R4 = double4;
   using F2 = float2;
+  using M = double;  // fp32 storage of (k, L0), fp64 force arithmetic
+  static constexpr int U = 6;
 };
 
 __device__ __forceinline__ uint32_t flags_of(float w) {
@@ -373,7 +379,7 @@ __device__ __forceinline__ bool entry_force(
     typename Tr<P>::R4 other, typename Tr<P>::F2 kl, double sim_t,
     typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
-  using F = typename Tr<P>::F;
+  using F = typename Tr<P>::M;
   const bool is_m2 = (jr & EJ_M2) != 0;
   // d = pos[m2] - pos[m1]
   F dx, dy, dz;
@@ -399,7 +405,7 @@ __device__ __forceinline__ bool entry_force(
   }
   F factor = (F)1.0;
   if (jr & EJ_SPECIAL) factor = (F)act_factor(S, S.ent_s[e], sim_t);
-  const F fmag = kl.x * (len - factor * kl.y);
+  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
   const F scale = fmag / len;
   const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
   if (is_m2) {
@@ -413,7 +419,7 @@ __device__ __forceinline__ bool entry_force(
   }
   if (jr & EJ_SPECIAL) {
     const int32_t s = S.ent_s[e];
-    const F thr = ((const F *)S.thr)[s];
+    const F thr = (F)((const typename Tr<P>::F *)S.thr)[s];
     const F mag = fmag >= (F)0.0 ? fmag : -fmag;
     if (mag > thr) {
       S.ent_j[e] = jr | EJ_DEAD;
@@ -452,18 +458,35 @@ __global__ void __launch_bounds__(256)
   }
   const int64_t w = i >> 5;
   const int lane = (int)(i & 31);
-  const int64_t base = S.slice_ptr[w];
-  const int width = (int)((S.slice_ptr[w + 1] - base) >> 5);
-  const uint32_t *ej = S.ent_j + base + lane;
-  const F2 *ekl = (const F2 *)S.ent_kL0 + base + lane;
-#pragma unroll 2
-  for (int t = 0; t < width; t++) {
-    const uint32_t jr = __ldg(ej + 32 * t);
-    if (jr & EJ_DEAD) continue;
-    const F2 kl = __ldg(ekl + 32 * t);
-    const R4 o = pos[jr & EJ_MASK];
-    entry_force<P>(S, base + lane + 32 * (int64_t)t, jr, me, o, kl, T.sim_t,
-                   fx, fy, fz);
+  const int64_t base = S.slice_ptr[w] + lane;
+  const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
+  const uint32_t *ej = S.ent_j + base;
+  const F2 *ekl = (const F2 *)S.ent_kL0 + base;
+  // Batches of U entries: issue every independent load of the batch (entry
+  // words, then (k, L0) and the neighbour positions) before consuming any,
+  // so each thread keeps U gathers in flight; accumulation then proceeds in
+  // ascending entry (= spring slot) order, preserving the serial sum order.
+  constexpr int U = Tr<P>::U;
+  for (int t0 = 0; t0 < width; t0 += U) {
+    uint32_t jr[U];
+    F2 kl[U];
+    R4 o[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      jr[u] = (t0 + u < width) ? __ldg(ej + 32 * (t0 + u)) : EJ_PAD;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (!(jr[u] & EJ_DEAD)) {
+        kl[u] = __ldg(ekl + 32 * (t0 + u));
+        o[u] = pos[jr[u] & EJ_MASK];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (!(jr[u] & EJ_DEAD))
+        entry_force<P>(S, base + 32 * (int64_t)(t0 + u), jr[u], me, o[u],
+                       kl[u], T.sim_t, fx, fy, fz);
+    }
   }
   if (FORCE_ONLY) {
     R4 f;
@@ -495,7 +518,8 @@ template <int P, bool SPECIAL>
 __global__ void __launch_bounds__(256)
     k_spring_atomic(const KState S, const StepP T) {
   using R = typename Tr<P>::R;
-  using F = typename Tr<P>::F;
+  using F = typename Tr<P>::M;
+  using FS = typename Tr<P>::F;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -518,17 +542,17 @@ __global__ void __launch_bounds__(256)
   F factor = (F)1.0;
   bool special = false;
   if (SPECIAL) {
-    special = S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+    special = S.mode[s] != 0 || ((const FS *)S.thr)[s] != (FS)CUDART_INF;
     if (S.mode[s] != 0) factor = (F)act_factor(S, s, T.sim_t);
   }
-  const F fmag = kl.x * (len - factor * kl.y);
+  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
   const F scale = fmag / len;
   const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
   R4 *fe = (R4 *)S.fext;
   red_add(fe + ab.x, (R)gx, (R)gy, (R)gz);
   red_add(fe + ab.y, -(R)gx, -(R)gy, -(R)gz);
   if (SPECIAL && special) {
-    const F thr = ((const F *)S.thr)[s];
+    const F thr = (F)((const FS *)S.thr)[s];
     const F mag = fmag >= (F)0.0 ? fmag : -fmag;
     if (mag > thr) {
       S.s_alive[s] = 0;

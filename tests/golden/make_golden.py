@@ -178,7 +178,7 @@ def main():
                         contacts=[ground(500.0, 0.6, 0.5)])
     save("lat3_contact_drag",
          lambda: lattice(3, corner=(0, 0, 0.01), stretch=1.05)[0],
-         env_c, 1e-4, 100, checkpoints=(1, 10))
+         env_c, 1e-4, 100, checkpoints=(1, 10, 100))
 
     # worm (pkg/scenarios/worm.ini / test_acceptance.py:297-326)
     def worm():
@@ -199,7 +199,7 @@ def main():
                 period=0.013, quiescent_before_offset=bool(i % 2)))
         return st
     save("actuated_quiescent", quiescent, Environment(gravity=g), 1e-4, 120,
-         checkpoints=(7,))
+         checkpoints=(7, 100))
 
     # yield breaking: nylon-like bars, stretched so some springs break
     nylon = Material(elastic_modulus=4.56e9, density=1150.0,
@@ -235,7 +235,7 @@ def main():
         ContactBall(center=Vec3(0.08, 0.08, 0.2), radius=0.12,
                     stiffness=400.0)])
     save("constraints_contacts", constrained, env_k, 1e-4, 150,
-         checkpoints=(1, 50))
+         checkpoints=(1, 50, 100))
 
     # topology edits: dead masses (lazy invalidation), deleted springs, LIFO
     # slot reuse, a degenerate (zero-length) spring
@@ -256,8 +256,8 @@ def main():
                                 stiffness=7.0, diameter=1e-3,
                                 yield_stress=1e3))
         return st
-    save("topology_edits", edited, Environment(gravity=g), 1e-4, 80,
-         checkpoints=(1,))
+    save("topology_edits", edited, Environment(gravity=g), 1e-4, 120,
+         checkpoints=(1, 100))
 
     # numerical abort (test_engine.py:160-168)
     def blowup():
