@@ -9,7 +9,9 @@
 // so a 12.7M-spring lattice re-indexes in milliseconds.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -85,6 +87,12 @@ struct sl_ctx {
   // incidence layout
   DevBuf slice_ptr, ent_j, ent_kL0, ent_s, e1, e2;
   int64_t n_slices = 0, n_entries = 0, alive_springs = 0, layout_builds = 0;
+  int64_t max_width = 0;     // widest slice (entries per mass, padded)
+  int tma_warps = 0;         // warps per CTA of the TMA kernel (0 = off)
+  int tma_grid = 0;
+  TmaCfg tma;
+  int sm_count = 0, smem_optin = 0;
+  bool tma_enabled = true;
   // scratch
   DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
   DevBuf status;
@@ -495,6 +503,26 @@ int ensure_springs(sl_ctx *c, int64_t s_n) {
   return SL_OK;
 }
 
+// Size the per-warp shared-memory rings of the TMA kernel for the widest
+// slice; one persistent CTA per SM with as many warps as fit.
+void configure_tma(sl_ctx *c) {
+  c->tma_warps = 0;
+  if (!c->tma_enabled || c->n_slices == 0 || c->max_width == 0) return;
+  const size_t f2 = 2 * c->fsz;
+  const size_t stage = (size_t)c->max_width * 32 * (4 + f2);
+  const size_t per_warp = 2 * stage + 16;
+  int warps = (int)std::min<size_t>(16, (size_t)c->smem_optin / per_warp);
+  if (warps < 2) return;  // hub masses: fall back to the plain kernel
+  c->tma.n_slices = c->n_slices;
+  c->tma.cap_w = (int)c->max_width;
+  c->tma.warps = warps;
+  c->tma.stage_bytes = (uint32_t)stage;
+  int64_t ctas = (c->n_slices + warps - 1) / warps;
+  c->tma_grid = (int)std::min<int64_t>(ctas, c->sm_count);
+  if (launchers(c->prec).tma_setup((int)(warps * per_warp)) != 0) return;
+  c->tma_warps = warps;
+}
+
 int build_layout(sl_ctx *c) {
   const int64_t m_n = c->m_n, s_n = c->s_n;
   if (m_n > (int64_t)EJ_MASK)
@@ -544,9 +572,24 @@ int build_layout(sl_ctx *c) {
                                    c->width.as<int64_t>(),
                                    c->slice_ptr.as<int64_t>(),
                                    (int)(n_slices + 1), c->st));
-  int64_t n_ent = 0;
+  int64_t n_ent = 0, max_ent = 0;
   CK(cudaMemcpyAsync(&n_ent, c->slice_ptr.as<int64_t>() + n_slices, 8,
                      cudaMemcpyDeviceToHost, c->st));
+  if (n_slices > 0) {
+    size_t rb = 0;
+    cub::DeviceReduce::Max(nullptr, rb, (int64_t *)nullptr,
+                           (int64_t *)nullptr, (int)n_slices);
+    if (rb > c->sort_tmp.bytes) {
+      CK(cudaStreamSynchronize(c->st));
+      CK(c->sort_tmp.ensure(rb));
+    }
+    rb = c->sort_tmp.bytes;
+    CK(cub::DeviceReduce::Max(c->sort_tmp.p, rb, c->width.as<int64_t>(),
+                              c->width.as<int64_t>() + n_slices,
+                              (int)n_slices, c->st));
+    CK(cudaMemcpyAsync(&max_ent, c->width.as<int64_t>() + n_slices, 8,
+                       cudaMemcpyDeviceToHost, c->st));
+  }
   CK(cudaStreamSynchronize(c->st));
   CK(c->ent_j.ensure(4 * n_ent));
   CK(c->ent_kL0.ensure(2 * c->fsz * n_ent));
@@ -579,6 +622,8 @@ int build_layout(sl_ctx *c) {
   CK(cudaStreamSynchronize(c->st));
   c->n_slices = n_slices;
   c->n_entries = n_ent;
+  c->max_width = max_ent / 32;
+  configure_tma(c);
   c->layout_valid = true;
   c->layout_builds++;
   c->launches += 5;
@@ -652,6 +697,7 @@ int sl_create(int device, int precision, sl_ctx **out) {
   c->prec = precision;
   c->rsz = precision == PREC_FP32 ? 4 : 8;
   c->fsz = precision == PREC_FP64 ? 8 : 4;
+  if (const char *ev = getenv("SL_DISABLE_TMA")) c->tma_enabled = ev[0] == '0';
   memset(&c->env, 0, sizeof c->env);
   cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
   if (e == cudaSuccess)
@@ -662,6 +708,13 @@ int sl_create(int device, int precision, sl_ctx **out) {
     e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount,
+                               device);
+  if (e == cudaSuccess)
+    e = cudaDeviceGetAttribute(&c->smem_optin,
+                               cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                               device);
   if (e == cudaSuccess) e = c->status.ensure(8 * 8);
   if (e == cudaSuccess)
     e = cudaMallocHost((void **)&c->h_status, 8 * 8);
@@ -1086,7 +1139,10 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     T.cur = (int)((c->cur + n) & 1);
     T.write_acc = n == n_steps - 1;
     if (accumulation == SL_ACC_GATHER) {
-      L.gather(S, c->env, T, c->st);
+      if (c->tma_warps)
+        L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
+      else
+        L.gather(S, c->env, T, c->st);
       c->launches++;
     } else {
       L.spring_atomic(S, T, c->has_special, c->st);

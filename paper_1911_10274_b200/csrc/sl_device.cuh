@@ -433,61 +433,56 @@ __device__ __forceinline__ bool entry_force(
   return true;
 }
 
-// Fused step: deterministic gather of spring forces + mass integration.
-// FORCE_ONLY = engine.spring_pass alone: add the forces into f_ext.
-template <int P, bool FORCE_ONLY>
-__global__ void __launch_bounds__(256)
-    k_gather_step(const KState S, const EnvP E, const StepP T) {
-  using R = typename Tr<P>::R;
+// Spring forces of one mass from its incidence list.  ej / ekl point at the
+// mass's first entry (lane-strided by 32: global memory or a shared-memory
+// stage); ebase is the global index of that entry (for side effects).
+// Batches of U entries: every independent load of a batch is issued before
+// any is consumed (U neighbour gathers in flight per thread), accumulation
+// then runs in ascending entry (= spring slot) order -- the serial order.
+template <int P, bool GLOBAL_SRC>
+__device__ __forceinline__ void gather_forces(
+    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::F2 *ekl, int width, int64_t ebase,
+    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= S.m_n) return;
-  if (!FORCE_ONLY && stopped(S, T.step)) return;
-  const R4 *pos = (const R4 *)S.pos[T.cur];
-  const R4 v = ((const R4 *)S.vel)[i];
-  const uint32_t fl = flags_of(v.w);
-  if (!(fl & MF_ALIVE)) return;
-  const R4 me = pos[i];
-  R fx = (R)0.0, fy = (R)0.0, fz = (R)0.0;
-  if (FORCE_ONLY || (fl & MF_FEXT)) {
-    const R4 f0 = ((const R4 *)S.fext)[i];
-    fx = f0.x;
-    fy = f0.y;
-    fz = f0.z;
-  }
-  const int64_t w = i >> 5;
-  const int lane = (int)(i & 31);
-  const int64_t base = S.slice_ptr[w] + lane;
-  const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
-  const uint32_t *ej = S.ent_j + base;
-  const F2 *ekl = (const F2 *)S.ent_kL0 + base;
-  // Batches of U entries: issue every independent load of the batch (entry
-  // words, then (k, L0) and the neighbour positions) before consuming any,
-  // so each thread keeps U gathers in flight; accumulation then proceeds in
-  // ascending entry (= spring slot) order, preserving the serial sum order.
   constexpr int U = Tr<P>::U;
   for (int t0 = 0; t0 < width; t0 += U) {
     uint32_t jr[U];
     F2 kl[U];
     R4 o[U];
 #pragma unroll
-    for (int u = 0; u < U; u++)
-      jr[u] = (t0 + u < width) ? __ldg(ej + 32 * (t0 + u)) : EJ_PAD;
+    for (int u = 0; u < U; u++) {
+      if (t0 + u < width)
+        jr[u] = GLOBAL_SRC ? __ldg(ej + 32 * (t0 + u)) : ej[32 * (t0 + u)];
+      else
+        jr[u] = EJ_PAD;
+    }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (!(jr[u] & EJ_DEAD)) {
-        kl[u] = __ldg(ekl + 32 * (t0 + u));
+        kl[u] = GLOBAL_SRC ? __ldg(ekl + 32 * (t0 + u)) : ekl[32 * (t0 + u)];
         o[u] = pos[jr[u] & EJ_MASK];
       }
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (!(jr[u] & EJ_DEAD))
-        entry_force<P>(S, base + 32 * (int64_t)(t0 + u), jr[u], me, o[u],
-                       kl[u], T.sim_t, fx, fy, fz);
+        entry_force<P>(S, ebase + 32 * (int64_t)(t0 + u), jr[u], me, o[u],
+                       kl[u], sim_t, fx, fy, fz);
     }
   }
+}
+
+// Tail of a mass update after its spring forces are known.
+template <int P, bool FORCE_ONLY>
+__device__ __forceinline__ void finish_mass(
+    const KState &S, const EnvP &E, const StepP &T, int64_t i,
+    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
+    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
   if (FORCE_ONLY) {
     R4 f;
     f.x = fx;
@@ -510,6 +505,172 @@ __global__ void __launch_bounds__(256)
     ((R4 *)S.fext)[i] = z;
   }
   integrate<P>(S, E, T, i, me, v, fl, fx, fy, fz);
+}
+
+template <int P>
+__device__ __forceinline__ void initial_force(const KState &S, int64_t i,
+                                              uint32_t fl, bool force_only,
+                                              typename Tr<P>::R &fx,
+                                              typename Tr<P>::R &fy,
+                                              typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  fx = fy = fz = (R)0.0;
+  if (force_only || (fl & MF_FEXT)) {
+    const R4 f0 = ((const R4 *)S.fext)[i];
+    fx = f0.x;
+    fy = f0.y;
+    fz = f0.z;
+  }
+}
+
+// Fused step, plain variant: one thread per mass, entries read straight
+// from global memory.  Used for spring_pass (FORCE_ONLY), for tiny bodies
+// and for layouts with very wide slices (hub masses).
+template <int P, bool FORCE_ONLY>
+__global__ void __launch_bounds__(256)
+    k_gather_step(const KState S, const EnvP E, const StepP T) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  if (!FORCE_ONLY && stopped(S, T.step)) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const R4 v = ((const R4 *)S.vel)[i];
+  const uint32_t fl = flags_of(v.w);
+  if (!(fl & MF_ALIVE)) return;
+  const R4 me = pos[i];
+  R fx, fy, fz;
+  initial_force<P>(S, i, fl, FORCE_ONLY, fx, fy, fz);
+  const int64_t w = i >> 5;
+  const int64_t ebase = S.slice_ptr[w] + (i & 31);
+  const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
+  gather_forces<P, true>(S, pos, S.ent_j + ebase,
+                         (const F2 *)S.ent_kL0 + ebase, width, ebase, me,
+                         T.sim_t, fx, fy, fz);
+  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
+}
+
+// ---------------------------------------------------------------------------
+// TMA-pipelined fused step (the production path).
+//
+// Persistent CTAs; every warp owns a strided sequence of 32-mass slices and
+// a private 2-stage shared-memory ring.  Lane 0 streams the NEXT slice's
+// incidence list (entry words + (k, L0)) from HBM into the free stage with
+// two 1-D bulk async copies (cp.async.bulk -> UBLKCP, completion counted on
+// an mbarrier) while the warp computes the current slice out of the other
+// stage.  The HBM stream is thereby decoupled from the dependent neighbour
+// gathers (which hit L2), and the bytes in flight per SM are bounded only by
+// the ring size, not by registers.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
+                                         uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+struct TmaCfg {
+  int64_t n_slices;
+  int cap_w;        // max slice width the stages hold
+  int warps;        // warps per CTA
+  uint32_t stage_bytes;  // bytes of one stage (j words + kL0 pairs)
+};
+
+template <int P>
+__global__ void __launch_bounds__(512)
+    k_gather_tma(const KState S, const EnvP E, const StepP T,
+                 const TmaCfg C) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  if (stopped(S, T.step)) return;  // uniform across the grid
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *ring = smem + (size_t)warp * 2 * C.stage_bytes;
+  uint64_t *bars =
+      (uint64_t *)(smem + (size_t)C.warps * 2 * C.stage_bytes) + 2 * warp;
+  const uint32_t jbytes_cap = (uint32_t)C.cap_w * 128u;
+  if (lane == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  const int64_t stride = (int64_t)gridDim.x * C.warps;
+  int64_t s = (int64_t)blockIdx.x * C.warps + warp;
+  auto issue = [&](int64_t sl, int stage) {
+    const int64_t e0 = S.slice_ptr[sl];
+    const uint32_t n = (uint32_t)(S.slice_ptr[sl + 1] - e0);  // entries
+    unsigned char *dst = ring + (size_t)stage * C.stage_bytes;
+    mbar_expect_tx(bars + stage, n * (uint32_t)(4 + sizeof(F2)));
+    if (n) {
+      bulk_g2s(dst, S.ent_j + e0, n * 4u, bars + stage);
+      bulk_g2s(dst + jbytes_cap, (const F2 *)S.ent_kL0 + e0,
+               n * (uint32_t)sizeof(F2), bars + stage);
+    }
+  };
+  if (lane == 0 && s < C.n_slices) issue(s, 0);
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  for (int k = 0; s < C.n_slices; s += stride, k++) {
+    const int stage = k & 1;
+    if (lane == 0 && s + stride < C.n_slices) {
+      fence_proxy_async();  // prior generic reads of that stage are done
+      issue(s + stride, stage ^ 1);
+    }
+    const int64_t i = s * 32 + lane;
+    const int64_t e0 = S.slice_ptr[s];
+    const int width = (int)((S.slice_ptr[s + 1] - e0) >> 5);
+    R4 v, me;
+    uint32_t fl = 0;
+    if (i < S.m_n) {
+      v = ((const R4 *)S.vel)[i];
+      me = pos[i];
+      fl = flags_of(v.w);
+    }
+    mbar_wait(bars + stage, (uint32_t)((k >> 1) & 1));
+    if (fl & MF_ALIVE) {
+      const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
+      R fx, fy, fz;
+      initial_force<P>(S, i, fl, false, fx, fy, fz);
+      gather_forces<P, false>(S, pos, (const uint32_t *)st + lane,
+                              (const F2 *)(st + jbytes_cap) + lane, width,
+                              e0 + lane, me, T.sim_t, fx, fy, fz);
+      finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+    }
+    __syncwarp();
+  }
 }
 
 // Atomic variant, spring side: one thread per spring slot (kernels.py:36-83
@@ -596,6 +757,9 @@ inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
 // Host-side launchers, one set per precision (defined in sl_kernels_*.cu).
 struct Launch {
   void (*gather)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  void (*gather_tma)(const KState &, const EnvP &, const StepP &,
+                     const TmaCfg &, int grid, cudaStream_t);
+  int (*tma_setup)(int smem_bytes);  // opt into large dynamic smem
   void (*force_only)(const KState &, const EnvP &, const StepP &,
                      cudaStream_t);
   void (*spring_atomic)(const KState &, const StepP &, bool special,

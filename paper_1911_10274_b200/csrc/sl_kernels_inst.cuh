@@ -12,6 +12,16 @@
                    cudaStream_t st) {                                        \
     if (S.m_n > 0) k_gather_step<PREC, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
   }                                                                          \
+  void FN##_tma(const KState &S, const EnvP &E, const StepP &T,             \
+               const TmaCfg &C, int grid, cudaStream_t st) {                 \
+    size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);                  \
+    k_gather_tma<PREC><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);          \
+  }                                                                          \
+  int FN##_tma_setup(int smem_bytes) {                                       \
+    return (int)cudaFuncSetAttribute(k_gather_tma<PREC>,                     \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     smem_bytes);                            \
+  }                                                                          \
   void FN##_force(const KState &S, const EnvP &E, const StepP &T,            \
                   cudaStream_t st) {                                         \
     if (S.m_n > 0) k_gather_step<PREC, true><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
@@ -30,7 +40,8 @@
   }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \
-    static const Launch L = {FN##_gather, FN##_force, FN##_spring, FN##_mass}; \
+    static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
+                             FN##_force, FN##_spring, FN##_mass};           \
     return L;                                                                \
   }                                                                          \
   }
