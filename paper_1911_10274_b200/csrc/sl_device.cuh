@@ -392,8 +392,8 @@ __device__ __forceinline__ bool entry_force(
     dy = (F)(other.y - me.y);
     dz = (F)(other.z - me.z);
   }
-  const F len = sqrt(dx * dx + dy * dy + dz * dz);
-  if (len == (F)0.0) {
+  const F len2 = dx * dx + dy * dy + dz * dz;
+  if (len2 == (F)0.0) {  // <=> sqrt(len2) == 0, kernels.py:50
     if (!is_m2) {
       const int32_t s = S.ent_s[e];
       if (!S.s_degen[s]) {
@@ -405,18 +405,31 @@ __device__ __forceinline__ bool entry_force(
   }
   F factor = (F)1.0;
   if (jr & EJ_SPECIAL) factor = (F)act_factor(S, S.ent_s[e], sim_t);
-  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
-  const F scale = fmag / len;
-  const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
-  if (is_m2) {
-    fx -= (R)gx;
-    fy -= (R)gy;
-    fz -= (R)gz;
+  F len, inv;  // |d| and the factor turning fmag into fmag/|d|
+  if constexpr (P == PREC_FP64) {
+    // parity mode: IEEE sqrt and a true division, as the reference
+    len = sqrt(len2);
+  } else if constexpr (P == PREC_FP32) {
+    // tolerance mode: one MUFU.RSQ replaces sqrt + divide
+    inv = rsqrtf(len2);
+    len = len2 * inv;
   } else {
-    fx += (R)gx;
-    fy += (R)gy;
-    fz += (R)gz;
+    // mixed: float rsqrt seed + one fp64 Newton step (~1e-14 relative)
+    double r = (double)rsqrtf((float)len2);
+    r = r * (1.5 - 0.5 * len2 * r * r);
+    inv = r;
+    len = len2 * r;
   }
+  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
+  F scale;
+  if constexpr (P == PREC_FP64)
+    scale = fmag / len;
+  else
+    scale = fmag * inv;
+  if (is_m2) scale = -scale;  // -(s*d) == (-s)*d exactly; f - g == f + (-g)
+  fx += (R)(scale * dx);
+  fy += (R)(scale * dy);
+  fz += (R)(scale * dz);
   if (jr & EJ_SPECIAL) {
     const int32_t s = S.ent_s[e];
     const F thr = (F)((const typename Tr<P>::F *)S.thr)[s];
