@@ -28,7 +28,9 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
           "-I", INCLUDE, "-I", CSRC]
 UNITS = {
     "sl_kernels_fp64.cu": ["-fmad=false"],
-    "sl_kernels_fp32.cu": [],
+    # tolerance modes: flush denormals (keeps MUFU.RSQ free of the
+    # denormal-rescaling sequence); IEEE divide/sqrt are not used there
+    "sl_kernels_fp32.cu": ["-ftz=true"],
     "sl_api.cu": [],
 }
 

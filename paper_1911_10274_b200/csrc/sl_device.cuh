@@ -452,8 +452,9 @@ __device__ __forceinline__ bool entry_force(
 // Batches of U entries: every independent load of a batch is issued before
 // any is consumed (U neighbour gathers in flight per thread), accumulation
 // then runs in ascending entry (= spring slot) order -- the serial order.
+// This exact path serves fp64 parity mode.
 template <int P, bool GLOBAL_SRC>
-__device__ __forceinline__ void gather_forces(
+__device__ __forceinline__ void gather_forces_exact(
     const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
     const typename Tr<P>::F2 *ekl, int width, int64_t ebase,
     typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
@@ -486,6 +487,95 @@ __device__ __forceinline__ void gather_forces(
                        kl[u], sim_t, fx, fy, fz);
     }
   }
+}
+
+// Tolerance modes (fp32 / mixed): branch-free main loop.  The endpoint
+// orientation cancels -- the force on this mass is
+// k(|d| - L0)/|d| * (p_other - p_me) for either endpoint -- so no sign
+// logic is needed; dead, special (actuated / finite-yield) and zero-length
+// entries contribute 0 here and are handled afterwards by the exact
+// per-entry code (rare).  Order of accumulation stays fixed, so results are
+// deterministic run to run.
+template <int P, bool GLOBAL_SRC>
+__device__ __forceinline__ void gather_forces_fast(
+    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::F2 *ekl, int width, int64_t ebase, int64_t self,
+    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using M = typename Tr<P>::M;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  constexpr int U = Tr<P>::U;
+  bool odd = false;
+  for (int t0 = 0; t0 < width; t0 += U) {
+    uint32_t jr[U];
+    F2 kl[U];
+    R4 o[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const bool in = t0 + u < width;
+      const int t = in ? t0 + u : 0;
+      jr[u] = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
+      kl[u] = GLOBAL_SRC ? __ldg(ekl + 32 * t) : ekl[32 * t];
+      if (!in) jr[u] = EJ_PAD;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = (jr[u] & EJ_DEAD) ? self : (int64_t)(jr[u] & EJ_MASK);
+      o[u] = pos[j];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const M dx = (M)(o[u].x - me.x), dy = (M)(o[u].y - me.y),
+              dz = (M)(o[u].z - me.z);
+      const M len2 = dx * dx + dy * dy + dz * dz;
+      const bool plain = !(jr[u] & (EJ_DEAD | EJ_SPECIAL)) && len2 > (M)0;
+      odd |= (jr[u] & (EJ_DEAD | EJ_SPECIAL)) == EJ_SPECIAL || len2 == (M)0;
+      M r;
+      if constexpr (P == PREC_FP32) {
+        r = rsqrtf(plain ? len2 : 1.0f);
+      } else {
+        const double l2 = plain ? (double)len2 : 1.0;
+        r = (double)rsqrtf((float)l2);
+        r = r * (1.5 - 0.5 * l2 * r * r);
+      }
+      const M fmag = (M)kl[u].x * (len2 * r - (M)kl[u].y);
+      const M sc = plain ? fmag * r : (M)0;
+      fx += (R)(sc * dx);
+      fy += (R)(sc * dy);
+      fz += (R)(sc * dz);
+    }
+  }
+  if (odd) {
+    // rare: actuated / breakable / zero-length entries, exact semantics
+    for (int t = 0; t < width; t++) {
+      const uint32_t jr = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
+      if (jr & EJ_DEAD) continue;
+      const R4 o = pos[jr & EJ_MASK];
+      const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y),
+              dz = (M)(o.z - me.z);
+      const M len2 = dx * dx + dy * dy + dz * dz;
+      if (!(jr & EJ_SPECIAL) && len2 > (M)0) continue;  // done above
+      const F2 kl = GLOBAL_SRC ? __ldg(ekl + 32 * t) : ekl[32 * t];
+      entry_force<P>(S, ebase + 32 * (int64_t)t, jr, me, o, kl, sim_t, fx,
+                     fy, fz);
+    }
+  }
+}
+
+template <int P, bool GLOBAL_SRC>
+__device__ __forceinline__ void gather_forces(
+    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::F2 *ekl, int width, int64_t ebase, int64_t self,
+    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+  if constexpr (P == PREC_FP64)
+    gather_forces_exact<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, me,
+                                       sim_t, fx, fy, fz);
+  else
+    gather_forces_fast<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, self,
+                                      me, sim_t, fx, fy, fz);
 }
 
 // Tail of a mass update after its spring forces are known.
@@ -560,7 +650,7 @@ __global__ void __launch_bounds__(256)
   const int64_t ebase = S.slice_ptr[w] + (i & 31);
   const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
   gather_forces<P, true>(S, pos, S.ent_j + ebase,
-                         (const F2 *)S.ent_kL0 + ebase, width, ebase, me,
+                         (const F2 *)S.ent_kL0 + ebase, width, ebase, i, me,
                          T.sim_t, fx, fy, fz);
   finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
 }
@@ -679,7 +769,7 @@ __global__ void __launch_bounds__(512)
       initial_force<P>(S, i, fl, false, fx, fy, fz);
       gather_forces<P, false>(S, pos, (const uint32_t *)st + lane,
                               (const F2 *)(st + jbytes_cap) + lane, width,
-                              e0 + lane, me, T.sim_t, fx, fy, fz);
+                              e0 + lane, i, me, T.sim_t, fx, fy, fz);
       finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
     }
     __syncwarp();
