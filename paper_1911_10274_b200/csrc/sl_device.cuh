@@ -531,7 +531,8 @@ __device__ __forceinline__ void gather_forces_fast(
               dz = (M)(o[u].z - me.z);
       const M len2 = dx * dx + dy * dy + dz * dz;
       const bool plain = !(jr[u] & (EJ_DEAD | EJ_SPECIAL)) && len2 > (M)0;
-      odd |= (jr[u] & (EJ_DEAD | EJ_SPECIAL)) == EJ_SPECIAL || len2 == (M)0;
+      odd |= !(jr[u] & EJ_DEAD) &&
+             ((jr[u] & EJ_SPECIAL) || len2 == (M)0);
       M r;
       if constexpr (P == PREC_FP32) {
         r = rsqrtf(plain ? len2 : 1.0f);
