@@ -79,7 +79,7 @@ struct sl_ctx {
   bool layout_valid = false, validate_dirty = true, has_special = false;
   bool snap_pending = false;
   // mass SoA
-  DevBuf pos[2], vel, acc, fext, load, m_gen, m_alive;
+  DevBuf pos[2], vel, acc, fext, load, m_gen, m_alive, xflags;
   DevBuf lc_off, lc_kind, lc_vec;
   bool has_lc = false;
   // spring SoA
@@ -146,7 +146,7 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
                               const int64_t *slots, void *pos0, void *pos1,
                               void *velo, void *acco, void *fexto,
                               void *loado, int64_t *gen_o, uint8_t *alive_o,
-                              const int64_t *gen_in) {
+                              const int64_t *gen_in, const uint8_t *xflags) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -176,6 +176,7 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
   v.z = (R)vel[3 * r + 2];
   // keep an existing local-constraint flag (set by sl_set_local_constraints)
   if (slots) fl |= flags_of(((R4 *)velo)[i].w) & MF_LC;
+  if (xflags && xflags[i]) fl |= MF_SPECIAL;  // layout-derived, still valid
   set_flags(v.w, fl);
   ((R4 *)velo)[i] = v;
   R *a = (R *)acco + 3 * i;
@@ -247,6 +248,19 @@ __global__ void k_set_lc_flags(int64_t n, const int64_t *lc_off, void *velb,
   }
 }
 
+__global__ void k_clear_flag(int64_t n, void *velb, int is_double,
+                             uint32_t bit) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (is_double) {
+    double4 *v = (double4 *)velb + i;
+    set_flags(v->w, flags_of(v->w) & ~bit);
+  } else {
+    float4 *v = (float4 *)velb + i;
+    set_flags(v->w, flags_of(v->w) & ~bit);
+  }
+}
+
 __global__ void k_set_fext_flags(int64_t n, void *velb, int is_double) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -305,6 +319,14 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
   } else if (layout_valid) {
     // keep the incidence copies of (k, L0) and the special bit in sync
     bool special = mode[r] != 0 || yield[r] != CUDART_INF;
+    int2 ab = S.ends[s];
+    if (special && ab.x >= 0) {
+      using R4 = typename Tr<P>::R4;
+      S.xflags[ab.x] = 1;
+      S.xflags[ab.y] = 1;
+      or_flags((R4 *)S.vel + ab.x, MF_SPECIAL);
+      or_flags((R4 *)S.vel + ab.y, MF_SPECIAL);
+    }
     int64_t es[2] = {S.e1[s], S.e2[s]};
     for (int q = 0; q < 2; q++) {
       int64_t e = es[q];
@@ -422,6 +444,10 @@ __global__ void k_fill_layout(int64_t n, const uint32_t *keys,
   bool special =
       S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
   ent_j[e] = other | (side ? EJ_M2 : 0u) | (special ? EJ_SPECIAL : 0u);
+  if (special) {
+    S.xflags[i] = 1;
+    or_flags((typename Tr<P>::R4 *)S.vel + i, MF_SPECIAL);
+  }
   ((F2 *)ent_kl)[e] = ((const F2 *)S.kL0)[s];
   ent_s[e] = (int32_t)s;
   (side ? e2 : e1)[s] = e;
@@ -456,6 +482,7 @@ KState make_state(sl_ctx *c) {
   S.e1 = c->layout_valid ? c->e1.as<int64_t>() : nullptr;
   S.e2 = c->layout_valid ? c->e2.as<int64_t>() : nullptr;
   S.status = c->status.as<unsigned long long>();
+  S.xflags = c->xflags.as<uint8_t>();
   return S;
 }
 
@@ -486,6 +513,7 @@ int ensure_masses(sl_ctx *c, int64_t m_n) {
   CK(c->load.ensure(3 * c->rsz * m_n));
   CK(c->m_gen.ensure(8 * m_n));
   CK(c->m_alive.ensure(m_n));
+  CK(c->xflags.ensure(m_n + 1));
   return SL_OK;
 }
 
@@ -595,6 +623,12 @@ int build_layout(sl_ctx *c) {
   CK(c->ent_kL0.ensure(2 * c->fsz * n_ent));
   CK(c->ent_s.ensure(4 * n_ent));
   CK(cudaMemsetAsync(c->ent_j.p, 0xFF, 4 * n_ent, c->st));
+  CK(cudaMemsetAsync(c->xflags.p, 0, m_n + 1, c->st));
+  if (m_n > 0) {
+    k_clear_flag<<<blocks_for(m_n), 256, 0, c->st>>>(m_n, c->vel.p,
+                                                      c->rsz == 8, MF_SPECIAL);
+    CKL();
+  }
   CK(cudaMemsetAsync(c->ent_s.p, 0xFF, 4 * n_ent, c->st));
   if (n_rec > 0) {
     tmp_bytes = c->sort_tmp.bytes;
@@ -734,7 +768,7 @@ int sl_destroy(sl_ctx *c) {
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->side) cudaStreamSynchronize(c->side);
   DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc, &c->fext,
-                    &c->load, &c->m_gen, &c->m_alive, &c->lc_off,
+                    &c->load, &c->m_gen, &c->m_alive, &c->xflags, &c->lc_off,
                     &c->lc_kind, &c->lc_vec, &c->ends, &c->kL0, &c->s_alive,
                     &c->s_degen, &c->mode, &c->act, &c->thr, &c->custom,
                     &c->m1gen, &c->m2gen, &c->slice_ptr, &c->ent_j,
@@ -829,7 +863,9 @@ int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
     k<<<blocks_for(m_n), 256, 0, c->st>>>(
         m_n, dp, dv, da, df, dl, dm, dfx, dal, nullptr, c->pos[0].p,
         c->pos[1].p, c->vel.p, c->acc.p, c->fext.p, c->load.p,
-        c->m_gen.as<int64_t>(), c->m_alive.as<uint8_t>(), dg);
+        c->m_gen.as<int64_t>(), c->m_alive.as<uint8_t>(), dg,
+        (c->layout_valid && m_n == c->m_n) ? c->xflags.as<uint8_t>()
+                                           : nullptr);
     CKL();
     c->launches++;
     if (c->has_lc) {
@@ -1019,7 +1055,8 @@ int sl_write_masses(sl_ctx *c, int64_t n, const int64_t *slots,
   k<<<blocks_for(n), 256, 0, c->st>>>(
       n, dp, dv, da, df, dl, dm, dfx, dal, ds, c->pos[0].p, c->pos[1].p,
       c->vel.p, c->acc.p, c->fext.p, c->load.p, c->m_gen.as<int64_t>(),
-      c->m_alive.as<uint8_t>(), dg);
+      c->m_alive.as<uint8_t>(), dg,
+      c->layout_valid ? c->xflags.as<uint8_t>() : nullptr);
   CKL();
   c->launches++;
   CK(cudaStreamSynchronize(c->st));

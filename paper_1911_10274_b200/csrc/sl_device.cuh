@@ -41,6 +41,7 @@ enum : uint32_t {
   MF_LC = 4u,     // has local constraints (CSR lookup needed)
   MF_LOAD = 8u,   // persistent load has non-zero bits
   MF_FEXT = 16u,  // f_ext accumulator has non-zero bits at step start
+  MF_SPECIAL = 32u,  // has actuated / breakable springs (exact entry path)
 };
 
 // incidence entry word: low 29 bits other endpoint
@@ -93,6 +94,7 @@ struct KState {
   const void *ent_kL0;  // F2
   const int32_t *ent_s;
   const int64_t *e1, *e2;
+  uint8_t *xflags;  // per-mass layout-derived flag bits (MF_SPECIAL)
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -146,6 +148,13 @@ __device__ __forceinline__ void set_flags(float &w, uint32_t f) {
 }
 __device__ __forceinline__ void set_flags(double &w, uint32_t f) {
   w = __longlong_as_double((long long)f);
+}
+// atomically OR flag bits into vel[i].w (flags live in the low 32 bits)
+__device__ __forceinline__ void or_flags(float4 *v, uint32_t f) {
+  atomicOr((unsigned int *)&v->w, f);
+}
+__device__ __forceinline__ void or_flags(double4 *v, uint32_t f) {
+  atomicOr((unsigned int *)&v->w, f);
 }
 
 // Python float % (CPython float_rem, which numba follows; kernels.py:58).
@@ -461,7 +470,9 @@ __device__ __forceinline__ void gather_forces_exact(
     typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
-  constexpr int U = Tr<P>::U;
+  // fp64 parity mode runs everything here; in the tolerance modes only
+  // masses with actuated / breakable springs do -- keep it register-light
+  constexpr int U = P == PREC_FP64 ? Tr<P>::U : 2;
   for (int t0 = 0; t0 < width; t0 += U) {
     uint32_t jr[U];
     F2 kl[U];
@@ -489,78 +500,88 @@ __device__ __forceinline__ void gather_forces_exact(
   }
 }
 
-// Tolerance modes (fp32 / mixed): branch-free main loop.  The endpoint
-// orientation cancels -- the force on this mass is
-// k(|d| - L0)/|d| * (p_other - p_me) for either endpoint -- so no sign
-// logic is needed; dead, special (actuated / finite-yield) and zero-length
-// entries contribute 0 here and are handled afterwards by the exact
-// per-entry code (rare).  Order of accumulation stays fixed, so results are
-// deterministic run to run.
+// Tolerance modes (fp32 / mixed), masses without actuated / breakable
+// springs: branch-free loop.  The endpoint orientation cancels -- the force
+// on this mass is k(|d| - L0)/|d| * (p_other - p_me) for either endpoint --
+// so no sign logic is needed.  Dead / padding entries gather this mass's own
+// position (|d| = 0) and are zeroed by a select; an alive zero-length spring
+// (also |d| = 0, force 0) only needs its flag side effect, detected as
+// "|d| == 0 xor dead" and replayed afterwards.  Accumulation order is fixed
+// (deterministic run to run).  Returns true if a zero-length spring was seen.
 template <int P, bool GLOBAL_SRC>
-__device__ __forceinline__ void gather_forces_fast(
-    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
-    const typename Tr<P>::F2 *ekl, int width, int64_t ebase, int64_t self,
-    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
-    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+__device__ __forceinline__ bool gather_forces_fast(
+    const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::F2 *ekl, int width, uint32_t self,
+    typename Tr<P>::R4 me, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
+    typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using M = typename Tr<P>::M;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   constexpr int U = Tr<P>::U;
   bool odd = false;
-  for (int t0 = 0; t0 < width; t0 += U) {
+  auto body = [&](uint32_t jr, F2 kl, R4 o) {
+    const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+    const M len2 = dx * dx + dy * dy + dz * dz;
+    M r;
+    if constexpr (P == PREC_FP32) {
+      r = rsqrtf(len2);  // +inf at 0: the select below discards it
+    } else {
+      r = (double)rsqrtf((float)len2);
+      r = r * (1.5 - 0.5 * len2 * r * r);  // one Newton step, ~1e-14
+    }
+    const M sc = (M)kl.x * (len2 * r - (M)kl.y) * r;
+    const bool zero = len2 == (M)0;
+    odd |= zero != ((jr & EJ_DEAD) != 0);
+    const M s = zero ? (M)0 : sc;
+    fx += (R)(s * dx);
+    fy += (R)(s * dy);
+    fz += (R)(s * dz);
+  };
+  auto ld_j = [&](const uint32_t *p) { return GLOBAL_SRC ? __ldg(p) : *p; };
+  auto ld_k = [&](const F2 *p) { return GLOBAL_SRC ? __ldg(p) : *p; };
+  auto nbr = [&](uint32_t jr) {
+    return pos[(jr & EJ_DEAD) ? self : (jr & EJ_MASK)];
+  };
+  int t = 0;
+  for (; t + U <= width; t += U, ej += 32 * U, ekl += 32 * U) {
     uint32_t jr[U];
     F2 kl[U];
     R4 o[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const bool in = t0 + u < width;
-      const int t = in ? t0 + u : 0;
-      jr[u] = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
-      kl[u] = GLOBAL_SRC ? __ldg(ekl + 32 * t) : ekl[32 * t];
-      if (!in) jr[u] = EJ_PAD;
+      jr[u] = ld_j(ej + 32 * u);
+      kl[u] = ld_k(ekl + 32 * u);
     }
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int64_t j = (jr[u] & EJ_DEAD) ? self : (int64_t)(jr[u] & EJ_MASK);
-      o[u] = pos[j];
-    }
+    for (int u = 0; u < U; u++) o[u] = nbr(jr[u]);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const M dx = (M)(o[u].x - me.x), dy = (M)(o[u].y - me.y),
-              dz = (M)(o[u].z - me.z);
-      const M len2 = dx * dx + dy * dy + dz * dz;
-      const bool plain = !(jr[u] & (EJ_DEAD | EJ_SPECIAL)) && len2 > (M)0;
-      odd |= !(jr[u] & EJ_DEAD) &&
-             ((jr[u] & EJ_SPECIAL) || len2 == (M)0);
-      M r;
-      if constexpr (P == PREC_FP32) {
-        r = rsqrtf(plain ? len2 : 1.0f);
-      } else {
-        const double l2 = plain ? (double)len2 : 1.0;
-        r = (double)rsqrtf((float)l2);
-        r = r * (1.5 - 0.5 * l2 * r * r);
-      }
-      const M fmag = (M)kl[u].x * (len2 * r - (M)kl[u].y);
-      const M sc = plain ? fmag * r : (M)0;
-      fx += (R)(sc * dx);
-      fy += (R)(sc * dy);
-      fz += (R)(sc * dz);
-    }
+    for (int u = 0; u < U; u++) body(jr[u], kl[u], o[u]);
   }
-  if (odd) {
-    // rare: actuated / breakable / zero-length entries, exact semantics
-    for (int t = 0; t < width; t++) {
-      const uint32_t jr = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
-      if (jr & EJ_DEAD) continue;
-      const R4 o = pos[jr & EJ_MASK];
-      const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y),
-              dz = (M)(o.z - me.z);
-      const M len2 = dx * dx + dy * dy + dz * dz;
-      if (!(jr & EJ_SPECIAL) && len2 > (M)0) continue;  // done above
-      const F2 kl = GLOBAL_SRC ? __ldg(ekl + 32 * t) : ekl[32 * t];
-      entry_force<P>(S, ebase + 32 * (int64_t)t, jr, me, o, kl, sim_t, fx,
-                     fy, fz);
+  for (; t < width; t++, ej += 32, ekl += 32) {
+    const uint32_t jr = ld_j(ej);
+    body(jr, ld_k(ekl), nbr(jr));
+  }
+  return odd;
+}
+
+// Side effects of alive zero-length springs (kernels.py:50-54) for a mass
+// that went through the fast loop.
+template <int P, bool GLOBAL_SRC>
+__device__ __noinline__ void degenerate_flags(
+    const int32_t *ent_s, uint8_t *s_degen, unsigned long long *status,
+    const typename Tr<P>::R4 *pos, const uint32_t *ej, int width,
+    int64_t ebase, typename Tr<P>::R4 me) {
+  for (int t = 0; t < width; t++) {
+    const uint32_t jr = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
+    if (jr & (EJ_DEAD | EJ_M2)) continue;
+    const typename Tr<P>::R4 o = pos[jr & EJ_MASK];
+    if (o.x == me.x && o.y == me.y && o.z == me.z) {
+      const int32_t s = ent_s[ebase + 32 * (int64_t)t];
+      if (!s_degen[s]) {
+        s_degen[s] = 1;
+        atomicAdd(status + 2, 1ull);
+      }
     }
   }
 }
@@ -569,14 +590,21 @@ template <int P, bool GLOBAL_SRC>
 __device__ __forceinline__ void gather_forces(
     const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
     const typename Tr<P>::F2 *ekl, int width, int64_t ebase, int64_t self,
-    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    uint32_t fl, typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
     typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
-  if constexpr (P == PREC_FP64)
+  if constexpr (P == PREC_FP64) {
     gather_forces_exact<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, me,
                                        sim_t, fx, fy, fz);
-  else
-    gather_forces_fast<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, self,
-                                      me, sim_t, fx, fy, fz);
+  } else {
+    if (fl & MF_SPECIAL)
+      gather_forces_exact<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, me,
+                                         sim_t, fx, fy, fz);
+    else if (gather_forces_fast<P, GLOBAL_SRC>(pos, ej, ekl, width,
+                                                 (uint32_t)self, me, fx, fy,
+                                                 fz))
+      degenerate_flags<P, GLOBAL_SRC>(S.ent_s, S.s_degen, S.status, pos, ej,
+                                      width, ebase, me);
+  }
 }
 
 // Tail of a mass update after its spring forces are known.
@@ -651,8 +679,8 @@ __global__ void __launch_bounds__(256)
   const int64_t ebase = S.slice_ptr[w] + (i & 31);
   const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
   gather_forces<P, true>(S, pos, S.ent_j + ebase,
-                         (const F2 *)S.ent_kL0 + ebase, width, ebase, i, me,
-                         T.sim_t, fx, fy, fz);
+                         (const F2 *)S.ent_kL0 + ebase, width, ebase, i, fl,
+                         me, T.sim_t, fx, fy, fz);
   finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
 }
 
@@ -770,7 +798,7 @@ __global__ void __launch_bounds__(512)
       initial_force<P>(S, i, fl, false, fx, fy, fz);
       gather_forces<P, false>(S, pos, (const uint32_t *)st + lane,
                               (const F2 *)(st + jbytes_cap) + lane, width,
-                              e0 + lane, i, me, T.sim_t, fx, fy, fz);
+                              e0 + lane, i, fl, me, T.sim_t, fx, fy, fz);
       finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
     }
     __syncwarp();
