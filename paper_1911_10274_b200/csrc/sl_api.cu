@@ -506,6 +506,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 int ensure_masses(sl_ctx *c, int64_t m_n) {
   size_t r4 = 4 * c->rsz;
+  m_n = (m_n + 31) / 32 * 32;  // bulk copies move whole 32-mass slices
   for (int b = 0; b < 2; b++) CK(c->pos[b].ensure(r4 * m_n));
   CK(c->vel.ensure(r4 * m_n));
   CK(c->acc.ensure(3 * c->rsz * m_n));
@@ -537,9 +538,10 @@ void configure_tma(sl_ctx *c) {
   c->tma_warps = 0;
   if (!c->tma_enabled || c->n_slices == 0 || c->max_width == 0) return;
   const size_t f2 = 2 * c->fsz;
-  const size_t stage = (size_t)c->max_width * 32 * (4 + f2);
+  // two 32-mass blocks (pos, vel) + entry words + (k, L0) pairs
+  const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)c->max_width * 32 * (4 + f2);
   const size_t per_warp = 2 * stage + 16;
-  int warps = (int)std::min<size_t>(16, (size_t)c->smem_optin / per_warp);
+  int warps = (int)std::min<size_t>(12, (size_t)c->smem_optin / per_warp);
   if (warps < 2) return;  // hub masses: fall back to the plain kernel
   c->tma.n_slices = c->n_slices;
   c->tma.cap_w = (int)c->max_width;

@@ -116,7 +116,8 @@ struct Tr<PREC_FP64> {
   using R4 = double4;
   using F2 = double2;
   using M = double;  // force arithmetic
-  static constexpr int U = 4;  // gather batch (registers: 4 x 52 B)
+  static constexpr int U = 4;
+  static constexpr int UP = 4;  // gather batch (registers: 4 x 52 B)
 };
 template <>
 struct Tr<PREC_FP32> {
@@ -126,6 +127,7 @@ struct Tr<PREC_FP32> {
   using F2 = float2;
   using M = float;
   static constexpr int U = 8;
+  static constexpr int UP = 6;  // pipelined batch (2 in flight)
 };
 template <>
 struct Tr<PREC_MIXED> {
@@ -135,6 +137,7 @@ struct Tr<PREC_MIXED> {
   using F2 = float2;
   using M = double;  // fp32 storage of (k, L0), fp64 force arithmetic
   static constexpr int U = 6;
+  static constexpr int UP = 4;
 };
 
 __device__ __forceinline__ uint32_t flags_of(float w) {
@@ -565,6 +568,77 @@ __device__ __forceinline__ bool gather_forces_fast(
   return odd;
 }
 
+// Same contract as gather_forces_fast, software-pipelined across batches:
+// the neighbour gathers of batch b+1 are issued before batch b is reduced,
+// so 2*U gathers are in flight per thread.  Used by the TMA kernel, which
+// runs few warps per SM and can afford the registers.
+template <int P, int U>
+__device__ __forceinline__ bool gather_forces_pipe(
+    const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::F2 *ekl, int width, uint32_t self,
+    typename Tr<P>::R4 me, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
+    typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using M = typename Tr<P>::M;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  bool odd = false;
+  auto body = [&](uint32_t jr, F2 kl, R4 o) {
+    const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+    const M len2 = dx * dx + dy * dy + dz * dz;
+    M r;
+    if constexpr (P == PREC_FP32) {
+      r = rsqrtf(len2);
+    } else {
+      r = (double)rsqrtf((float)len2);
+      r = r * (1.5 - 0.5 * len2 * r * r);
+    }
+    const M sc = (M)kl.x * (len2 * r - (M)kl.y) * r;
+    const bool zero = len2 == (M)0;
+    odd |= zero != ((jr & EJ_DEAD) != 0);
+    const M s = zero ? (M)0 : sc;
+    fx += (R)(s * dx);
+    fy += (R)(s * dy);
+    fz += (R)(s * dz);
+  };
+  auto nbr = [&](uint32_t jr) {
+    return pos[(jr & EJ_DEAD) ? self : (jr & EJ_MASK)];
+  };
+  struct Batch {
+    uint32_t j[U];
+    F2 k[U];
+    R4 o[U];
+  };
+  auto load = [&](Batch &B, int t) {
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      B.j[u] = ej[32 * (t + u)];
+      B.k[u] = ekl[32 * (t + u)];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) B.o[u] = nbr(B.j[u]);
+  };
+  auto reduce = [&](const Batch &B) {
+#pragma unroll
+    for (int u = 0; u < U; u++) body(B.j[u], B.k[u], B.o[u]);
+  };
+  const int nb = width / U;
+  Batch A, B;
+  if (nb > 0) load(A, 0);
+  for (int b = 0; b < nb; b += 2) {
+    if (b + 1 < nb) load(B, (b + 1) * U);
+    reduce(A);
+    if (b + 1 >= nb) break;
+    if (b + 2 < nb) load(A, (b + 2) * U);
+    reduce(B);
+  }
+  for (int t = nb * U; t < width; t++) {
+    const uint32_t jr = ej[32 * t];
+    body(jr, ekl[32 * t], nbr(jr));
+  }
+  return odd;
+}
+
 // Side effects of alive zero-length springs (kernels.py:50-54) for a mass
 // that went through the fast loop.
 template <int P, bool GLOBAL_SRC>
@@ -735,13 +809,17 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 struct TmaCfg {
   int64_t n_slices;
-  int cap_w;        // max slice width the stages hold
-  int warps;        // warps per CTA
-  uint32_t stage_bytes;  // bytes of one stage (j words + kL0 pairs)
+  int cap_w;             // max slice width the stages hold
+  int warps;             // warps per CTA
+  uint32_t stage_bytes;  // one stage: 32 pos + 32 vel records, j, (k, L0)
 };
 
+// Stage layout: [pos of the slice's 32 masses][their vel][cap_w*32 entry
+// words][cap_w*32 (k, L0) pairs].  Everything a warp needs for one slice
+// arrives through four bulk copies on one mbarrier, so the only exposed
+// latency left in the loop is the L2 gather of neighbour positions.
 template <int P>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(384)
     k_gather_tma(const KState S, const EnvP E, const StepP T,
                  const TmaCfg C) {
   using R = typename Tr<P>::R;
@@ -753,53 +831,83 @@ __global__ void __launch_bounds__(512)
   unsigned char *ring = smem + (size_t)warp * 2 * C.stage_bytes;
   uint64_t *bars =
       (uint64_t *)(smem + (size_t)C.warps * 2 * C.stage_bytes) + 2 * warp;
-  const uint32_t jbytes_cap = (uint32_t)C.cap_w * 128u;
+  constexpr uint32_t MB = 32 * sizeof(R4);  // mass block bytes
+  const uint32_t j_off = 2 * MB;
+  const uint32_t k_off = j_off + (uint32_t)C.cap_w * 128u;
   if (lane == 0) {
     mbar_init(bars + 0, 1);
     mbar_init(bars + 1, 1);
     fence_proxy_async();
   }
   __syncwarp();
+  const R4 *pos = (const R4 *)S.pos[T.cur];
   const int64_t stride = (int64_t)gridDim.x * C.warps;
   int64_t s = (int64_t)blockIdx.x * C.warps + warp;
-  auto issue = [&](int64_t sl, int stage) {
-    const int64_t e0 = S.slice_ptr[sl];
-    const uint32_t n = (uint32_t)(S.slice_ptr[sl + 1] - e0);  // entries
+  // lane 0 holds slice_ptr of the current and the next slice
+  int64_t cur0 = 0, cur1 = 0, nxt0 = 0, nxt1 = 0;
+  auto issue = [&](int64_t sl, int64_t e0, int64_t e1, int stage) {
+    const uint32_t n = (uint32_t)(e1 - e0);
     unsigned char *dst = ring + (size_t)stage * C.stage_bytes;
-    mbar_expect_tx(bars + stage, n * (uint32_t)(4 + sizeof(F2)));
+    mbar_expect_tx(bars + stage, 2 * MB + n * (uint32_t)(4 + sizeof(F2)));
+    bulk_g2s(dst, pos + sl * 32, MB, bars + stage);
+    bulk_g2s(dst + MB, (const R4 *)S.vel + sl * 32, MB, bars + stage);
     if (n) {
-      bulk_g2s(dst, S.ent_j + e0, n * 4u, bars + stage);
-      bulk_g2s(dst + jbytes_cap, (const F2 *)S.ent_kL0 + e0,
+      bulk_g2s(dst + j_off, S.ent_j + e0, n * 4u, bars + stage);
+      bulk_g2s(dst + k_off, (const F2 *)S.ent_kL0 + e0,
                n * (uint32_t)sizeof(F2), bars + stage);
     }
   };
-  if (lane == 0 && s < C.n_slices) issue(s, 0);
-  const R4 *pos = (const R4 *)S.pos[T.cur];
+  if (lane == 0 && s < C.n_slices) {
+    cur0 = S.slice_ptr[s];
+    cur1 = S.slice_ptr[s + 1];
+    issue(s, cur0, cur1, 0);
+    if (s + stride < C.n_slices) {
+      nxt0 = S.slice_ptr[s + stride];
+      nxt1 = S.slice_ptr[s + stride + 1];
+    }
+  }
   for (int k = 0; s < C.n_slices; s += stride, k++) {
     const int stage = k & 1;
+    const int64_t e0 = __shfl_sync(0xffffffffu, cur0, 0);
+    const int width = (int)((__shfl_sync(0xffffffffu, cur1, 0) - e0) >> 5);
     if (lane == 0 && s + stride < C.n_slices) {
-      fence_proxy_async();  // prior generic reads of that stage are done
-      issue(s + stride, stage ^ 1);
+      fence_proxy_async();  // generic reads of that stage finished (syncwarp)
+      issue(s + stride, nxt0, nxt1, stage ^ 1);
+      cur0 = nxt0;
+      cur1 = nxt1;
+      const int64_t s2 = s + 2 * stride;
+      if (s2 < C.n_slices) {  // metadata one slice further ahead
+        nxt0 = S.slice_ptr[s2];
+        nxt1 = S.slice_ptr[s2 + 1];
+      }
     }
     const int64_t i = s * 32 + lane;
-    const int64_t e0 = S.slice_ptr[s];
-    const int width = (int)((S.slice_ptr[s + 1] - e0) >> 5);
-    R4 v, me;
-    uint32_t fl = 0;
-    if (i < S.m_n) {
-      v = ((const R4 *)S.vel)[i];
-      me = pos[i];
-      fl = flags_of(v.w);
-    }
+    const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
     mbar_wait(bars + stage, (uint32_t)((k >> 1) & 1));
-    if (fl & MF_ALIVE) {
-      const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
-      R fx, fy, fz;
-      initial_force<P>(S, i, fl, false, fx, fy, fz);
-      gather_forces<P, false>(S, pos, (const uint32_t *)st + lane,
-                              (const F2 *)(st + jbytes_cap) + lane, width,
-                              e0 + lane, i, fl, me, T.sim_t, fx, fy, fz);
-      finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+    if (i < S.m_n) {
+      const R4 v = ((const R4 *)(st + MB))[lane];
+      const uint32_t fl = flags_of(v.w);
+      if (fl & MF_ALIVE) {
+        const R4 me = ((const R4 *)st)[lane];
+        R fx, fy, fz;
+        initial_force<P>(S, i, fl, false, fx, fy, fz);
+        const uint32_t *ej = (const uint32_t *)(st + j_off) + lane;
+        const F2 *ekl = (const F2 *)(st + k_off) + lane;
+        if constexpr (P == PREC_FP64) {
+          gather_forces_exact<P, false>(S, pos, ej, ekl, width, e0 + lane,
+                                        me, T.sim_t, fx, fy, fz);
+        } else {
+          if (fl & MF_SPECIAL)
+            gather_forces_exact<P, false>(S, pos, ej, ekl, width, e0 + lane,
+                                          me, T.sim_t, fx, fy, fz);
+          else if (gather_forces_pipe<P, Tr<P>::UP>(pos, ej, ekl, width,
+                                                     (uint32_t)i, me, fx, fy,
+                                                     fz))
+            degenerate_flags<P, false>(S.ent_s, S.s_degen, S.status, pos, ej,
+                                       width, e0 + lane, me);
+        }
+        finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+      }
     }
     __syncwarp();
   }
