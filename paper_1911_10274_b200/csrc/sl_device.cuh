@@ -127,7 +127,7 @@ struct Tr<PREC_FP32> {
   using F2 = float2;
   using M = float;
   static constexpr int U = 8;
-  static constexpr int UP = 6;  // pipelined batch (2 in flight)
+  static constexpr int UP = 11;  // pipelined batch (2 in flight)
 };
 template <>
 struct Tr<PREC_MIXED> {
@@ -137,7 +137,7 @@ struct Tr<PREC_MIXED> {
   using F2 = float2;
   using M = double;  // fp32 storage of (k, L0), fp64 force arithmetic
   static constexpr int U = 6;
-  static constexpr int UP = 4;
+  static constexpr int UP = 6;
 };
 
 __device__ __forceinline__ uint32_t flags_of(float w) {
@@ -604,33 +604,29 @@ __device__ __forceinline__ bool gather_forces_pipe(
   auto nbr = [&](uint32_t jr) {
     return pos[(jr & EJ_DEAD) ? self : (jr & EJ_MASK)];
   };
+  // only the gathered positions live in registers; entry words and (k, L0)
+  // are re-read from the shared-memory stage when the batch is reduced
   struct Batch {
-    uint32_t j[U];
-    F2 k[U];
     R4 o[U];
   };
   auto load = [&](Batch &B, int t) {
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      B.j[u] = ej[32 * (t + u)];
-      B.k[u] = ekl[32 * (t + u)];
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) B.o[u] = nbr(B.j[u]);
+    for (int u = 0; u < U; u++) B.o[u] = nbr(ej[32 * (t + u)]);
   };
-  auto reduce = [&](const Batch &B) {
+  auto reduce_at = [&](const Batch &B, int t) {
 #pragma unroll
-    for (int u = 0; u < U; u++) body(B.j[u], B.k[u], B.o[u]);
+    for (int u = 0; u < U; u++)
+      body(ej[32 * (t + u)], ekl[32 * (t + u)], B.o[u]);
   };
   const int nb = width / U;
   Batch A, B;
   if (nb > 0) load(A, 0);
   for (int b = 0; b < nb; b += 2) {
     if (b + 1 < nb) load(B, (b + 1) * U);
-    reduce(A);
+    reduce_at(A, b * U);
     if (b + 1 >= nb) break;
     if (b + 2 < nb) load(A, (b + 2) * U);
-    reduce(B);
+    reduce_at(B, (b + 1) * U);
   }
   for (int t = nb * U; t < width; t++) {
     const uint32_t jr = ej[32 * t];
