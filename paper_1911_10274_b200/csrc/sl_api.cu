@@ -22,6 +22,7 @@
 
 #include "../../include/softlat_cuda.h"
 #include "sl_device.cuh"
+#include "sl_split.cuh"
 
 namespace sl {
 const Launch &launch_fp64();
@@ -93,6 +94,18 @@ struct sl_ctx {
   TmaCfg tma;
   int sm_count = 0, smem_optin = 0;
   bool tma_enabled = true;
+  // split layout (tolerance modes, sl_split.cuh)
+  bool split_enabled = true;  // SL_DISABLE_SPLIT=1 forces the exact layout
+  bool split = false;         // the current layout is split
+  int sp_a = 0, sp_rows = 0;
+  int64_t sp_wa = 0, sp_wb = 0;  // widest A / B sections
+  DevBuf sp_j, sp_kl, sp_s, sp_w, sp_ekl, degB, sp_meta;
+  SplitCfg scfg;
+  int split_warps = 0, split_grid = 0;
+  // device copy of the kernel state block (KState::self)
+  DevBuf kdev;
+  KState khost;
+  bool khost_valid = false;
   // scratch
   DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
   DevBuf status;
@@ -327,6 +340,10 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
       or_flags((R4 *)S.vel + ab.x, MF_SPECIAL);
       or_flags((R4 *)S.vel + ab.y, MF_SPECIAL);
     }
+    if (S.split) {
+      if (ab.x >= 0 && S.e1[s] >= 0) ((F2 *)S.sp_kl)[S.sp_ekl[s]] = kl;
+      return;
+    }
     int64_t es[2] = {S.e1[s], S.e2[s]};
     for (int q = 0; q < 2; q++) {
       int64_t e = es[q];
@@ -345,10 +362,7 @@ __global__ void k_kill_springs(int64_t n, const int64_t *slots, KState S,
   int64_t s = slots[r];
   S.ends[s] = make_int2(-1, -1);
   S.s_alive[s] = 0;
-  if (layout_valid) {
-    if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
-    if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
-  }
+  if (layout_valid) kill_entries(S, s);
 }
 
 __global__ void k_set_custom(int64_t n, const int64_t *slots,
@@ -374,10 +388,7 @@ __global__ void k_validate(KState S, const uint8_t *m_alive,
     return;
   S.ends[s] = make_int2(-1, -1);
   S.s_alive[s] = 0;
-  if (layout_valid) {
-    if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
-    if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
-  }
+  if (layout_valid) kill_entries(S, s);
   atomicAdd(S.status + 1, 1ull);
 }
 
@@ -453,6 +464,107 @@ __global__ void k_fill_layout(int64_t n, const uint32_t *keys,
   (side ? e2 : e1)[s] = e;
 }
 
+
+// ------------------------------------------------ split layout build kernels
+// Records: (key 2*m1, s) for the A entry, (key 2*m2+1, s) for the B entry;
+// a stable radix sort by key groups each mass's A then B records, each in
+// ascending spring slot; the rank within a group is the entry row.
+__global__ void k_split_keys(int64_t s_n, const int2 *ends, uint32_t m_n,
+                             uint32_t *keys, uint32_t *vals, uint32_t *deg_a,
+                             uint32_t *deg_b) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s_n) return;
+  int2 ab = ends[s];
+  bool al = ab.x >= 0;
+  keys[2 * s] = al ? 2u * (uint32_t)ab.x : 2u * m_n;
+  keys[2 * s + 1] = al ? 2u * (uint32_t)ab.y + 1u : 2u * m_n;
+  vals[2 * s] = (uint32_t)s;
+  vals[2 * s + 1] = (uint32_t)s;
+  if (al) {
+    atomicAdd(deg_a + ab.x, 1u);
+    atomicAdd(deg_b + ab.y, 1u);
+  }
+}
+
+// per-slice section widths; meta[0..1] = widest A / B, meta[2] = streamed
+// entries (sum over slices of 32 * (wA + wB))
+__global__ void k_split_widths(int64_t m_n, const uint32_t *deg_a,
+                               const uint32_t *deg_b, int64_t n_slices,
+                               uint32_t *sp_w, unsigned long long *meta) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t w = i >> 5;
+  if (w >= n_slices) return;
+  uint32_t da = i < m_n ? deg_a[i] : 0u, db = i < m_n ? deg_b[i] : 0u;
+  for (int o = 16; o; o >>= 1) {
+    da = max(da, __shfl_xor_sync(0xffffffffu, da, o));
+    db = max(db, __shfl_xor_sync(0xffffffffu, db, o));
+  }
+  if ((i & 31) == 0) {
+    sp_w[w] = min(da, 0xFFFFu) | (min(db, 0xFFFFu) << 16);
+    atomicMax(meta + 0, (unsigned long long)da);
+    atomicMax(meta + 1, (unsigned long long)db);
+    atomicAdd(meta + 2, 32ull * (da + db));
+  }
+}
+
+__global__ void k_split_init(int64_t n, int rows, int wa_stride,
+                             uint32_t sent, uint32_t nul, uint32_t *sp_j) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  int row = (int)((e >> 5) % rows);
+  sp_j[e] = row < wa_stride ? sent : nul;
+}
+
+template <int P>
+__global__ void k_split_sentinel(void *pos0, void *pos1, int64_t m_pad) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  int q = threadIdx.x;
+  R4 p;
+  p.x = p.y = p.z = (R)SENTINEL_POS;
+  p.w = (R)0.0;
+  ((R4 *)pos0)[m_pad + q] = p;
+  ((R4 *)pos1)[m_pad + q] = p;
+}
+
+template <int P>
+__global__ void k_split_fill(int64_t n, const uint32_t *keys,
+                             const uint32_t *vals, uint32_t kbound,
+                             const int64_t *start, KState S, uint32_t *sp_j,
+                             void *sp_kl, int32_t *sp_s, uint32_t *sp_ekl,
+                             int64_t *e1, int64_t *e2, int pass) {
+  using F = typename Tr<P>::F;
+  using F2 = typename Tr<P>::F2;
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint32_t key = keys[p];
+  if (key >= kbound || (int)(key & 1u) != pass) return;
+  uint32_t owner = key >> 1;
+  int64_t s = vals[p];
+  int64_t r = p - start[key];
+  int64_t sl = owner >> 5, lane = owner & 31;
+  int2 ab = S.ends[s];
+  if (pass == 0) {
+    int64_t e = (sl * S.sp_rows + r) * 32 + lane;
+    uint32_t kli = (uint32_t)((sl << (S.sp_a + 5)) | (r << 5) | lane);
+    sp_j[e] = (uint32_t)ab.y;
+    ((F2 *)sp_kl)[kli] = ((const F2 *)S.kL0)[s];
+    sp_s[e] = (int32_t)s;
+    sp_ekl[s] = kli;
+    e1[s] = e;
+  } else {
+    int64_t e = (sl * S.sp_rows + ((int64_t)1 << S.sp_a) + r) * 32 + lane;
+    sp_j[e] = sp_ekl[s];
+    sp_s[e] = (int32_t)s;
+    e2[s] = e;
+  }
+  bool special = S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+  if (special) {
+    S.xflags[owner] = 1;
+    or_flags((typename Tr<P>::R4 *)S.vel + owner, MF_SPECIAL);
+  }
+}
+
 KState make_state(sl_ctx *c) {
   KState S;
   memset(&S, 0, sizeof S);
@@ -483,6 +595,21 @@ KState make_state(sl_ctx *c) {
   S.e2 = c->layout_valid ? c->e2.as<int64_t>() : nullptr;
   S.status = c->status.as<unsigned long long>();
   S.xflags = c->xflags.as<uint8_t>();
+  S.fsz8 = c->fsz == 8;
+  S.self = c->kdev.as<KState>();
+  S.split = c->layout_valid && c->split;
+  if (c->split) {
+    S.sp_a = c->sp_a;
+    S.sp_rows = c->sp_rows;
+    const int64_t m_pad = (c->m_n + 31) / 32 * 32;
+    S.sp_sent = (uint32_t)m_pad;
+    S.sp_null = (uint32_t)((m_pad / 32) << (c->sp_a + 5));
+    S.sp_j = c->sp_j.as<uint32_t>();
+    S.sp_kl = c->sp_kl.p;
+    S.sp_s = c->sp_s.as<int32_t>();
+    S.sp_w = c->sp_w.as<uint32_t>();
+    S.sp_ekl = c->sp_ekl.as<uint32_t>();
+  }
   return S;
 }
 
@@ -507,7 +634,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 int ensure_masses(sl_ctx *c, int64_t m_n) {
   size_t r4 = 4 * c->rsz;
   m_n = (m_n + 31) / 32 * 32;  // bulk copies move whole 32-mass slices
-  for (int b = 0; b < 2; b++) CK(c->pos[b].ensure(r4 * m_n));
+  // + one slice of sentinel records (split layout's dead / padding target)
+  for (int b = 0; b < 2; b++) CK(c->pos[b].ensure(r4 * (m_n + 32)));
   CK(c->vel.ensure(r4 * m_n));
   CK(c->acc.ensure(3 * c->rsz * m_n));
   CK(c->fext.ensure(r4 * m_n));
@@ -553,7 +681,7 @@ void configure_tma(sl_ctx *c) {
   c->tma_warps = warps;
 }
 
-int build_layout(sl_ctx *c) {
+int build_exact_layout(sl_ctx *c) {
   const int64_t m_n = c->m_n, s_n = c->s_n;
   if (m_n > (int64_t)EJ_MASK)
     return fail(c, SL_EUNSUPPORTED, "too many masses for one context (%lld)",
@@ -666,6 +794,168 @@ int build_layout(sl_ctx *c) {
   return SL_OK;
 }
 
+
+// Size the per-warp rings of the split TMA kernel for the widest sections.
+void configure_split_tma(sl_ctx *c) {
+  c->split_warps = 0;
+  if (!c->tma_enabled || c->n_slices == 0) return;
+  const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(c->sp_wa + c->sp_wb) * 128 +
+                       (size_t)c->sp_wa * 32 * 2 * c->fsz;
+  const size_t per_warp = 2 * stage + 16;
+  int warps = (int)std::min<size_t>(SPLIT_MAX_WARPS,
+                                     (size_t)c->smem_optin / per_warp);
+  if (warps < 2) return;
+  c->scfg.n_slices = c->n_slices;
+  c->scfg.cap_a = (int)c->sp_wa;
+  c->scfg.cap_b = (int)c->sp_wb;
+  c->scfg.warps = warps;
+  c->scfg.stage_bytes = (uint32_t)stage;
+  int64_t ctas = (c->n_slices + warps - 1) / warps;
+  c->split_grid = (int)std::min<int64_t>(ctas, c->sm_count);
+  if (launchers(c->prec).split_setup((int)(warps * per_warp)) != 0) return;
+  c->split_warps = warps;
+}
+
+// Device build of the split layout (sl_split.cuh).  *used = false when the
+// mesh does not fit its index encoding (the caller falls back to the exact
+// layout).
+int build_split_layout(sl_ctx *c, bool *used) {
+  *used = false;
+  const int64_t m_n = c->m_n, s_n = c->s_n;
+  const int64_t n_slices = (m_n + 31) / 32;
+  const int64_t m_pad = n_slices * 32;
+  if (m_pad + 32 >= (int64_t)0xFFFFFFFF || 2 * m_n + 1 >= (int64_t)0xFFFFFFFF ||
+      2 * s_n >= (int64_t)0x7fffffff)
+    return SL_OK;
+  const int64_t n_rec = 2 * s_n;
+  CK(c->deg.ensure(4 * (m_n + 1)));
+  CK(c->degB.ensure(4 * (m_n + 1)));
+  CK(c->sp_w.ensure(4 * (n_slices + 1)));
+  CK(c->sp_meta.ensure(8 * 4));
+  CK(cudaMemsetAsync(c->deg.p, 0, 4 * (m_n + 1), c->st));
+  CK(cudaMemsetAsync(c->degB.p, 0, 4 * (m_n + 1), c->st));
+  CK(cudaMemsetAsync(c->sp_meta.p, 0, 8 * 4, c->st));
+  CK(cudaMemsetAsync(c->sp_w.p, 0, 4 * (n_slices + 1), c->st));
+  for (int b = 0; b < 2; b++) {
+    CK(c->keys[b].ensure(4 * n_rec));
+    CK(c->vals[b].ensure(4 * n_rec));
+  }
+  if (s_n > 0) {
+    k_split_keys<<<blocks_for(s_n), 256, 0, c->st>>>(
+        s_n, c->ends.as<int2>(), (uint32_t)m_n, c->keys[0].as<uint32_t>(),
+        c->vals[0].as<uint32_t>(), c->deg.as<uint32_t>(),
+        c->degB.as<uint32_t>());
+    CKL();
+  }
+  if (n_slices > 0) {
+    k_split_widths<<<blocks_for(32 * n_slices), 256, 0, c->st>>>(
+        m_n, c->deg.as<uint32_t>(), c->degB.as<uint32_t>(), n_slices,
+        c->sp_w.as<uint32_t>(), c->sp_meta.as<unsigned long long>());
+    CKL();
+  }
+  unsigned long long meta[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(meta, c->sp_meta.p, sizeof meta, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const int64_t wa = (int64_t)meta[0], wb = (int64_t)meta[1];
+  int a = 0;
+  while (((int64_t)1 << a) < std::max<int64_t>(wa, 1)) a++;
+  const int64_t rows = ((int64_t)1 << a) + wb;
+  // encodings: 16-bit widths, 32-bit kl indices (incl. the zero slice)
+  if (wa > 0xFFFF || wb > 0xFFFF || a > 16 ||
+      ((n_slices + 1) << (a + 5)) >= ((int64_t)1 << 32) ||
+      // footprint guard for hub masses: stride padding must not explode
+      n_slices * rows * 32 > 4 * (int64_t)meta[2] + (1 << 20))
+    return SL_OK;
+  c->split = true;
+  c->sp_a = a;
+  c->sp_rows = (int)rows;
+  c->sp_wa = wa;
+  c->sp_wb = wb;
+  const int64_t n_j = n_slices * rows * 32;
+  const int64_t n_kl = (n_slices + 1) << (a + 5);
+  const size_t f2 = 2 * c->fsz;
+  CK(c->sp_j.ensure(4 * n_j));
+  CK(c->sp_s.ensure(4 * n_j));
+  CK(c->sp_kl.ensure(f2 * n_kl));
+  CK(c->sp_ekl.ensure(4 * std::max<int64_t>(s_n, 1)));
+  CK(c->e1.ensure(8 * s_n));
+  CK(c->e2.ensure(8 * s_n));
+  CK(cudaMemsetAsync(c->e1.p, 0xFF, 8 * s_n, c->st));
+  CK(cudaMemsetAsync(c->e2.p, 0xFF, 8 * s_n, c->st));
+  CK(cudaMemsetAsync(c->sp_kl.p, 0, f2 * n_kl, c->st));
+  CK(cudaMemsetAsync(c->sp_s.p, 0xFF, 4 * n_j, c->st));
+  CK(cudaMemsetAsync(c->xflags.p, 0, m_n + 1, c->st));
+  if (n_j > 0) {
+    k_split_init<<<blocks_for(n_j), 256, 0, c->st>>>(
+        n_j, (int)rows, 1 << a, (uint32_t)m_pad,
+        (uint32_t)(n_slices << (a + 5)), c->sp_j.as<uint32_t>());
+    CKL();
+  }
+  if (m_n > 0) {
+    k_clear_flag<<<blocks_for(m_n), 256, 0, c->st>>>(m_n, c->vel.p,
+                                                      c->rsz == 8, MF_SPECIAL);
+    CKL();
+  }
+  auto sent = c->prec == PREC_FP32 ? k_split_sentinel<PREC_FP32>
+                                   : k_split_sentinel<PREC_MIXED>;
+  sent<<<1, 32, 0, c->st>>>(c->pos[0].p, c->pos[1].p, m_pad);
+  CKL();
+  if (n_rec > 0) {
+    int end_bit = 1;
+    while (((uint64_t)1 << end_bit) <= (uint64_t)(2 * m_n)) end_bit++;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(
+        nullptr, tb, (uint32_t *)nullptr, (uint32_t *)nullptr,
+        (uint32_t *)nullptr, (uint32_t *)nullptr, (int)n_rec, 0, end_bit);
+    CK(c->sort_tmp.ensure(tb));
+    tb = c->sort_tmp.bytes;
+    CK(cub::DeviceRadixSort::SortPairs(
+        c->sort_tmp.p, tb, c->keys[0].as<uint32_t>(),
+        c->keys[1].as<uint32_t>(), c->vals[0].as<uint32_t>(),
+        c->vals[1].as<uint32_t>(), (int)n_rec, 0, end_bit, c->st));
+    CK(c->start.ensure(8 * (2 * m_n + 1)));
+    k_owner_start<<<blocks_for(n_rec), 256, 0, c->st>>>(
+        n_rec, c->keys[1].as<uint32_t>(), (uint32_t)(2 * m_n),
+        c->start.as<int64_t>());
+    CKL();
+    KState S = make_state(c);
+    auto fill = c->prec == PREC_FP32 ? k_split_fill<PREC_FP32>
+                                     : k_split_fill<PREC_MIXED>;
+    for (int pass = 0; pass < 2; pass++) {
+      fill<<<blocks_for(n_rec), 256, 0, c->st>>>(
+          n_rec, c->keys[1].as<uint32_t>(), c->vals[1].as<uint32_t>(),
+          (uint32_t)(2 * m_n), c->start.as<int64_t>(), S,
+          c->sp_j.as<uint32_t>(), c->sp_kl.p, c->sp_s.as<int32_t>(),
+          c->sp_ekl.as<uint32_t>(), c->e1.as<int64_t>(), c->e2.as<int64_t>(),
+          pass);
+      CKL();
+    }
+  }
+  CK(cudaStreamSynchronize(c->st));
+  c->n_slices = n_slices;
+  c->n_entries = (int64_t)meta[2];
+  c->max_width = 0;
+  c->tma_warps = 0;
+  configure_split_tma(c);
+  c->layout_valid = true;
+  c->layout_builds++;
+  c->launches += 8;
+  *used = true;
+  return SL_OK;
+}
+
+int build_layout(sl_ctx *c) {
+  c->split = false;
+  if (c->prec != PREC_FP64 && c->split_enabled) {
+    bool used = false;
+    int rc = build_split_layout(c, &used);
+    if (rc || used) return rc;
+    c->split = false;
+  }
+  return build_exact_layout(c);
+}
+
 int prepare(sl_ctx *c, bool need_layout) {
   if (!c->masses_set || !c->springs_set)
     return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
@@ -685,6 +975,17 @@ int prepare(sl_ctx *c, bool need_layout) {
     int rc = build_layout(c);
     if (rc) return rc;
   }
+  return SL_OK;
+}
+
+// Refresh the device copy of S (read by out-of-line rare paths) when it
+// changed since the last upload.
+int upload_state(sl_ctx *c, const KState &S) {
+  if (c->khost_valid && memcmp(&c->khost, &S, sizeof S) == 0) return SL_OK;
+  c->khost = S;
+  CK(cudaMemcpyAsync(c->kdev.p, &c->khost, sizeof S, cudaMemcpyHostToDevice,
+                     c->st));
+  c->khost_valid = true;
   return SL_OK;
 }
 
@@ -734,6 +1035,8 @@ int sl_create(int device, int precision, sl_ctx **out) {
   c->rsz = precision == PREC_FP32 ? 4 : 8;
   c->fsz = precision == PREC_FP64 ? 8 : 4;
   if (const char *ev = getenv("SL_DISABLE_TMA")) c->tma_enabled = ev[0] == '0';
+  if (const char *ev = getenv("SL_DISABLE_SPLIT"))
+    c->split_enabled = ev[0] == '0';
   memset(&c->env, 0, sizeof c->env);
   cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
   if (e == cudaSuccess)
@@ -752,6 +1055,8 @@ int sl_create(int device, int precision, sl_ctx **out) {
                                cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                device);
   if (e == cudaSuccess) e = c->status.ensure(8 * 8);
+  if (e == cudaSuccess) e = c->kdev.ensure(sizeof(KState));
+  if (e == cudaSuccess) memset(&c->khost, 0, sizeof c->khost);
   if (e == cudaSuccess)
     e = cudaMallocHost((void **)&c->h_status, 8 * 8);
   if (e != cudaSuccess) {
@@ -777,7 +1082,8 @@ int sl_destroy(sl_ctx *c) {
                     &c->ent_kL0, &c->ent_s, &c->e1, &c->e2, &c->stage,
                     &c->sort_tmp, &c->keys[0], &c->keys[1], &c->vals[0],
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
-                    &c->snap_dev};
+                    &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
+                    &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -809,7 +1115,8 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
                           &c->m2gen, &c->slice_ptr, &c->ent_j, &c->ent_kL0,
                           &c->ent_s, &c->e1, &c->e2, &c->stage, &c->sort_tmp,
                           &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1],
-                          &c->deg, &c->width};
+                          &c->deg, &c->width, &c->sp_j, &c->sp_kl, &c->sp_s,
+                          &c->sp_w, &c->sp_ekl, &c->degB};
   for (const DevBuf *b : bufs) o->device_bytes += (int64_t)b->bytes;
   if (c->springs_set) {
     std::vector<uint8_t> al(c->s_n);
@@ -1170,6 +1477,7 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
   if (rc) return rc;
   const Launch &L = launchers(c->prec);
   KState S = make_state(c);
+  if ((rc = upload_state(c, S))) return rc;
   for (int64_t n = 0; n < n_steps; n++) {
     StepP T;
     T.sim_t = sim_times[n];
@@ -1178,10 +1486,16 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     T.cur = (int)((c->cur + n) & 1);
     T.write_acc = n == n_steps - 1;
     if (accumulation == SL_ACC_GATHER) {
-      if (c->tma_warps)
+      if (c->split) {
+        if (c->split_warps)
+          L.split_tma(S, c->env, T, c->scfg, c->split_grid, c->st);
+        else
+          L.split(S, c->env, T, c->st);
+      } else if (c->tma_warps) {
         L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
-      else
+      } else {
         L.gather(S, c->env, T, c->st);
+      }
       c->launches++;
     } else {
       L.spring_atomic(S, T, c->has_special, c->st);
@@ -1210,6 +1524,7 @@ int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
   if (rc) return rc;
   const Launch &L = launchers(c->prec);
   KState S = make_state(c);
+  if ((rc = upload_state(c, S))) return rc;
   StepP T;
   T.sim_t = sim_t;
   T.dt = 0.0;
@@ -1217,7 +1532,10 @@ int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
   T.cur = c->cur;
   T.write_acc = 0;
   if (accumulation == SL_ACC_GATHER) {
-    L.force_only(S, c->env, T, c->st);
+    if (c->split)
+      L.split_force(S, c->env, T, c->st);
+    else
+      L.force_only(S, c->env, T, c->st);
     c->launches++;
   } else {
     L.spring_atomic(S, T, c->has_special, c->st);

@@ -95,6 +95,19 @@ struct KState {
   const int32_t *ent_s;
   const int64_t *e1, *e2;
   uint8_t *xflags;  // per-mass layout-derived flag bits (MF_SPECIAL)
+  // split layout (tolerance modes, sl_split.cuh); split == 0 => exact layout
+  const KState *self;  // device-memory copy of this struct (rare paths)
+  int split;
+  int fsz8;        // sizeof(F) == 8 (fp64 spring parameters)
+  int sp_a;        // log2 of the A-section row stride
+  int sp_rows;     // rows per slice block (A stride + widest B section)
+  uint32_t sp_sent;  // sentinel mass index (dead / padding A entries)
+  uint32_t sp_null;  // zero (k, L0) cell (dead / padding B entries)
+  uint32_t *sp_j;
+  const void *sp_kl;
+  const int32_t *sp_s;
+  const uint32_t *sp_w;
+  const uint32_t *sp_ekl;  // per spring: kl index of its A cell
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -139,6 +152,14 @@ struct Tr<PREC_MIXED> {
   static constexpr int U = 6;
   static constexpr int UP = 6;
 };
+
+// read-only 16/32-byte loads through the non-coherent path
+__device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ double4 ldg4(const double4 *p) {
+  const double2 a = __ldg((const double2 *)p);
+  const double2 b = __ldg((const double2 *)p + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
 
 __device__ __forceinline__ uint32_t flags_of(float w) {
   return __float_as_uint(w);
@@ -909,6 +930,25 @@ __global__ void __launch_bounds__(384)
   }
 }
 
+// Mark both incidence entries of spring s dead (host-time kills and the
+// atomic variant's yield breaks; no fused step is running concurrently, so
+// the split layout's (k, L0) cell can be zeroed as well).
+__device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
+  if (S.split) {
+    if (S.e1[s] >= 0) {
+      S.sp_j[S.e1[s]] = S.sp_sent;
+      if (S.fsz8)
+        ((double2 *)S.sp_kl)[S.sp_ekl[s]] = make_double2(0.0, 0.0);
+      else
+        ((float2 *)S.sp_kl)[S.sp_ekl[s]] = make_float2(0.f, 0.f);
+    }
+    if (S.e2[s] >= 0) S.sp_j[S.e2[s]] = S.sp_null;
+    return;
+  }
+  if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
+  if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
+}
+
 // Atomic variant, spring side: one thread per spring slot (kernels.py:36-83
 // with the accumulation of the paper's GPU design).
 template <int P, bool SPECIAL>
@@ -954,10 +994,8 @@ __global__ void __launch_bounds__(256)
     if (mag > thr) {
       S.s_alive[s] = 0;
       S.ends[s] = make_int2(-1, -1);
-      if (S.e1) {  // incidence layout present: keep it consistent
-        if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
-        if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
-      }
+      if (S.e1) kill_entries(S, s);  // incidence layout present: keep it
+                                     // consistent
       count(S, 0);
     }
   }
@@ -1001,6 +1039,13 @@ struct Launch {
   void (*spring_atomic)(const KState &, const StepP &, bool special,
                         cudaStream_t);
   void (*mass)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  // split layout (tolerance modes; null for fp64)
+  void (*split)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  void (*split_force)(const KState &, const EnvP &, const StepP &,
+                      cudaStream_t);
+  void (*split_tma)(const KState &, const EnvP &, const StepP &,
+                    const struct SplitCfg &, int grid, cudaStream_t);
+  int (*split_setup)(int smem_bytes);
 };
 
 const Launch &launchers(int prec);

@@ -4,6 +4,43 @@
 // sl_kernels_fp32.cu (FMA contraction allowed: tolerance modes).
 #pragma once
 #include "sl_device.cuh"
+#include "sl_split.cuh"
+
+// gathers issued per batch in the split TMA kernel
+#define SPLIT_U(PREC) ((PREC) == PREC_FP32 ? 8 : 4)
+
+namespace sl {
+// split-layout launchers; the fp64 parity mode never uses the split layout
+template <int P>
+struct SplitLaunch {
+  static void step(const KState &S, const EnvP &E, const StepP &T,
+                   cudaStream_t st, bool force_only) {
+    if (S.m_n <= 0) return;
+    if (force_only)
+      k_split_step<P, true><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
+    else
+      k_split_step<P, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
+  }
+  static void tma(const KState &S, const EnvP &E, const StepP &T,
+                  const SplitCfg &C, int grid, cudaStream_t st) {
+    size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
+    k_split_tma<P, SPLIT_U(P)><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
+  }
+  static int setup(int smem_bytes) {
+    return (int)cudaFuncSetAttribute(
+        k_split_tma<P, SPLIT_U(P)>,
+        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  }
+};
+template <>
+struct SplitLaunch<PREC_FP64> {
+  static void step(const KState &, const EnvP &, const StepP &, cudaStream_t,
+                   bool) {}
+  static void tma(const KState &, const EnvP &, const StepP &,
+                  const SplitCfg &, int, cudaStream_t) {}
+  static int setup(int) { return 1; }
+};
+}  // namespace sl
 
 #define SL_DEFINE_LAUNCHERS(PREC, FN)                                        \
   namespace sl {                                                             \
@@ -38,10 +75,27 @@
                  cudaStream_t st) {                                          \
     if (S.m_n > 0) k_mass<PREC><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
   }                                                                          \
+  void FN##_split(const KState &S, const EnvP &E, const StepP &T,           \
+                  cudaStream_t st) {                                         \
+    SplitLaunch<PREC>::step(S, E, T, st, false);                             \
+  }                                                                          \
+  void FN##_split_force(const KState &S, const EnvP &E, const StepP &T,     \
+                        cudaStream_t st) {                                   \
+    SplitLaunch<PREC>::step(S, E, T, st, true);                              \
+  }                                                                          \
+  void FN##_split_tma(const KState &S, const EnvP &E, const StepP &T,       \
+                      const SplitCfg &C, int grid, cudaStream_t st) {        \
+    SplitLaunch<PREC>::tma(S, E, T, C, grid, st);                            \
+  }                                                                          \
+  int FN##_split_setup(int smem_bytes) {                                     \
+    return SplitLaunch<PREC>::setup(smem_bytes);                             \
+  }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \
     static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
-                             FN##_force, FN##_spring, FN##_mass};           \
+                             FN##_force, FN##_spring, FN##_mass,             \
+                             FN##_split, FN##_split_force, FN##_split_tma,   \
+                             FN##_split_setup};                              \
     return L;                                                                \
   }                                                                          \
   }

@@ -1,0 +1,343 @@
+// sl_split.cuh -- the "split" (half-duplex) incidence layout and its fused
+// step kernels, used by the tolerance modes (fp32 / mixed).
+//
+// Why: the exact layout of sl_device.cuh stores every spring twice -- once
+// in the incidence list of each endpoint, each copy carrying (k, L0) -- so a
+// step streams 2 x (4 + 8) = 24 B per spring from HBM against the 16 B of
+// algorithmic spring data (i, j, k, L0).  Here each spring
+// keeps (k, L0) once, in the list of its m1 endpoint (section A); the m2
+// endpoint's entry (section B) is a single 32-bit word holding the index of
+// that (k, L0) cell, from which the partner mass is also decoded.  HBM bytes
+// per spring: A word 4 + (k, L0) 8 + B word 4 = 16 -- the algorithmic
+// figure.  The (k, L0) read of a B entry is a gather that hits L2 (the cell
+// was streamed recently by the partner's slice, and the lattice's row-major
+// ordering keeps partners within a few thousand masses).
+//
+// Layout (m_pad = m_n rounded up to 32, n_slices = m_pad / 32, WA = 2^a >=
+// widest A section, WB = widest B section, rows = WA + WB):
+//   sp_j [slice][rows][32] u32  rows [0, WA): A entries = partner mass index
+//                               (sentinel m_pad if dead / padding)
+//                               rows [WA, rows): B entries = kl index of the
+//                               spring's A cell (sp_null if dead / padding)
+//   sp_kl[slice][WA][32] F2     (k, L0) of A entries; kl index of (slice, r,
+//                               lane) = slice << (a+5) | r << 5 | lane, so a
+//                               B word decodes its partner with two ops:
+//                               j = ((w >> a) & ~31) | (w & 31)
+//   sp_s [slice][rows][32] i32  spring slot of every entry (special path)
+//   sp_w [slice] u32            wA | wB << 16 (this slice's section widths;
+//                               only these rows are streamed)
+// Slice n_slices of sp_kl is all zero (sp_null points into it) and mass
+// records [m_pad, m_pad + 32) hold a far-away sentinel position, so dead and
+// padding entries contribute exactly 0 force (k = 0 at a finite distance)
+// without a branch.
+//
+// Fast path (masses without actuated / breakable springs): branch-free
+// k (|d| - L0) / |d| * d with one MUFU.RSQ.  A zero-length alive spring
+// makes the sum non-finite (0 * inf); such a mass -- like a genuinely
+// non-finite one -- is recomputed through the special path, which owns all
+// side effects (zero-length flag, yield break, counters: kernels.py:50-54,
+// 77-86).  Accumulation order is fixed by the layout (deterministic run to
+// run), not the reference's slot order: tolerance modes only.
+#pragma once
+#include "sl_device.cuh"
+
+namespace sl {
+
+constexpr int SPLIT_MAX_WARPS = 12;  // warps per CTA (register budget)
+constexpr double SENTINEL_POS = 1.0e15;  // |d| finite, k = 0 => force 0
+
+struct SplitCfg {
+  int64_t n_slices;
+  int cap_a, cap_b;      // widest sections (stage capacity, rows)
+  int warps;             // warps per CTA
+  uint32_t stage_bytes;  // pos + vel + A words + B words + A (k, L0)
+};
+
+__device__ __forceinline__ uint32_t split_partner(uint32_t w, int a) {
+  return ((w >> a) & ~31u) | (w & 31u);
+}
+
+// Force on this mass from one entry, fast form (see header comment).
+template <int P>
+__device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
+                                           typename Tr<P>::R4 o,
+                                           typename Tr<P>::F2 kl,
+                                           typename Tr<P>::R &fx,
+                                           typename Tr<P>::R &fy,
+                                           typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using M = typename Tr<P>::M;
+  const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+  const M len2 = dx * dx + dy * dy + dz * dz;
+  M r;
+  if constexpr (P == PREC_FP32) {
+    r = rsqrtf(len2);
+  } else {
+    r = (double)rsqrtf((float)len2);
+    r = r * (1.5 - 0.5 * len2 * r * r);  // one Newton step, ~1e-14
+  }
+  const M sc = (M)kl.x * (len2 * r - (M)kl.y) * r;
+  fx += (R)(sc * dx);
+  fy += (R)(sc * dy);
+  fz += (R)(sc * dz);
+}
+
+// Fast spring forces of one mass.  ja / jb / kla point at the lane's first
+// A word, B word and A (k, L0) (lane-strided by 32; shared-memory stage or
+// global memory); wa / wb are the slice's section widths.
+template <int P, int U>
+__device__ __forceinline__ void split_fast(const KState &S,
+                                           const typename Tr<P>::R4 *pos,
+                                           const uint32_t *ja,
+                                           const uint32_t *jb,
+                                           const typename Tr<P>::F2 *kla,
+                                           int wa, int wb,
+                                           typename Tr<P>::R4 me,
+                                           typename Tr<P>::R &fx,
+                                           typename Tr<P>::R &fy,
+                                           typename Tr<P>::R &fz) {
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const F2 *gkl = (const F2 *)S.sp_kl;
+  const int a = S.sp_a;
+  // section A: partner index + (k, L0) from the stage
+  for (int t = 0; t < wa; t += U) {
+    R4 o[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u < wa) split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
+  }
+  // section B: (k, L0) gathered from the partner's A cell (L2)
+  for (int t = 0; t < wb; t += U) {
+    R4 o[U];
+    F2 kl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u < wb) {
+        const uint32_t w = jb[32 * (t + u)];
+        kl[u] = __ldg(gkl + w);
+        o[u] = ldg4(pos + split_partner(w, a));
+      }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
+  }
+}
+
+// One entry through the full reference semantics (kernels.py:46-83):
+// actuation factor, zero-length flag, yield break.  Side effects on the
+// spring (alive flag, counters, zero-length flag) are made once, by the m1
+// endpoint (section A); each endpoint marks only its own entry dead, both
+// reaching the same decision from bit-identical inputs (d and -d square to
+// the same bits).
+template <int P>
+__device__ __forceinline__ void split_entry_exact(
+    const KState *S, int64_t e, bool side_b, typename Tr<P>::R4 me,
+    typename Tr<P>::R4 other, typename Tr<P>::F2 kl, double sim_t,
+    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  using F = typename Tr<P>::M;
+  using FS = typename Tr<P>::F;
+  const F dx = (F)(other.x - me.x), dy = (F)(other.y - me.y),
+          dz = (F)(other.z - me.z);
+  const F len2 = dx * dx + dy * dy + dz * dz;
+  const int32_t s = S->sp_s[e];
+  if (len2 == (F)0.0) {
+    if (!side_b && !S->s_degen[s]) {
+      S->s_degen[s] = 1;
+      atomicAdd(S->status + 2, 1ull);
+    }
+    return;
+  }
+  const int mode = S->mode[s];
+  F factor = (F)1.0;
+  if (mode != 0) factor = (F)act_factor(*S, s, sim_t);
+  const F len = sqrt(len2);
+  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
+  const F scale = fmag / len;
+  fx += (R)(scale * dx);
+  fy += (R)(scale * dy);
+  fz += (R)(scale * dz);
+  const F thr = (F)((const FS *)S->thr)[s];
+  const F mag = fmag >= (F)0.0 ? fmag : -fmag;
+  if (mag > thr) {
+    S->sp_j[e] = side_b ? S->sp_null : S->sp_sent;
+    if (!side_b) {
+      S->s_alive[s] = 0;
+      S->ends[s] = make_int2(-1, -1);
+      atomicAdd(S->status + 0, 1ull);
+    }
+  }
+}
+
+// Rare path, kept out of line; it reads the context state through the
+// device-memory copy (S.self) so the kernel never spills its parameter block
+// to the stack.
+template <int P>
+__device__ __noinline__ void split_special(
+    const KState *S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
+    const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
+    int64_t ea, int64_t eb, typename Tr<P>::R4 me, double sim_t,
+    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+  using F2 = typename Tr<P>::F2;
+  const F2 *gkl = (const F2 *)S->sp_kl;
+  const uint32_t sent = S->sp_sent, nul = S->sp_null;
+  const int a = S->sp_a;
+  for (int t = 0; t < wa; t++) {
+    const uint32_t j = ja[32 * t];
+    if (j == sent) continue;
+    split_entry_exact<P>(S, ea + 32 * (int64_t)t, false, me, pos[j],
+                         kla[32 * t], sim_t, fx, fy, fz);
+  }
+  for (int t = 0; t < wb; t++) {
+    const uint32_t w = jb[32 * t];
+    if (w == nul) continue;
+    split_entry_exact<P>(S, eb + 32 * (int64_t)t, true, me,
+                         pos[split_partner(w, a)], gkl[w], sim_t, fx, fy,
+                         fz);
+  }
+}
+
+template <int P, int U>
+__device__ __forceinline__ void split_forces(
+    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
+    const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
+    int64_t ea, int64_t eb, uint32_t fl, typename Tr<P>::R4 me,
+    double sim_t, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
+    typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
+  if (!(fl & MF_SPECIAL)) {
+    R gx = fx, gy = fy, gz = fz;
+    split_fast<P, U>(S, pos, ja, jb, kla, wa, wb, me, gx, gy, gz);
+    if (isfinite(gx + gy + gz)) {
+      fx = gx;
+      fy = gy;
+      fz = gz;
+      return;
+    }
+  }
+  split_special<P>(S.self, pos, ja, jb, kla, wa, wb, ea, eb, me, sim_t, fx,
+                   fy, fz);
+}
+
+// Plain variant: one thread per mass, entries read from global memory.
+// Serves spring_pass (FORCE_ONLY) and layouts too wide for the TMA stages.
+template <int P, bool FORCE_ONLY>
+__global__ void __launch_bounds__(256)
+    k_split_step(const KState S, const EnvP E, const StepP T) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  if (!FORCE_ONLY && stopped(S, T.step)) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const R4 v = ((const R4 *)S.vel)[i];
+  const uint32_t fl = flags_of(v.w);
+  if (!(fl & MF_ALIVE)) return;
+  const R4 me = pos[i];
+  R fx, fy, fz;
+  initial_force<P>(S, i, fl, FORCE_ONLY, fx, fy, fz);
+  const int64_t w = i >> 5;
+  const uint32_t wd = __ldg(S.sp_w + w);
+  const int64_t ea = w * S.sp_rows * 32 + (i & 31);
+  const int64_t eb = ea + ((int64_t)32 << S.sp_a);
+  const F2 *kla = (const F2 *)S.sp_kl + ((w << (S.sp_a + 5)) | (i & 31));
+  split_forces<P, 4>(S, pos, S.sp_j + ea, S.sp_j + eb, kla, wd & 0xFFFF,
+                     wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
+  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
+}
+
+// TMA-pipelined fused step on the split layout (production path of the
+// tolerance modes).  Same skeleton as k_gather_tma: persistent CTAs, each
+// warp owns a strided sequence of 32-mass slices and a private 2-stage
+// shared-memory ring; lane 0 streams the next slice (pos, vel, A words,
+// B words, A (k, L0): five bulk async copies on one mbarrier) while the warp
+// computes the current one.
+template <int P, int U>
+__global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
+    k_split_tma(const KState S, const EnvP E, const StepP T,
+                const SplitCfg C) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  extern __shared__ __align__(128) unsigned char smem[];
+  if (stopped(S, T.step)) return;  // uniform across the grid
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char *ring = smem + (size_t)warp * 2 * C.stage_bytes;
+  uint64_t *bars =
+      (uint64_t *)(smem + (size_t)C.warps * 2 * C.stage_bytes) + 2 * warp;
+  constexpr uint32_t MB = 32 * sizeof(R4);
+  const uint32_t ja_off = 2 * MB;
+  const uint32_t jb_off = ja_off + (uint32_t)C.cap_a * 128u;
+  const uint32_t kl_off = jb_off + (uint32_t)C.cap_b * 128u;
+  if (lane == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const int a = S.sp_a;
+  const int64_t rows32 = (int64_t)S.sp_rows * 32;
+  const int64_t stride = (int64_t)gridDim.x * C.warps;
+  int64_t s = (int64_t)blockIdx.x * C.warps + warp;
+  uint32_t wcur = 0, wnxt = 0;  // lane 0: widths of current / next slice
+  auto issue = [&](int64_t sl, uint32_t wd, int stage) {
+    const uint32_t wa = wd & 0xFFFF, wb = wd >> 16;
+    unsigned char *dst = ring + (size_t)stage * C.stage_bytes;
+    mbar_expect_tx(bars + stage,
+                   2 * MB + (wa + wb) * 128u + wa * 32u * (uint32_t)sizeof(F2));
+    bulk_g2s(dst, pos + sl * 32, MB, bars + stage);
+    bulk_g2s(dst + MB, (const R4 *)S.vel + sl * 32, MB, bars + stage);
+    const uint32_t *jsl = S.sp_j + sl * rows32;
+    if (wa) {
+      bulk_g2s(dst + ja_off, jsl, wa * 128u, bars + stage);
+      bulk_g2s(dst + kl_off, (const F2 *)S.sp_kl + (sl << (a + 5)),
+               wa * 32u * (uint32_t)sizeof(F2), bars + stage);
+    }
+    if (wb)
+      bulk_g2s(dst + jb_off, jsl + ((int64_t)32 << a), wb * 128u,
+               bars + stage);
+  };
+  if (lane == 0 && s < C.n_slices) {
+    wcur = __ldg(S.sp_w + s);
+    issue(s, wcur, 0);
+    if (s + stride < C.n_slices) wnxt = __ldg(S.sp_w + s + stride);
+  }
+  for (int k = 0; s < C.n_slices; s += stride, k++) {
+    const int stage = k & 1;
+    const uint32_t wd = __shfl_sync(0xffffffffu, wcur, 0);
+    if (lane == 0 && s + stride < C.n_slices) {
+      fence_proxy_async();  // generic reads of that stage finished (syncwarp)
+      issue(s + stride, wnxt, stage ^ 1);
+      wcur = wnxt;
+      if (s + 2 * stride < C.n_slices) wnxt = __ldg(S.sp_w + s + 2 * stride);
+    }
+    const int64_t i = s * 32 + lane;
+    const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
+    mbar_wait(bars + stage, (uint32_t)((k >> 1) & 1));
+    if (i < S.m_n) {
+      const R4 v = ((const R4 *)(st + MB))[lane];
+      const uint32_t fl = flags_of(v.w);
+      if (fl & MF_ALIVE) {
+        const R4 me = ((const R4 *)st)[lane];
+        R fx, fy, fz;
+        initial_force<P>(S, i, fl, false, fx, fy, fz);
+        const int64_t ea = s * rows32 + lane;
+        const int64_t eb = ea + ((int64_t)32 << a);
+        split_forces<P, U>(S, pos, (const uint32_t *)(st + ja_off) + lane,
+                           (const uint32_t *)(st + jb_off) + lane,
+                           (const F2 *)(st + kl_off) + lane, wd & 0xFFFF,
+                           wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
+        finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace sl
