@@ -795,24 +795,53 @@ int build_exact_layout(sl_ctx *c) {
 }
 
 
-// Size the per-warp rings of the split TMA kernel for the widest sections.
-void configure_split_tma(sl_ctx *c) {
+// Size the per-warp rings of the split TMA kernel and pick its gather batch
+// U: every section is processed in whole batches of U rows (the stage pads
+// the tail with zero-force rows), so U trades padded rows against exposed
+// gather latency (one L2 round trip per batch).  Cost model per slice:
+// padded rows + 3 x batches.
+void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->split_warps = 0;
   if (!c->tma_enabled || c->n_slices == 0) return;
-  const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(c->sp_wa + c->sp_wb) * 128 +
-                       (size_t)c->sp_wa * 32 * 2 * c->fsz;
+  const int cands_fp32[] = {4, 8, 13}, cands_mixed[] = {4, 8};
+  const int *cands = c->prec == PREC_FP32 ? cands_fp32 : cands_mixed;
+  const int n_cands = c->prec == PREC_FP32 ? 3 : 2;
+  int best_u = 4;
+  double best = 1e300;
+  for (int q = 0; q < n_cands; q++) {
+    const int u = cands[q];
+    double cost = 0;
+    for (uint32_t wd : widths) {
+      const int wa = wd & 0xFFFF, wb = wd >> 16;
+      const int ba = (wa + u - 1) / u, bb = (wb + u - 1) / u;
+      cost += (double)(ba + bb) * u + 3.0 * (ba + bb);
+    }
+    if (cost < best) {
+      best = cost;
+      best_u = u;
+    }
+  }
+  const int u = best_u;
+  const int64_t cap_a = (c->sp_wa + u - 1) / u * u;
+  const int64_t cap_b = (c->sp_wb + u - 1) / u * u;
+  const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(cap_a + cap_b) * 128 +
+                       (size_t)cap_a * 32 * 2 * c->fsz;
   const size_t per_warp = 2 * stage + 16;
   int warps = (int)std::min<size_t>(SPLIT_MAX_WARPS,
                                      (size_t)c->smem_optin / per_warp);
   if (warps < 2) return;
   c->scfg.n_slices = c->n_slices;
-  c->scfg.cap_a = (int)c->sp_wa;
-  c->scfg.cap_b = (int)c->sp_wb;
+  c->scfg.u = u;
+  c->scfg.cap_a = (int)cap_a;
+  c->scfg.cap_b = (int)cap_b;
   c->scfg.warps = warps;
   c->scfg.stage_bytes = (uint32_t)stage;
   int64_t ctas = (c->n_slices + warps - 1) / warps;
   c->split_grid = (int)std::min<int64_t>(ctas, c->sm_count);
-  if (launchers(c->prec).split_setup((int)(warps * per_warp)) != 0) return;
+  if (launchers(c->prec).split_setup((int)(warps * per_warp), u) != 0) {
+    cudaGetLastError();
+    return;
+  }
   c->split_warps = warps;
 }
 
@@ -932,12 +961,16 @@ int build_split_layout(sl_ctx *c, bool *used) {
       CKL();
     }
   }
+  std::vector<uint32_t> widths(n_slices);
+  if (n_slices > 0)
+    CK(cudaMemcpyAsync(widths.data(), c->sp_w.p, 4 * n_slices,
+                       cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   c->n_slices = n_slices;
   c->n_entries = (int64_t)meta[2];
   c->max_width = 0;
   c->tma_warps = 0;
-  configure_split_tma(c);
+  configure_split_tma(c, widths);
   c->layout_valid = true;
   c->layout_builds++;
   c->launches += 8;

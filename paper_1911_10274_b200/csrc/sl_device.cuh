@@ -1045,7 +1045,7 @@ struct Launch {
                       cudaStream_t);
   void (*split_tma)(const KState &, const EnvP &, const StepP &,
                     const struct SplitCfg &, int grid, cudaStream_t);
-  int (*split_setup)(int smem_bytes);
+  int (*split_setup)(int smem_bytes, int u);
 };
 
 const Launch &launchers(int prec);

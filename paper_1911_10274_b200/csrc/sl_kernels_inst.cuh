@@ -6,8 +6,6 @@
 #include "sl_device.cuh"
 #include "sl_split.cuh"
 
-// gathers issued per batch in the split TMA kernel
-#define SPLIT_U(PREC) ((PREC) == PREC_FP32 ? 8 : 4)
 
 namespace sl {
 // split-layout launchers; the fp64 parity mode never uses the split layout
@@ -21,15 +19,36 @@ struct SplitLaunch {
     else
       k_split_step<P, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
   }
+  template <int U>
+  static void tma_u(const KState &S, const EnvP &E, const StepP &T,
+                    const SplitCfg &C, int grid, cudaStream_t st) {
+    size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
+    k_split_tma<P, U><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
+  }
   static void tma(const KState &S, const EnvP &E, const StepP &T,
                   const SplitCfg &C, int grid, cudaStream_t st) {
-    size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
-    k_split_tma<P, SPLIT_U(P)><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
+    switch (C.u) {
+      case 4: tma_u<4>(S, E, T, C, grid, st); break;
+      case 8: tma_u<8>(S, E, T, C, grid, st); break;
+      default:
+        if constexpr (P == PREC_FP32) tma_u<13>(S, E, T, C, grid, st);
+        else tma_u<8>(S, E, T, C, grid, st);
+    }
   }
-  static int setup(int smem_bytes) {
+  template <int U>
+  static int setup_u(int smem_bytes) {
     return (int)cudaFuncSetAttribute(
-        k_split_tma<P, SPLIT_U(P)>,
-        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        k_split_tma<P, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        smem_bytes);
+  }
+  static int setup(int smem_bytes, int u) {
+    switch (u) {
+      case 4: return setup_u<4>(smem_bytes);
+      case 8: return setup_u<8>(smem_bytes);
+      default:
+        if constexpr (P == PREC_FP32) return setup_u<13>(smem_bytes);
+        else return setup_u<8>(smem_bytes);
+    }
   }
 };
 template <>
@@ -38,7 +57,7 @@ struct SplitLaunch<PREC_FP64> {
                    bool) {}
   static void tma(const KState &, const EnvP &, const StepP &,
                   const SplitCfg &, int, cudaStream_t) {}
-  static int setup(int) { return 1; }
+  static int setup(int, int) { return 1; }
 };
 }  // namespace sl
 
@@ -87,8 +106,8 @@ struct SplitLaunch<PREC_FP64> {
                       const SplitCfg &C, int grid, cudaStream_t st) {        \
     SplitLaunch<PREC>::tma(S, E, T, C, grid, st);                            \
   }                                                                          \
-  int FN##_split_setup(int smem_bytes) {                                     \
-    return SplitLaunch<PREC>::setup(smem_bytes);                             \
+  int FN##_split_setup(int smem_bytes, int u) {                              \
+    return SplitLaunch<PREC>::setup(smem_bytes, u);                          \
   }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \

@@ -48,7 +48,8 @@ constexpr double SENTINEL_POS = 1.0e15;  // |d| finite, k = 0 => force 0
 
 struct SplitCfg {
   int64_t n_slices;
-  int cap_a, cap_b;      // widest sections (stage capacity, rows)
+  int u;                 // gather batch (rows per batch; stage rows padded)
+  int cap_a, cap_b;      // stage capacity, rows (widest sections padded to u)
   int warps;             // warps per CTA
   uint32_t stage_bytes;  // pos + vel + A words + B words + A (k, L0)
 };
@@ -85,7 +86,7 @@ __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
 // Fast spring forces of one mass.  ja / jb / kla point at the lane's first
 // A word, B word and A (k, L0) (lane-strided by 32; shared-memory stage or
 // global memory); wa / wb are the slice's section widths.
-template <int P, int U>
+template <int P, int U, bool PADDED>
 __device__ __forceinline__ void split_fast(const KState &S,
                                            const typename Tr<P>::R4 *pos,
                                            const uint32_t *ja,
@@ -105,10 +106,11 @@ __device__ __forceinline__ void split_fast(const KState &S,
     R4 o[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
+      if (PADDED || t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wa) split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
+      if (PADDED || t + u < wa)
+        split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
   }
   // section B: (k, L0) gathered from the partner's A cell (L2)
   for (int t = 0; t < wb; t += U) {
@@ -116,14 +118,14 @@ __device__ __forceinline__ void split_fast(const KState &S,
     F2 kl[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wb) {
+      if (PADDED || t + u < wb) {
         const uint32_t w = jb[32 * (t + u)];
         kl[u] = __ldg(gkl + w);
         o[u] = ldg4(pos + split_partner(w, a));
       }
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
+      if (PADDED || t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
   }
 }
 
@@ -176,12 +178,17 @@ __device__ __forceinline__ void split_entry_exact(
 // Rare path, kept out of line; it reads the context state through the
 // device-memory copy (S.self) so the kernel never spills its parameter block
 // to the stack.
+template <class R>
+struct Vec3R {
+  R x, y, z;
+};
+
 template <int P>
-__device__ __noinline__ void split_special(
+__device__ __noinline__ Vec3R<typename Tr<P>::R> split_special(
     const KState *S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
     const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
     int64_t ea, int64_t eb, typename Tr<P>::R4 me, double sim_t,
-    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S->sp_kl;
   const uint32_t sent = S->sp_sent, nul = S->sp_null;
@@ -199,9 +206,10 @@ __device__ __noinline__ void split_special(
                          pos[split_partner(w, a)], gkl[w], sim_t, fx, fy,
                          fz);
   }
+  return {fx, fy, fz};
 }
 
-template <int P, int U>
+template <int P, int U, bool PADDED>
 __device__ __forceinline__ void split_forces(
     const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
     const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
@@ -211,7 +219,7 @@ __device__ __forceinline__ void split_forces(
   using R = typename Tr<P>::R;
   if (!(fl & MF_SPECIAL)) {
     R gx = fx, gy = fy, gz = fz;
-    split_fast<P, U>(S, pos, ja, jb, kla, wa, wb, me, gx, gy, gz);
+    split_fast<P, U, PADDED>(S, pos, ja, jb, kla, wa, wb, me, gx, gy, gz);
     if (isfinite(gx + gy + gz)) {
       fx = gx;
       fy = gy;
@@ -219,8 +227,11 @@ __device__ __forceinline__ void split_forces(
       return;
     }
   }
-  split_special<P>(S.self, pos, ja, jb, kla, wa, wb, ea, eb, me, sim_t, fx,
-                   fy, fz);
+  const Vec3R<R> f = split_special<P>(S.self, pos, ja, jb, kla, wa, wb, ea,
+                                      eb, me, sim_t, fx, fy, fz);
+  fx = f.x;
+  fy = f.y;
+  fz = f.z;
 }
 
 // Plain variant: one thread per mass, entries read from global memory.
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(256)
   const int64_t ea = w * S.sp_rows * 32 + (i & 31);
   const int64_t eb = ea + ((int64_t)32 << S.sp_a);
   const F2 *kla = (const F2 *)S.sp_kl + ((w << (S.sp_a + 5)) | (i & 31));
-  split_forces<P, 4>(S, pos, S.sp_j + ea, S.sp_j + eb, kla, wd & 0xFFFF,
+  split_forces<P, 4, false>(S, pos, S.sp_j + ea, S.sp_j + eb, kla, wd & 0xFFFF,
                      wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
   finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
 }
@@ -319,6 +330,24 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
     }
     const int64_t i = s * 32 + lane;
     const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
+    {
+      // rows between the section widths and the next multiple of U are not
+      // TMA destinations: fill them with zero-force padding so the batches
+      // run without guards
+      const int wa = wd & 0xFFFF, wb = wd >> 16;
+      uint32_t *sja = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
+                                   ja_off) + lane;
+      F2 *skl = (F2 *)(ring + (size_t)stage * C.stage_bytes + kl_off) + lane;
+      F2 zero;
+      zero.x = zero.y = 0;
+      for (int r = wa; r < (wa + U - 1) / U * U; r++) {
+        sja[32 * r] = S.sp_sent;
+        skl[32 * r] = zero;
+      }
+      uint32_t *sjb = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
+                                   jb_off) + lane;
+      for (int r = wb; r < (wb + U - 1) / U * U; r++) sjb[32 * r] = S.sp_null;
+    }
     mbar_wait(bars + stage, (uint32_t)((k >> 1) & 1));
     if (i < S.m_n) {
       const R4 v = ((const R4 *)(st + MB))[lane];
@@ -329,7 +358,7 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
         initial_force<P>(S, i, fl, false, fx, fy, fz);
         const int64_t ea = s * rows32 + lane;
         const int64_t eb = ea + ((int64_t)32 << a);
-        split_forces<P, U>(S, pos, (const uint32_t *)(st + ja_off) + lane,
+        split_forces<P, U, true>(S, pos, (const uint32_t *)(st + ja_off) + lane,
                            (const uint32_t *)(st + jb_off) + lane,
                            (const F2 *)(st + kl_off) + lane, wd & 0xFFFF,
                            wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
