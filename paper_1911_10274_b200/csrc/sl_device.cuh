@@ -820,6 +820,44 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src,
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Warp-collective issue of one stage: every lane calls with the same
+// (warp-uniform) operands, elect.sync picks one lane for the expect_tx
+// arrival and up to five bulk copies (zero-byte copies are skipped).  With
+// uniform operands ptxas keeps them in uniform registers instead of
+// serialising the copies through a per-lane loop.
+__device__ __forceinline__ void bulk_stage_elect(
+    uint64_t *bar, uint32_t tx, void *d0, const void *s0, uint32_t n0,
+    void *d1, const void *s1, uint32_t n1, void *d2, const void *s2,
+    uint32_t n2, void *d3, const void *s3, uint32_t n3, void *d4,
+    const void *s4, uint32_t n4) {
+  asm volatile(
+      "{\n"
+      ".reg .pred E, Q;\n"
+      "elect.sync _|E, 0xffffffff;\n"
+      "@E mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+      "setp.ne.and.u32 Q, %4, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%2], [%3], %4, [%0];\n"
+      "setp.ne.and.u32 Q, %7, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%5], [%6], %7, [%0];\n"
+      "setp.ne.and.u32 Q, %10, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%8], [%9], %10, [%0];\n"
+      "setp.ne.and.u32 Q, %13, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%11], [%12], %13, [%0];\n"
+      "setp.ne.and.u32 Q, %16, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%14], [%15], %16, [%0];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(tx), "r"(smem_u32(d0)), "l"(s0), "r"(n0), "r"(smem_u32(d1)),
+      "l"(s1), "r"(n1), "r"(smem_u32(d2)), "l"(s2), "r"(n2),
+      "r"(smem_u32(d3)), "l"(s3), "r"(n3), "r"(smem_u32(d4)), "l"(s4),
+      "r"(n4)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

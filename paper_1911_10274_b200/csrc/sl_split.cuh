@@ -101,16 +101,47 @@ __device__ __forceinline__ void split_fast(const KState &S,
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S.sp_kl;
   const int a = S.sp_a;
-  // section A: partner index + (k, L0) from the stage
+  if constexpr (PADDED) {
+    // stage rows are padded to whole batches: batch t of section A and
+    // batch t of section B issue all their gathers together (one exposed L2
+    // round trip per pair), then reduce A then B
+    for (int t = 0; t < wa || t < wb; t += U) {
+      R4 oa[U], ob[U];
+      F2 kb[U];
+      const bool has_a = t < wa, has_b = t < wb;  // warp-uniform
+      if (has_a) {
+#pragma unroll
+        for (int u = 0; u < U; u++) oa[u] = ldg4(pos + ja[32 * (t + u)]);
+      }
+      if (has_b) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const uint32_t w = jb[32 * (t + u)];
+          kb[u] = __ldg(gkl + w);
+          ob[u] = ldg4(pos + split_partner(w, a));
+        }
+      }
+      if (has_a) {
+#pragma unroll
+        for (int u = 0; u < U; u++)
+          split_body<P>(me, oa[u], kla[32 * (t + u)], fx, fy, fz);
+      }
+      if (has_b) {
+#pragma unroll
+        for (int u = 0; u < U; u++) split_body<P>(me, ob[u], kb[u], fx, fy, fz);
+      }
+    }
+    return;
+  }
+  // section A: partner index + (k, L0) from the source rows
   for (int t = 0; t < wa; t += U) {
     R4 o[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (PADDED || t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
+      if (t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (PADDED || t + u < wa)
-        split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
+      if (t + u < wa) split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
   }
   // section B: (k, L0) gathered from the partner's A cell (L2)
   for (int t = 0; t < wb; t += U) {
@@ -118,14 +149,14 @@ __device__ __forceinline__ void split_fast(const KState &S,
     F2 kl[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (PADDED || t + u < wb) {
+      if (t + u < wb) {
         const uint32_t w = jb[32 * (t + u)];
         kl[u] = __ldg(gkl + w);
         o[u] = ldg4(pos + split_partner(w, a));
       }
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (PADDED || t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
+      if (t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
   }
 }
 
@@ -277,7 +308,10 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
   using F2 = typename Tr<P>::F2;
   extern __shared__ __align__(128) unsigned char smem[];
   if (stopped(S, T.step)) return;  // uniform across the grid
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: provably warp-uniform for ptxas, so
+  // the stage addresses below live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
   unsigned char *ring = smem + (size_t)warp * 2 * C.stage_bytes;
   uint64_t *bars =
       (uint64_t *)(smem + (size_t)C.warps * 2 * C.stage_bytes) + 2 * warp;
@@ -296,37 +330,33 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
   const int64_t rows32 = (int64_t)S.sp_rows * 32;
   const int64_t stride = (int64_t)gridDim.x * C.warps;
   int64_t s = (int64_t)blockIdx.x * C.warps + warp;
-  uint32_t wcur = 0, wnxt = 0;  // lane 0: widths of current / next slice
+  // whole warp: issue the five bulk copies of slice sl into a stage
   auto issue = [&](int64_t sl, uint32_t wd, int stage) {
     const uint32_t wa = wd & 0xFFFF, wb = wd >> 16;
     unsigned char *dst = ring + (size_t)stage * C.stage_bytes;
-    mbar_expect_tx(bars + stage,
-                   2 * MB + (wa + wb) * 128u + wa * 32u * (uint32_t)sizeof(F2));
-    bulk_g2s(dst, pos + sl * 32, MB, bars + stage);
-    bulk_g2s(dst + MB, (const R4 *)S.vel + sl * 32, MB, bars + stage);
     const uint32_t *jsl = S.sp_j + sl * rows32;
-    if (wa) {
-      bulk_g2s(dst + ja_off, jsl, wa * 128u, bars + stage);
-      bulk_g2s(dst + kl_off, (const F2 *)S.sp_kl + (sl << (a + 5)),
-               wa * 32u * (uint32_t)sizeof(F2), bars + stage);
-    }
-    if (wb)
-      bulk_g2s(dst + jb_off, jsl + ((int64_t)32 << a), wb * 128u,
-               bars + stage);
+    const uint32_t kb = wa * 32u * (uint32_t)sizeof(F2);
+    bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb, dst,
+                     pos + sl * 32, MB, dst + MB, (const R4 *)S.vel + sl * 32,
+                     MB, dst + ja_off, jsl, wa * 128u, dst + kl_off,
+                     (const F2 *)S.sp_kl + (sl << (a + 5)), kb, dst + jb_off,
+                     jsl + ((int64_t)32 << a), wb * 128u);
   };
-  if (lane == 0 && s < C.n_slices) {
-    wcur = __ldg(S.sp_w + s);
-    issue(s, wcur, 0);
-    if (s + stride < C.n_slices) wnxt = __ldg(S.sp_w + s + stride);
-  }
+  // slice widths, loaded by every lane (one transaction) and broadcast
+  auto widths = [&](int64_t sl) {
+    const uint32_t w = sl < C.n_slices ? __ldg(S.sp_w + sl) : 0u;
+    return __shfl_sync(0xffffffffu, w, 0);
+  };
+  uint32_t wcur = widths(s), wnxt = widths(s + stride);
+  if (s < C.n_slices) issue(s, wcur, 0);
   for (int k = 0; s < C.n_slices; s += stride, k++) {
     const int stage = k & 1;
-    const uint32_t wd = __shfl_sync(0xffffffffu, wcur, 0);
-    if (lane == 0 && s + stride < C.n_slices) {
+    const uint32_t wd = wcur;
+    if (s + stride < C.n_slices) {
       fence_proxy_async();  // generic reads of that stage finished (syncwarp)
       issue(s + stride, wnxt, stage ^ 1);
       wcur = wnxt;
-      if (s + 2 * stride < C.n_slices) wnxt = __ldg(S.sp_w + s + 2 * stride);
+      wnxt = widths(s + 2 * stride);
     }
     const int64_t i = s * 32 + lane;
     const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
