@@ -821,14 +821,22 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
       best_u = u;
     }
   }
+  if (const char *ev = getenv("SL_SPLIT_U")) {  // tuning override
+    const int f = atoi(ev);
+    for (int q = 0; q < n_cands; q++)
+      if (cands[q] == f) best_u = f;
+  }
   const int u = best_u;
   const int64_t cap_a = (c->sp_wa + u - 1) / u * u;
   const int64_t cap_b = (c->sp_wb + u - 1) / u * u;
   const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(cap_a + cap_b) * 128 +
                        (size_t)cap_a * 32 * 2 * c->fsz;
   const size_t per_warp = 2 * stage + 16;
-  int warps = (int)std::min<size_t>(SPLIT_MAX_WARPS,
-                                     (size_t)c->smem_optin / per_warp);
+  int want = SPLIT_DEFAULT_WARPS;
+  if (const char *ev = getenv("SL_SPLIT_WARPS"))  // tuning override
+    want = std::max(2, std::min(SPLIT_MAX_WARPS, atoi(ev)));
+  int warps = (int)std::min<size_t>((size_t)want,
+                                    (size_t)c->smem_optin / per_warp);
   if (warps < 2) return;
   c->scfg.n_slices = c->n_slices;
   c->scfg.u = u;
@@ -838,7 +846,8 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->scfg.stage_bytes = (uint32_t)stage;
   int64_t ctas = (c->n_slices + warps - 1) / warps;
   c->split_grid = (int)std::min<int64_t>(ctas, c->sm_count);
-  if (launchers(c->prec).split_setup((int)(warps * per_warp), u) != 0) {
+  if (launchers(c->prec).split_setup((int)(warps * per_warp), u, warps) !=
+      0) {
     cudaGetLastError();
     return;
   }

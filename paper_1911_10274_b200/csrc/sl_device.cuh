@@ -1083,7 +1083,7 @@ struct Launch {
                       cudaStream_t);
   void (*split_tma)(const KState &, const EnvP &, const StepP &,
                     const struct SplitCfg &, int grid, cudaStream_t);
-  int (*split_setup)(int smem_bytes, int u);
+  int (*split_setup)(int smem_bytes, int u, int warps);
 };
 
 const Launch &launchers(int prec);

@@ -19,36 +19,49 @@ struct SplitLaunch {
     else
       k_split_step<P, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
   }
-  template <int U>
+  template <int U, int MW>
   static void tma_u(const KState &S, const EnvP &E, const StepP &T,
                     const SplitCfg &C, int grid, cudaStream_t st) {
     size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
-    k_split_tma<P, U><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
+    k_split_tma<P, U, MW><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
+  }
+  template <int MW>
+  static void tma_w(const KState &S, const EnvP &E, const StepP &T,
+                    const SplitCfg &C, int grid, cudaStream_t st) {
+    switch (C.u) {
+      case 4: tma_u<4, MW>(S, E, T, C, grid, st); break;
+      case 8: tma_u<8, MW>(S, E, T, C, grid, st); break;
+      default:
+        if constexpr (P == PREC_FP32) tma_u<13, MW>(S, E, T, C, grid, st);
+        else tma_u<8, MW>(S, E, T, C, grid, st);
+    }
   }
   static void tma(const KState &S, const EnvP &E, const StepP &T,
                   const SplitCfg &C, int grid, cudaStream_t st) {
-    switch (C.u) {
-      case 4: tma_u<4>(S, E, T, C, grid, st); break;
-      case 8: tma_u<8>(S, E, T, C, grid, st); break;
-      default:
-        if constexpr (P == PREC_FP32) tma_u<13>(S, E, T, C, grid, st);
-        else tma_u<8>(S, E, T, C, grid, st);
-    }
+    if (C.warps > 12)
+      tma_w<16>(S, E, T, C, grid, st);
+    else
+      tma_w<12>(S, E, T, C, grid, st);
   }
-  template <int U>
+  template <int U, int MW>
   static int setup_u(int smem_bytes) {
     return (int)cudaFuncSetAttribute(
-        k_split_tma<P, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        k_split_tma<P, U, MW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
         smem_bytes);
   }
-  static int setup(int smem_bytes, int u) {
+  template <int MW>
+  static int setup_w(int smem_bytes, int u) {
     switch (u) {
-      case 4: return setup_u<4>(smem_bytes);
-      case 8: return setup_u<8>(smem_bytes);
+      case 4: return setup_u<4, MW>(smem_bytes);
+      case 8: return setup_u<8, MW>(smem_bytes);
       default:
-        if constexpr (P == PREC_FP32) return setup_u<13>(smem_bytes);
-        else return setup_u<8>(smem_bytes);
+        if constexpr (P == PREC_FP32) return setup_u<13, MW>(smem_bytes);
+        else return setup_u<8, MW>(smem_bytes);
     }
+  }
+  static int setup(int smem_bytes, int u, int warps) {
+    return warps > 12 ? setup_w<16>(smem_bytes, u)
+                      : setup_w<12>(smem_bytes, u);
   }
 };
 template <>
@@ -57,7 +70,7 @@ struct SplitLaunch<PREC_FP64> {
                    bool) {}
   static void tma(const KState &, const EnvP &, const StepP &,
                   const SplitCfg &, int, cudaStream_t) {}
-  static int setup(int, int) { return 1; }
+  static int setup(int, int, int) { return 1; }
 };
 }  // namespace sl
 
@@ -106,8 +119,8 @@ struct SplitLaunch<PREC_FP64> {
                       const SplitCfg &C, int grid, cudaStream_t st) {        \
     SplitLaunch<PREC>::tma(S, E, T, C, grid, st);                            \
   }                                                                          \
-  int FN##_split_setup(int smem_bytes, int u) {                              \
-    return SplitLaunch<PREC>::setup(smem_bytes, u);                          \
+  int FN##_split_setup(int smem_bytes, int u, int warps) {                   \
+    return SplitLaunch<PREC>::setup(smem_bytes, u, warps);                   \
   }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \

@@ -43,7 +43,8 @@
 
 namespace sl {
 
-constexpr int SPLIT_MAX_WARPS = 12;  // warps per CTA (register budget)
+constexpr int SPLIT_MAX_WARPS = 16;  // warps per CTA, upper bound
+constexpr int SPLIT_DEFAULT_WARPS = 12;  // default (register budget)
 constexpr double SENTINEL_POS = 1.0e15;  // |d| finite, k = 0 => force 0
 
 struct SplitCfg {
@@ -299,8 +300,8 @@ __global__ void __launch_bounds__(256)
 // shared-memory ring; lane 0 streams the next slice (pos, vel, A words,
 // B words, A (k, L0): five bulk async copies on one mbarrier) while the warp
 // computes the current one.
-template <int P, int U>
-__global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
+template <int P, int U, int MW>
+__global__ void __launch_bounds__(MW * 32)
     k_split_tma(const KState S, const EnvP E, const StepP T,
                 const SplitCfg C) {
   using R = typename Tr<P>::R;
