@@ -102,9 +102,6 @@ struct sl_ctx {
   DevBuf sp_j, sp_kl, sp_s, sp_w, sp_ekl, degB, sp_meta;
   SplitCfg scfg;
   int split_warps = 0, split_grid = 0;
-  PipeCfg pcfg;
-  int pipe_warps = 0, pipe_grid = 0;
-  bool pipe_enabled = true;  // SL_SPLIT_PIPE=0 selects the register kernel
   // device copy of the kernel state block (KState::self)
   DevBuf kdev;
   KState khost;
@@ -803,8 +800,6 @@ int build_exact_layout(sl_ctx *c) {
 // the tail with zero-force rows), so U trades padded rows against exposed
 // gather latency (one L2 round trip per batch).  Cost model per slice:
 // padded rows + 3 x batches.
-void configure_split_pipe(sl_ctx *c);
-
 void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->split_warps = 0;
   if (!c->tma_enabled || c->n_slices == 0) return;
@@ -857,40 +852,6 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
     return;
   }
   c->split_warps = warps;
-  configure_split_pipe(c);
-}
-
-// The gather-pipelined kernel (fp32): three stream stages + two gather
-// stages per warp; used when at least 3 warps fit per SM.
-void configure_split_pipe(sl_ctx *c) {
-  c->pipe_warps = 0;
-  if (!c->pipe_enabled || c->prec != PREC_FP32 || c->n_slices == 0) return;
-  const size_t r4 = 4 * c->rsz;
-  size_t t = 2 * 32 * r4 + (size_t)(c->sp_wa + c->sp_wb) * 128 +
-             (size_t)c->sp_wa * 32 * 2 * c->fsz;
-  size_t g = (size_t)(c->sp_wa + c->sp_wb) * 32 * r4 +
-             (size_t)c->sp_wb * 32 * 2 * c->fsz;
-  t = (t + 127) & ~(size_t)127;
-  g = (g + 127) & ~(size_t)127;
-  const size_t per_warp = 3 * t + 2 * g + 24;
-  int want = 8;
-  if (const char *ev = getenv("SL_PIPE_WARPS")) want = std::max(1, atoi(ev));
-  int warps = (int)std::min<size_t>(std::min(want, 8),
-                                    (size_t)c->smem_optin / per_warp);
-  if (warps < 3) return;
-  c->pcfg.n_slices = c->n_slices;
-  c->pcfg.cap_a = (int)c->sp_wa;
-  c->pcfg.cap_b = (int)c->sp_wb;
-  c->pcfg.warps = warps;
-  c->pcfg.t_bytes = (uint32_t)t;
-  c->pcfg.g_bytes = (uint32_t)g;
-  int64_t ctas = (c->n_slices + warps - 1) / warps;
-  c->pipe_grid = (int)std::min<int64_t>(ctas, c->sm_count);
-  if (launchers(c->prec).pipe_setup((int)(warps * per_warp)) != 0) {
-    cudaGetLastError();
-    return;
-  }
-  c->pipe_warps = warps;
 }
 
 // Device build of the split layout (sl_split.cuh).  *used = false when the
@@ -1118,7 +1079,6 @@ int sl_create(int device, int precision, sl_ctx **out) {
   if (const char *ev = getenv("SL_DISABLE_TMA")) c->tma_enabled = ev[0] == '0';
   if (const char *ev = getenv("SL_DISABLE_SPLIT"))
     c->split_enabled = ev[0] == '0';
-  if (const char *ev = getenv("SL_SPLIT_PIPE")) c->pipe_enabled = ev[0] != '0';
   memset(&c->env, 0, sizeof c->env);
   cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
   if (e == cudaSuccess)
@@ -1569,9 +1529,7 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     T.write_acc = n == n_steps - 1;
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
-        if (c->pipe_warps)
-          L.split_pipe(S, c->env, T, c->pcfg, c->pipe_grid, c->st);
-        else if (c->split_warps)
+        if (c->split_warps)
           L.split_tma(S, c->env, T, c->scfg, c->split_grid, c->st);
         else
           L.split(S, c->env, T, c->st);

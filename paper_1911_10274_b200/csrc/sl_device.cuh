@@ -1084,9 +1084,6 @@ struct Launch {
   void (*split_tma)(const KState &, const EnvP &, const StepP &,
                     const struct SplitCfg &, int grid, cudaStream_t);
   int (*split_setup)(int smem_bytes, int u, int warps);
-  void (*split_pipe)(const KState &, const EnvP &, const StepP &,
-                     const struct PipeCfg &, int grid, cudaStream_t);
-  int (*pipe_setup)(int smem_bytes);
 };
 
 const Launch &launchers(int prec);

@@ -59,21 +59,6 @@ struct SplitLaunch {
         else return setup_u<8, MW>(smem_bytes);
     }
   }
-  static void pipe(const KState &S, const EnvP &E, const StepP &T,
-                   const PipeCfg &C, int grid, cudaStream_t st) {
-    if constexpr (P == PREC_FP32) {
-      size_t sm = (size_t)C.warps * (3 * (size_t)C.t_bytes +
-                                     2 * (size_t)C.g_bytes + 24);
-      k_split_pipe<P><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
-    }
-  }
-  static int pipe_setup(int smem_bytes) {
-    if constexpr (P == PREC_FP32)
-      return (int)cudaFuncSetAttribute(
-          k_split_pipe<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          smem_bytes);
-    return 1;
-  }
   static int setup(int smem_bytes, int u, int warps) {
     return warps > 12 ? setup_w<16>(smem_bytes, u)
                       : setup_w<12>(smem_bytes, u);
@@ -86,9 +71,6 @@ struct SplitLaunch<PREC_FP64> {
   static void tma(const KState &, const EnvP &, const StepP &,
                   const SplitCfg &, int, cudaStream_t) {}
   static int setup(int, int, int) { return 1; }
-  static void pipe(const KState &, const EnvP &, const StepP &,
-                   const PipeCfg &, int, cudaStream_t) {}
-  static int pipe_setup(int) { return 1; }
 };
 }  // namespace sl
 
@@ -140,20 +122,12 @@ struct SplitLaunch<PREC_FP64> {
   int FN##_split_setup(int smem_bytes, int u, int warps) {                   \
     return SplitLaunch<PREC>::setup(smem_bytes, u, warps);                   \
   }                                                                          \
-  void FN##_pipe(const KState &S, const EnvP &E, const StepP &T,            \
-                 const PipeCfg &C, int grid, cudaStream_t st) {              \
-    SplitLaunch<PREC>::pipe(S, E, T, C, grid, st);                           \
-  }                                                                          \
-  int FN##_pipe_setup(int smem_bytes) {                                      \
-    return SplitLaunch<PREC>::pipe_setup(smem_bytes);                        \
-  }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \
     static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
                              FN##_force, FN##_spring, FN##_mass,             \
                              FN##_split, FN##_split_force, FN##_split_tma,   \
-                             FN##_split_setup, FN##_pipe,                    \
-                             FN##_pipe_setup};                               \
+                             FN##_split_setup};                              \
     return L;                                                                \
   }                                                                          \
   }

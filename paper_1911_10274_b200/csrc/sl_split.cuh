@@ -400,191 +400,4 @@ __global__ void __launch_bounds__(MW * 32)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Gather-pipelined fused step (fp32).  The register-gather kernel above is
-// latency-bound: a warp stalls on its own neighbour gathers once per slice.
-// Here the gathers are asynchronous too: for slice k+1 every lane issues
-// 16-byte cp.async copies of its partners' positions (and the B sections'
-// (k, L0) cells) straight into a shared-memory gather stage, while the warp
-// computes slice k out of stages that landed earlier.  Three stream stages
-// (bulk copies, as above) and two gather stages per warp; each lane waits
-// only for its own copies (cp.async groups), since every lane reads back only
-// what it gathered itself.  No registers are held across the latency, so a
-// warp's compute never waits on L2.
-struct PipeCfg {
-  int64_t n_slices;
-  int cap_a, cap_b;
-  int warps;
-  uint32_t t_bytes;  // stream stage: pos, vel, A words, B words, A (k, L0)
-  uint32_t g_bytes;  // gather stage: A partners, B partners, B (k, L0)
-};
-
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
-                   smem_u32(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void *dst, const void *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   smem_u32(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int P>
-__global__ void __launch_bounds__(256, 1)
-    k_split_pipe(const KState S, const EnvP E, const StepP T,
-                 const PipeCfg C) {
-  using R = typename Tr<P>::R;
-  using R4 = typename Tr<P>::R4;
-  using F2 = typename Tr<P>::F2;
-  extern __shared__ __align__(128) unsigned char smem[];
-  if (stopped(S, T.step)) return;
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-  const int lane = threadIdx.x & 31;
-  const size_t per_warp = 3 * (size_t)C.t_bytes + 2 * (size_t)C.g_bytes;
-  unsigned char *tring = smem + (size_t)warp * per_warp;
-  unsigned char *gring = tring + 3 * (size_t)C.t_bytes;
-  uint64_t *bars = (uint64_t *)(smem + (size_t)C.warps * per_warp) + 3 * warp;
-  constexpr uint32_t MB = 32 * sizeof(R4);
-  const uint32_t ja_off = 2 * MB;
-  const uint32_t jb_off = ja_off + (uint32_t)C.cap_a * 128u;
-  const uint32_t kl_off = jb_off + (uint32_t)C.cap_b * 128u;
-  const uint32_t gb_off = (uint32_t)C.cap_a * 32u * sizeof(R4);
-  const uint32_t gk_off = gb_off + (uint32_t)C.cap_b * 32u * sizeof(R4);
-  if (lane == 0) {
-    for (int q = 0; q < 3; q++) mbar_init(bars + q, 1);
-    fence_proxy_async();
-  }
-  __syncwarp();
-  const R4 *pos = (const R4 *)S.pos[T.cur];
-  const F2 *gkl = (const F2 *)S.sp_kl;
-  const int a = S.sp_a;
-  const int64_t rows32 = (int64_t)S.sp_rows * 32;
-  const int64_t stride = (int64_t)gridDim.x * C.warps;
-  const int64_t s0 = (int64_t)blockIdx.x * C.warps + warp;
-  auto slice = [&](int64_t k) { return s0 + k * stride; };
-  auto widths = [&](int64_t sl) {
-    const uint32_t w = sl < C.n_slices ? __ldg(S.sp_w + sl) : 0u;
-    return __shfl_sync(0xffffffffu, w, 0);
-  };
-  auto issue = [&](int64_t sl, uint32_t wd, int stage) {
-    const uint32_t wa = wd & 0xFFFF, wb = wd >> 16;
-    unsigned char *dst = tring + (size_t)stage * C.t_bytes;
-    const uint32_t *jsl = S.sp_j + sl * rows32;
-    const uint32_t kb = wa * 32u * (uint32_t)sizeof(F2);
-    bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb, dst,
-                     pos + sl * 32, MB, dst + MB, (const R4 *)S.vel + sl * 32,
-                     MB, dst + ja_off, jsl, wa * 128u, dst + kl_off,
-                     (const F2 *)S.sp_kl + (sl << (a + 5)), kb, dst + jb_off,
-                     jsl + ((int64_t)32 << a), wb * 128u);
-  };
-  // this lane's partner gathers of one slice: stream stage -> gather stage
-  auto gather = [&](uint32_t wd, int tst, int gst) {
-    const int wa = wd & 0xFFFF, wb = wd >> 16;
-    const unsigned char *ts = tring + (size_t)tst * C.t_bytes;
-    unsigned char *gs = gring + (size_t)gst * C.g_bytes;
-    const uint32_t *ja = (const uint32_t *)(ts + ja_off) + lane;
-    const uint32_t *jb = (const uint32_t *)(ts + jb_off) + lane;
-    R4 *ga = (R4 *)gs + lane;
-    R4 *gb = (R4 *)(gs + gb_off) + lane;
-    F2 *gk = (F2 *)(gs + gk_off) + lane;
-#pragma unroll 4
-    for (int r = 0; r < wa; r++) cp_async16(ga + 32 * r, pos + ja[32 * r]);
-#pragma unroll 4
-    for (int r = 0; r < wb; r++) {
-      const uint32_t w = jb[32 * r];
-      cp_async16(gb + 32 * r, pos + split_partner(w, a));
-      cp_async8(gk + 32 * r, gkl + w);
-    }
-    cp_async_commit();
-  };
-  uint32_t w0 = widths(slice(0)), w1 = widths(slice(1)), w2 = widths(slice(2));
-  if (slice(0) < C.n_slices) issue(slice(0), w0, 0);
-  if (slice(1) < C.n_slices) issue(slice(1), w1, 1);
-  if (slice(0) < C.n_slices) {
-    mbar_wait(bars + 0, 0);
-    gather(w0, 0, 0);
-  }
-  for (int64_t k = 0; slice(k) < C.n_slices; k++) {
-    const int64_t s = slice(k);
-    const int tst = (int)(k % 3), gst = (int)(k & 1);
-    const uint32_t wd = w0;
-    if (slice(k + 1) < C.n_slices) {
-      const int t1 = (int)((k + 1) % 3);
-      mbar_wait(bars + t1, (uint32_t)(((k + 1) / 3) & 1));
-      if (slice(k + 2) < C.n_slices) {
-        fence_proxy_async();
-        issue(slice(k + 2), w2, (int)((k + 2) % 3));
-      }
-      gather(w1, t1, gst ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    w0 = w1;
-    w1 = w2;
-    w2 = widths(slice(k + 3));
-    const int64_t i = s * 32 + lane;
-    const unsigned char *ts = tring + (size_t)tst * C.t_bytes;
-    const unsigned char *gs = gring + (size_t)gst * C.g_bytes;
-    if (i < S.m_n) {
-      const R4 v = ((const R4 *)(ts + MB))[lane];
-      const uint32_t fl = flags_of(v.w);
-      if (fl & MF_ALIVE) {
-        const R4 me = ((const R4 *)ts)[lane];
-        R fx, fy, fz;
-        initial_force<P>(S, i, fl, false, fx, fy, fz);
-        const int wa = wd & 0xFFFF, wb = wd >> 16;
-        const uint32_t *ja = (const uint32_t *)(ts + ja_off) + lane;
-        const uint32_t *jb = (const uint32_t *)(ts + jb_off) + lane;
-        const F2 *kla = (const F2 *)(ts + kl_off) + lane;
-        bool done = false;
-        if (!(fl & MF_SPECIAL)) {
-          const R4 *ga = (const R4 *)gs + lane;
-          const R4 *gb = (const R4 *)(gs + gb_off) + lane;
-          const F2 *gk = (const F2 *)(gs + gk_off) + lane;
-          R ax = fx, ay = fy, az = fz, bx = 0, by = 0, bz = 0;
-#pragma unroll 4
-          for (int r = 0; r < wa; r++)
-            split_body<P>(me, ga[32 * r], kla[32 * r], ax, ay, az);
-#pragma unroll 4
-          for (int r = 0; r < wb; r++)
-            split_body<P>(me, gb[32 * r], gk[32 * r], bx, by, bz);
-          ax += bx;
-          ay += by;
-          az += bz;
-          if (isfinite(ax + ay + az)) {
-            fx = ax;
-            fy = ay;
-            fz = az;
-            done = true;
-          }
-        }
-        if (!done) {
-          const int64_t ea = s * rows32 + lane;
-          const int64_t eb = ea + ((int64_t)32 << a);
-          const Vec3R<R> f = split_special<P>(S.self, pos, ja, jb, kla, wa,
-                                              wb, ea, eb, me, T.sim_t, fx,
-                                              fy, fz);
-          fx = f.x;
-          fy = f.y;
-          fz = f.z;
-        }
-        finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
-      }
-    }
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-}
-
 }  // namespace sl
