@@ -902,6 +902,7 @@ int build_split_layout(sl_ctx *c, bool *used) {
   // encodings: 16-bit widths, 32-bit kl indices (incl. the zero slice)
   if (wa > 0xFFFF || wb > 0xFFFF || a > 16 ||
       ((n_slices + 1) << (a + 5)) >= ((int64_t)1 << 32) ||
+      n_slices * rows * 32 >= ((int64_t)1 << 32) ||
       // footprint guard for hub masses: stride padding must not explode
       n_slices * rows * 32 > 4 * (int64_t)meta[2] + (1 << 20))
     return SL_OK;

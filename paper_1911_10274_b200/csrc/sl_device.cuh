@@ -315,7 +315,17 @@ __device__ __forceinline__ void integrate(
       fz += sc * ddz;
     }
   }
-  const R ax = fx / mm, ay = fy / mm, az = fz / mm;
+  R ax, ay, az;
+  if constexpr (P == PREC_FP64) {  // parity: three true divisions
+    ax = fx / mm;
+    ay = fy / mm;
+    az = fz / mm;
+  } else {  // tolerance modes: one correctly rounded reciprocal
+    const R im = (R)1.0 / mm;
+    ax = fx * im;
+    ay = fy * im;
+    az = fz * im;
+  }
   const R dt = (R)T.dt;
   vx += ax * dt;
   vy += ay * dt;
@@ -370,9 +380,10 @@ __device__ __forceinline__ void integrate(
     a[1] = ay;
     a[2] = az;
   }
-  if (!(isfinite(px) && isfinite(py) && isfinite(pz) && isfinite(vx) &&
-        isfinite(vy) && isfinite(vz)))
-    mark_nonfinite(S, i, T.step);
+  // x * 0 is 0 for finite x and NaN for +-inf / NaN
+  const R z0 = px * (R)0.0 + py * (R)0.0 + pz * (R)0.0 + vx * (R)0.0 +
+               vy * (R)0.0 + vz * (R)0.0;
+  if (!(z0 == (R)0.0)) mark_nonfinite(S, i, T.step);
 }
 
 template <int P>

@@ -98,6 +98,7 @@ __device__ __forceinline__ void split_fast(const KState &S,
                                            typename Tr<P>::R &fx,
                                            typename Tr<P>::R &fy,
                                            typename Tr<P>::R &fz) {
+  using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S.sp_kl;
@@ -106,6 +107,8 @@ __device__ __forceinline__ void split_fast(const KState &S,
     // stage rows are padded to whole batches: batch t of section A and
     // batch t of section B issue all their gathers together (one exposed L2
     // round trip per pair), then reduce A then B
+    // B sums into its own accumulators: two independent FFMA chains
+    R bx = 0, by = 0, bz = 0;
     for (int t = 0; t < wa || t < wb; t += U) {
       R4 oa[U], ob[U];
       F2 kb[U];
@@ -129,9 +132,12 @@ __device__ __forceinline__ void split_fast(const KState &S,
       }
       if (has_b) {
 #pragma unroll
-        for (int u = 0; u < U; u++) split_body<P>(me, ob[u], kb[u], fx, fy, fz);
+        for (int u = 0; u < U; u++) split_body<P>(me, ob[u], kb[u], bx, by, bz);
       }
     }
+    fx += bx;
+    fy += by;
+    fz += bz;
     return;
   }
   // section A: partner index + (k, L0) from the source rows
@@ -332,16 +338,21 @@ __global__ void __launch_bounds__(MW * 32)
   const int64_t stride = (int64_t)gridDim.x * C.warps;
   int64_t s = (int64_t)blockIdx.x * C.warps + warp;
   // whole warp: issue the five bulk copies of slice sl into a stage
+  // 32-bit element offsets (the layout build guarantees they fit)
+  const uint32_t rows32u = (uint32_t)rows32;
+  const uint32_t jb_rel = 32u << a;
   auto issue = [&](int64_t sl, uint32_t wd, int stage) {
+    const uint32_t su = (uint32_t)sl;
     const uint32_t wa = wd & 0xFFFF, wb = wd >> 16;
-    unsigned char *dst = ring + (size_t)stage * C.stage_bytes;
-    const uint32_t *jsl = S.sp_j + sl * rows32;
+    unsigned char *dst = ring + (stage ? C.stage_bytes : 0u);
+    const uint32_t *jsl = S.sp_j + su * rows32u;
     const uint32_t kb = wa * 32u * (uint32_t)sizeof(F2);
     bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb, dst,
-                     pos + sl * 32, MB, dst + MB, (const R4 *)S.vel + sl * 32,
-                     MB, dst + ja_off, jsl, wa * 128u, dst + kl_off,
-                     (const F2 *)S.sp_kl + (sl << (a + 5)), kb, dst + jb_off,
-                     jsl + ((int64_t)32 << a), wb * 128u);
+                     pos + su * 32u, MB, dst + MB,
+                     (const R4 *)S.vel + su * 32u, MB, dst + ja_off, jsl,
+                     wa * 128u, dst + kl_off,
+                     (const F2 *)S.sp_kl + (su << (a + 5)), kb, dst + jb_off,
+                     jsl + jb_rel, wb * 128u);
   };
   // slice widths, loaded by every lane (one transaction) and broadcast
   auto widths = [&](int64_t sl) {
@@ -349,6 +360,8 @@ __global__ void __launch_bounds__(MW * 32)
     return __shfl_sync(0xffffffffu, w, 0);
   };
   uint32_t wcur = widths(s), wnxt = widths(s + stride);
+  uint32_t wraw = s + 2 * stride < C.n_slices ? __ldg(S.sp_w + s + 2 * stride)
+                                               : 0u;  // one more in flight
   if (s < C.n_slices) issue(s, wcur, 0);
   for (int k = 0; s < C.n_slices; s += stride, k++) {
     const int stage = k & 1;
@@ -356,9 +369,10 @@ __global__ void __launch_bounds__(MW * 32)
     if (s + stride < C.n_slices) {
       fence_proxy_async();  // generic reads of that stage finished (syncwarp)
       issue(s + stride, wnxt, stage ^ 1);
-      wcur = wnxt;
-      wnxt = widths(s + 2 * stride);
     }
+    wcur = wnxt;
+    wnxt = __shfl_sync(0xffffffffu, wraw, 0);
+    wraw = s + 3 * stride < C.n_slices ? __ldg(S.sp_w + s + 3 * stride) : 0u;
     const int64_t i = s * 32 + lane;
     const unsigned char *st = ring + (size_t)stage * C.stage_bytes;
     {
