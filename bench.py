@@ -41,7 +41,7 @@ PAPER_RATE = 3.0e8  # PAPER.md:10,20 headline (Titan X); north_star x50 base
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=100, help="lattice edge")
@@ -133,7 +133,7 @@ class ClockSampler:
                  "clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -271,7 +271,13 @@ def main():
     done, err = mir.ctx.step(times(args.steps), dt, acc, counters)
     ms = mir.ctx.timer_stop()
     clk = clocks.stop()
-    launches = mir.ctx.stats()["kernel_launches"] - launches0
+    stats = mir.ctx.stats()
+    launches = stats["kernel_launches"] - launches0
+    from paper_1911_10274_b200._native import STEP_PATHS
+    kernel = (STEP_PATHS.get(stats["step_path"], "?")
+              if args.accumulation == "gather" else "k_spring_atomic+k_mass")
+    if stats.get("split_batch"):
+        kernel += f" (U={stats['split_batch']})"
     if err:
         raise SystemExit(f"numerical abort at step {done}")
     sec = ms / 1e3
@@ -295,8 +301,7 @@ def main():
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "peak_kind": peak_kind, "algorithmic_bytes_per_step": algo,
             "bytes_per_spring_update": algo / springs,
-            "kernel": "k_gather_step" if args.accumulation == "gather"
-            else "k_spring_atomic+k_mass"}
+            "kernel": kernel}
 
     # e2e through the public API, host store authoritative at both ends
     e2e = None

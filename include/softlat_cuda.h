@@ -67,7 +67,16 @@ typedef struct sl_stats {
   int64_t kernel_launches; /* kernels launched by the context so far        */
   int32_t precision;
   int32_t device;
+  int32_t step_path;   /* fused gather kernel in use: SL_PATH_*             */
+  int32_t split_batch; /* gather batch U of the split TMA kernel (0 = n/a) */
 } sl_stats;
+
+/* sl_stats.step_path */
+#define SL_PATH_NONE 0        /* no incidence layout built yet              */
+#define SL_PATH_EXACT 1       /* exact layout, one thread per mass          */
+#define SL_PATH_EXACT_TMA 2   /* exact layout, TMA-pipelined (k_gather_tma) */
+#define SL_PATH_SPLIT 3       /* split layout, one thread per mass          */
+#define SL_PATH_SPLIT_TMA 4   /* split layout, TMA-pipelined (k_split_tma)  */
 
 /* ---------------------------------------------------------------- lifecycle */
 int sl_abi_version(void);

@@ -39,7 +39,11 @@ class SlStats(C.Structure):
                 ("alive_springs", C.c_int64), ("entries", C.c_int64),
                 ("slices", C.c_int64), ("layout_builds", C.c_int64),
                 ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
-                ("precision", C.c_int32), ("device", C.c_int32)]
+                ("precision", C.c_int32), ("device", C.c_int32),
+                ("step_path", C.c_int32), ("split_batch", C.c_int32)]
+
+STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
+              3: "k_split_step", 4: "k_split_tma"}
 
 
 _lib = None

@@ -1151,6 +1151,11 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
   o->kernel_launches = c->launches;
   o->precision = c->prec;
   o->device = c->device;
+  o->step_path = !c->layout_valid ? SL_PATH_NONE
+                 : c->split       ? (c->split_warps ? SL_PATH_SPLIT_TMA
+                                                    : SL_PATH_SPLIT)
+                 : (c->tma_warps ? SL_PATH_EXACT_TMA : SL_PATH_EXACT);
+  o->split_batch = c->split && c->split_warps ? c->scfg.u : 0;
   const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc,
                           &c->fext, &c->load, &c->m_gen, &c->m_alive,
                           &c->ends, &c->kL0, &c->s_alive, &c->s_degen,
