@@ -166,6 +166,19 @@ int sl_step(sl_ctx *ctx, int64_t n_steps, const double *sim_times, double dt,
             int accumulation, int64_t *counters, int64_t *err_slot,
             int64_t *steps_done);
 
+/* Asynchronous stepping (partitioned runs, partition.py): enqueue n_steps
+ * on the context's stream and return at once; successive calls continue
+ * the same run (step indices and status accumulate) until sl_step_finish
+ * synchronises and reports exactly what sl_step would have for the
+ * concatenated steps.  Between calls the caller may enqueue its own work
+ * on the context stream (sl_get_stream), e.g. a halo exchange that
+ * rewrites ghost positions in the buffer the next step reads
+ * (sl_state_pointers). */
+int sl_step_async(sl_ctx *ctx, int64_t n_steps, const double *sim_times,
+                  double dt, int accumulation);
+int sl_step_finish(sl_ctx *ctx, int64_t *counters, int64_t *err_slot,
+                   int64_t *steps_done);
+
 /* Single spring pass only (engine.spring_pass, engine.py:158-202): spring
  * forces are added into the device f_ext accumulator. */
 int sl_spring_pass(sl_ctx *ctx, double sim_t, int accumulation,
@@ -187,6 +200,20 @@ int sl_download_springs(sl_ctx *ctx, uint8_t *alive, uint8_t *degen);
 int sl_snapshot_begin(sl_ctx *ctx);
 int sl_snapshot_ready(sl_ctx *ctx, int *ready);
 int sl_snapshot_wait(sl_ctx *ctx, double *pos, double *vel);
+
+/* ------------------------------------------------- partitioned runs */
+/* Mark mass slots as ghosts (copies of masses owned by another rank):
+ * they must also be fixed (never integrated); spring events whose m1
+ * endpoint is a ghost are not counted here (the owner counts them).
+ * Cleared when the mass count changes. */
+int sl_mark_ghosts(sl_ctx *ctx, int64_t n, const int64_t *slots);
+/* Device pointer of the position buffer the next step reads: rows records
+ * of record_bytes (x, y, z, m as float or double).  Valid until the next
+ * step call. */
+int sl_state_pointers(sl_ctx *ctx, void **pos_read, int64_t *rows,
+                      int32_t *record_bytes);
+/* The context's CUDA stream (cudaStream_t) for ordering foreign work. */
+int sl_get_stream(sl_ctx *ctx, void **stream);
 
 /* ---------------------------------------------------------- timing / sync */
 /* CUDA events on the context's stream (bench.py measures with these). */

@@ -31,7 +31,9 @@ EXPORTS = (
     "sl_write_masses", "sl_write_spring_params", "sl_kill_springs", "sl_step",
     "sl_spring_pass", "sl_mass_pass", "sl_download_masses",
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
-    "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync")
+    "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
+    "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
+    "sl_get_stream")
 
 
 class SlStats(C.Structure):
@@ -88,6 +90,11 @@ def load_library(path: str = LIB_PATH):
             "sl_timer_start": ([P], I),
             "sl_timer_stop": ([P, P], I),
             "sl_sync": ([P], I),
+            "sl_step_async": ([P, I64, P, D, I], I),
+            "sl_step_finish": ([P, P, P, P], I),
+            "sl_mark_ghosts": ([P, I64, P], I),
+            "sl_state_pointers": ([P, P, P, P], I),
+            "sl_get_stream": ([P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -251,6 +258,46 @@ class Context:
             return int(done.value), int(err.value)
         self._check(rc, "sl_step")
         return int(done.value), 0
+
+    def step_async(self, sim_times, dt: float, accumulation: int):
+        """Enqueue steps without synchronising (sl_step_async)."""
+        t = _c(sim_times, np.float64)
+        self._check(self.lib.sl_step_async(self.h, len(t), _ptr(t),
+                                           float(dt), int(accumulation)),
+                    "sl_step_async")
+
+    def step_finish(self, counters: np.ndarray) -> tuple[int, int]:
+        """Synchronise an asynchronous run: (steps_done, err_slot)."""
+        err = C.c_int64(0)
+        done = C.c_int64(0)
+        rc = self.lib.sl_step_finish(self.h, _ptr(counters), C.byref(err),
+                                     C.byref(done))
+        if rc == SL_ENUMERIC:
+            return int(done.value), int(err.value)
+        self._check(rc, "sl_step_finish")
+        return int(done.value), 0
+
+    def mark_ghosts(self, slots):
+        s = _c(slots, np.int64)
+        self._check(self.lib.sl_mark_ghosts(self.h, len(s), _ptr(s)),
+                    "sl_mark_ghosts")
+
+    def state_pointers(self) -> tuple[int, int, int]:
+        """(device pointer of the position buffer the next step reads,
+        rows, bytes per record)."""
+        p = C.c_void_p()
+        rows = C.c_int64(0)
+        rb = C.c_int32(0)
+        self._check(self.lib.sl_state_pointers(self.h, C.byref(p),
+                                               C.byref(rows), C.byref(rb)),
+                    "sl_state_pointers")
+        return int(p.value or 0), int(rows.value), int(rb.value)
+
+    def stream(self) -> int:
+        p = C.c_void_p()
+        self._check(self.lib.sl_get_stream(self.h, C.byref(p)),
+                    "sl_get_stream")
+        return int(p.value or 0)
 
     def spring_pass(self, sim_t: float, accumulation: int,
                     counters: np.ndarray):

@@ -102,6 +102,12 @@ struct sl_ctx {
   DevBuf sp_j, sp_kl, sp_s, sp_w, sp_ekl, degB, sp_meta;
   SplitCfg scfg;
   int split_warps = 0, split_grid = 0;
+  // partitioned runs
+  DevBuf ghost;
+  bool has_ghost = false;
+  bool async_open = false;
+  int64_t async_steps = 0;
+  int async_cur0 = 0;
   // device copy of the kernel state block (KState::self)
   DevBuf kdev;
   KState khost;
@@ -386,10 +392,10 @@ __global__ void k_validate(KState S, const uint8_t *m_alive,
   if (m_alive[ab.x] && m_alive[ab.y] && m_gen[ab.x] == m1gen[s] &&
       m_gen[ab.y] == m2gen[s])
     return;
+  count_spring(S, 1, s);
   S.ends[s] = make_int2(-1, -1);
   S.s_alive[s] = 0;
   if (layout_valid) kill_entries(S, s);
-  atomicAdd(S.status + 1, 1ull);
 }
 
 // ------------------------------------------------------- layout build kernels
@@ -596,6 +602,7 @@ KState make_state(sl_ctx *c) {
   S.status = c->status.as<unsigned long long>();
   S.xflags = c->xflags.as<uint8_t>();
   S.fsz8 = c->fsz == 8;
+  S.ghost = c->has_ghost ? c->ghost.as<uint8_t>() : nullptr;
   S.self = c->kdev.as<KState>();
   S.split = c->layout_valid && c->split;
   if (c->split) {
@@ -999,12 +1006,12 @@ int build_layout(sl_ctx *c) {
   return build_exact_layout(c);
 }
 
-int prepare(sl_ctx *c, bool need_layout) {
+int prepare(sl_ctx *c, bool need_layout, bool reset_status = true) {
   if (!c->masses_set || !c->springs_set)
     return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
   if (!c->env_set)
     return fail(c, SL_ESTATE, "environment not set (sl_set_environment)");
-  CK(cudaMemsetAsync(c->status.p, 0, 8 * 8, c->st));
+  if (reset_status) CK(cudaMemsetAsync(c->status.p, 0, 8 * 8, c->st));
   if (c->validate_dirty && c->s_n > 0) {
     KState S = make_state(c);
     k_validate<<<blocks_for(c->s_n), 256, 0, c->st>>>(
@@ -1126,7 +1133,8 @@ int sl_destroy(sl_ctx *c) {
                     &c->sort_tmp, &c->keys[0], &c->keys[1], &c->vals[0],
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
-                    &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev};
+                    &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
+                    &c->ghost};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -1188,7 +1196,12 @@ int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
                               !gen)))
     return fail(c, SL_EINVAL, "sl_upload_masses: bad arguments");
   CK(cudaSetDevice(c->device));
-  if (m_n != c->m_n) c->layout_valid = false;  // slices follow mass count
+  if (m_n != c->m_n) {
+    c->layout_valid = false;  // slices follow mass count
+    c->has_ghost = false;
+  }
+  if (c->async_open)
+    return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
   int rc = ensure_masses(c, m_n);
   if (rc) return rc;
   std::vector<double> zeros;
@@ -1520,6 +1533,8 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
   if (err_slot) *err_slot = 0;
   if (steps_done) *steps_done = 0;
+  if (c->async_open)
+    return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
   CK(cudaSetDevice(c->device));
   int rc = prepare(c, accumulation == SL_ACC_GATHER);
   if (rc) return rc;
@@ -1720,6 +1735,136 @@ int sl_snapshot_wait(sl_ctx *c, double *pos, double *vel) {
   if (pos) memcpy(pos, c->snap_host, 24 * m);
   if (vel) memcpy(vel, c->snap_host + 3 * m, 24 * m);
   c->snap_pending = false;
+  return SL_OK;
+}
+
+// Enqueue the launches of n steps starting at run-relative step index base
+// (the loop of sl_step without the final synchronisation).
+static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
+                         const double *sim_times, double dt,
+                         int accumulation, int64_t base, int cur0) {
+  const Launch &L = launchers(c->prec);
+  for (int64_t n = 0; n < n_steps; n++) {
+    StepP T;
+    T.sim_t = sim_times[n];
+    T.dt = dt;
+    T.step = base + n;
+    T.cur = (int)((cur0 + n) & 1);
+    T.write_acc = 1;
+    if (accumulation == SL_ACC_GATHER) {
+      if (c->split) {
+        if (c->split_warps)
+          L.split_tma(S, c->env, T, c->scfg, c->split_grid, c->st);
+        else
+          L.split(S, c->env, T, c->st);
+      } else if (c->tma_warps) {
+        L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
+      } else {
+        L.gather(S, c->env, T, c->st);
+      }
+      c->launches++;
+    } else {
+      L.spring_atomic(S, T, c->has_special, c->st);
+      L.mass(S, c->env, T, c->st);
+      c->launches += 2;
+    }
+  }
+  CKL();
+  return SL_OK;
+}
+
+int sl_step_async(sl_ctx *c, int64_t n_steps, const double *sim_times,
+                  double dt, int accumulation) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (n_steps < 0 || (n_steps > 0 && !sim_times))
+    return fail(c, SL_EINVAL, "sl_step_async: bad arguments");
+  if (!(dt > 0) || !std::isfinite(dt))
+    return fail(c, SL_EINVAL, "dt must be positive, got %g", dt);
+  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC)
+    return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
+  CK(cudaSetDevice(c->device));
+  int rc = prepare(c, accumulation == SL_ACC_GATHER, !c->async_open);
+  if (rc) return rc;
+  if (!c->async_open) {
+    c->async_open = true;
+    c->async_steps = 0;
+    c->async_cur0 = c->cur;
+  }
+  KState S = make_state(c);
+  if ((rc = upload_state(c, S))) return rc;
+  rc = enqueue_steps(c, S, n_steps, sim_times, dt, accumulation,
+                     c->async_steps, c->cur);
+  if (rc) return rc;
+  c->async_steps += n_steps;
+  c->cur = (int)((c->cur + n_steps) & 1);
+  return SL_OK;
+}
+
+int sl_step_finish(sl_ctx *c, int64_t *counters, int64_t *err_slot,
+                   int64_t *steps_done) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (err_slot) *err_slot = 0;
+  if (steps_done) *steps_done = 0;
+  if (!c->async_open) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  c->async_open = false;
+  int64_t err = 0;
+  int rc = finish_status(c, counters, &err);
+  if (rc) return rc;
+  int64_t done = c->async_steps;
+  if (c->h_status[4]) done = (int64_t)c->h_status[4];
+  c->cur = (int)((c->async_cur0 + done) & 1);
+  if (steps_done) *steps_done = done;
+  if (err_slot) *err_slot = err;
+  if (err) return fail(c, SL_ENUMERIC, "non-finite state on mass slot %lld",
+                       (long long)(err - 1));
+  return SL_OK;
+}
+
+__global__ void k_set_ghosts(int64_t n, const int64_t *slots, uint8_t *g) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) g[slots[r]] = 1;
+}
+
+int sl_mark_ghosts(sl_ctx *c, int64_t n, const int64_t *slots) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (n < 0 || (n > 0 && !slots))
+    return fail(c, SL_EINVAL, "sl_mark_ghosts: bad arguments");
+  for (int64_t r = 0; r < n; r++)
+    if (slots[r] < 0 || slots[r] >= c->m_n)
+      return fail(c, SL_EINVAL, "mass slot %lld out of range",
+                  (long long)slots[r]);
+  CK(cudaSetDevice(c->device));
+  CK(c->ghost.ensure(c->m_n + 1));
+  CK(cudaMemsetAsync(c->ghost.p, 0, c->m_n + 1, c->st));
+  if (n > 0) {
+    CK(c->stage.ensure(8 * n + 256));
+    size_t off = 0;
+    const int64_t *ds;
+    int rc = stage_copy(c, off, slots, n, &ds);
+    if (rc) return rc;
+    k_set_ghosts<<<blocks_for(n), 256, 0, c->st>>>(n, ds,
+                                                   c->ghost.as<uint8_t>());
+    CKL();
+    c->launches++;
+  }
+  CK(cudaStreamSynchronize(c->st));
+  c->has_ghost = n > 0;
+  return SL_OK;
+}
+
+int sl_state_pointers(sl_ctx *c, void **pos_read, int64_t *rows,
+                      int32_t *record_bytes) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (pos_read) *pos_read = c->pos[c->cur].p;
+  if (rows) *rows = (int64_t)(c->pos[c->cur].bytes / (4 * c->rsz));
+  if (record_bytes) *record_bytes = (int32_t)(4 * c->rsz);
+  return SL_OK;
+}
+
+int sl_get_stream(sl_ctx *c, void **stream) {
+  if (!c || !stream) return fail(c, SL_EINVAL, "NULL argument");
+  *stream = (void *)c->st;
   return SL_OK;
 }
 

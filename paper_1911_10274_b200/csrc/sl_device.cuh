@@ -95,6 +95,9 @@ struct KState {
   const int32_t *ent_s;
   const int64_t *e1, *e2;
   uint8_t *xflags;  // per-mass layout-derived flag bits (MF_SPECIAL)
+  // ghost masses of a partitioned run (partition.py): spring side effects
+  // are counted only where the m1 endpoint is owned; null when no ghosts
+  const uint8_t *ghost;
   // split layout (tolerance modes, sl_split.cuh); split == 0 => exact layout
   const KState *self;  // device-memory copy of this struct (rare paths)
   int split;
@@ -214,6 +217,12 @@ __device__ __forceinline__ bool stopped(const KState &S, int64_t step) {
 
 __device__ __forceinline__ void count(const KState &S, int which) {
   atomicAdd(S.status + which, 1ull);
+}
+// count a spring event unless the spring's m1 endpoint is a ghost (the
+// owning rank counts it); m1 = ends[s].x, read before a kill clears it
+__device__ __forceinline__ void count_spring(const KState &S, int which,
+                                             int64_t s) {
+  if (!S.ghost || !S.ghost[S.ends[s].x]) atomicAdd(S.status + which, 1ull);
 }
 
 __device__ __forceinline__ void mark_nonfinite(const KState &S, int64_t i,
@@ -442,7 +451,7 @@ __device__ __forceinline__ bool entry_force(
       const int32_t s = S.ent_s[e];
       if (!S.s_degen[s]) {
         S.s_degen[s] = 1;
-        count(S, 2);
+        count_spring(S, 2, s);
       }
     }
     return false;
@@ -481,9 +490,9 @@ __device__ __forceinline__ bool entry_force(
     if (mag > thr) {
       S.ent_j[e] = jr | EJ_DEAD;
       if (!is_m2) {
+        count_spring(S, 0, s);
         S.s_alive[s] = 0;
         S.ends[s] = make_int2(-1, -1);
-        count(S, 0);
       }
     }
   }
@@ -672,8 +681,8 @@ __device__ __forceinline__ bool gather_forces_pipe(
 template <int P, bool GLOBAL_SRC>
 __device__ __noinline__ void degenerate_flags(
     const int32_t *ent_s, uint8_t *s_degen, unsigned long long *status,
-    const typename Tr<P>::R4 *pos, const uint32_t *ej, int width,
-    int64_t ebase, typename Tr<P>::R4 me) {
+    const uint8_t *ghost, int64_t self, const typename Tr<P>::R4 *pos,
+    const uint32_t *ej, int width, int64_t ebase, typename Tr<P>::R4 me) {
   for (int t = 0; t < width; t++) {
     const uint32_t jr = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
     if (jr & (EJ_DEAD | EJ_M2)) continue;
@@ -682,7 +691,7 @@ __device__ __noinline__ void degenerate_flags(
       const int32_t s = ent_s[ebase + 32 * (int64_t)t];
       if (!s_degen[s]) {
         s_degen[s] = 1;
-        atomicAdd(status + 2, 1ull);
+        if (!ghost || !ghost[self]) atomicAdd(status + 2, 1ull);  // self = m1
       }
     }
   }
@@ -704,8 +713,8 @@ __device__ __forceinline__ void gather_forces(
     else if (gather_forces_fast<P, GLOBAL_SRC>(pos, ej, ekl, width,
                                                  (uint32_t)self, me, fx, fy,
                                                  fz))
-      degenerate_flags<P, GLOBAL_SRC>(S.ent_s, S.s_degen, S.status, pos, ej,
-                                      width, ebase, me);
+      degenerate_flags<P, GLOBAL_SRC>(S.ent_s, S.s_degen, S.status, S.ghost,
+                                      self, pos, ej, width, ebase, me);
   }
 }
 
@@ -969,8 +978,8 @@ __global__ void __launch_bounds__(384)
           else if (gather_forces_pipe<P, Tr<P>::UP>(pos, ej, ekl, width,
                                                      (uint32_t)i, me, fx, fy,
                                                      fz))
-            degenerate_flags<P, false>(S.ent_s, S.s_degen, S.status, pos, ej,
-                                       width, e0 + lane, me);
+            degenerate_flags<P, false>(S.ent_s, S.s_degen, S.status, S.ghost,
+                                       i, pos, ej, width, e0 + lane, me);
         }
         finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
       }
@@ -1021,7 +1030,7 @@ __global__ void __launch_bounds__(256)
   if (len == (F)0.0) {
     if (!S.s_degen[s]) {
       S.s_degen[s] = 1;
-      count(S, 2);
+      count_spring(S, 2, s);
     }
     return;
   }
@@ -1041,11 +1050,11 @@ __global__ void __launch_bounds__(256)
     const F thr = (F)((const FS *)S.thr)[s];
     const F mag = fmag >= (F)0.0 ? fmag : -fmag;
     if (mag > thr) {
+      count_spring(S, 0, s);
       S.s_alive[s] = 0;
       S.ends[s] = make_int2(-1, -1);
       if (S.e1) kill_entries(S, s);  // incidence layout present: keep it
                                      // consistent
-      count(S, 0);
     }
   }
 }

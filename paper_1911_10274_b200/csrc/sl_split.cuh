@@ -188,7 +188,7 @@ __device__ __forceinline__ void split_entry_exact(
   if (len2 == (F)0.0) {
     if (!side_b && !S->s_degen[s]) {
       S->s_degen[s] = 1;
-      atomicAdd(S->status + 2, 1ull);
+      count_spring(*S, 2, s);
     }
     return;
   }
@@ -206,9 +206,9 @@ __device__ __forceinline__ void split_entry_exact(
   if (mag > thr) {
     S->sp_j[e] = side_b ? S->sp_null : S->sp_sent;
     if (!side_b) {
+      count_spring(*S, 0, s);
       S->s_alive[s] = 0;
       S->ends[s] = make_int2(-1, -1);
-      atomicAdd(S->status + 0, 1ull);
     }
   }
 }

@@ -1,0 +1,137 @@
+"""Running one partitioned store across devices (config E) and independent
+instances across ranks (configs B / D).
+
+``PartitionedRun`` drives one shard (partition.py) on one device: its
+context holds the owned masses plus ghosts; before every step the halo
+exchange rewrites the ghost rows of the position buffer the step will read,
+on the context's own CUDA stream, then the step is enqueued asynchronously
+(sl_step_async).  The host never synchronises inside the run; the only
+cross-rank traffic is the point-to-point halo (NCCL over NVLink on GPUs,
+gloo in the CPU tests) -- no collective on the step path.
+
+The position buffer is exposed to torch through
+``__cuda_array_interface__`` (sl_state_pointers); torch is plumbing here:
+the index gather / scatter of the halo rows and the NCCL calls.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .partition import HaloPlan, Shard, exchange
+
+
+def context_for_case(case: dict, device: int = 0, precision: str = "fp64",
+                     v_stick: float = 1e-6) -> _native.Context:
+    """A context loaded with a case dict (store arrays in the reference
+    layout, e.g. a Shard.case or a golden case)."""
+    ctx = _native.Context(device, precision)
+    ctx.upload_masses(case["m_pos"], case["m_vel"], case["m_acc"],
+                      case["m_fext"], case["m_load"], case["m_mass"],
+                      case["m_fixed"], case["m_alive"], case["m_gen"])
+    ctx.upload_springs(case["s_m1"], case["s_m2"], case["s_m1gen"],
+                       case["s_m2gen"], case["s_rest"], case["s_k"],
+                       case["s_diam"], case["s_yield"], case["s_mode"],
+                       case["s_amp"], case["s_freq"], case["s_off"],
+                       case["s_per"], case["s_alive"], case["s_degen"])
+    n = len(case["m_mass"])
+    ctx.set_local_constraints(case.get("lc_off", np.zeros(n + 1, np.int64)),
+                              case.get("lc_kind", np.zeros(0, np.int8)),
+                              case.get("lc_vec", np.zeros((0, 3))))
+    ctx.set_environment(case["gravity"], float(np.asarray(case["drag"])),
+                        case.get("planes", np.zeros((0, 7))),
+                        case.get("balls", np.zeros((0, 5))),
+                        case.get("gc_kind", np.zeros(0, np.int8)),
+                        case.get("gc_vec", np.zeros((0, 3))), v_stick)
+    return ctx
+
+
+class _DeviceArray:
+    def __init__(self, ptr: int, rows: int, record_bytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (rows, 4),
+            "typestr": "<f4" if record_bytes == 16 else "<f8",
+            "data": (ptr, False), "version": 2, "strides": None}
+
+
+def position_view(ctx: _native.Context):
+    """torch view (rows, 4) = (x, y, z, m) of the buffer the next step
+    reads.  Re-fetch after every step (the buffers ping-pong)."""
+    import torch
+    ptr, rows, rb = ctx.state_pointers()
+    return torch.as_tensor(_DeviceArray(ptr, rows, rb),
+                           device=f"cuda:{ctx.device}")
+
+
+class PartitionedRun:
+    """One shard of a mass-range partition on one device."""
+
+    def __init__(self, shard: Shard, plan: HaloPlan, device: int = 0,
+                 precision: str = "fp64", accumulation: int =
+                 _native.ACC_GATHER):
+        self.shard = shard
+        self.plan = plan
+        self.acc = accumulation
+        self.ctx = context_for_case(shard.case, device, precision)
+        if len(shard.ghost_local):
+            self.ctx.mark_ghosts(shard.ghost_local)
+        self.counters = np.zeros(3, np.int64)
+
+    def stream(self):
+        import torch
+        return torch.cuda.ExternalStream(self.ctx.stream(),
+                                         device=f"cuda:{self.ctx.device}")
+
+    def step_async(self, sim_t: float, dt: float, halo) -> None:
+        """Halo exchange then one step, both enqueued on the context
+        stream.  ``halo(plan, pos_view)`` performs the exchange."""
+        import torch
+        with torch.cuda.stream(self.stream()):
+            halo(self.plan, position_view(self.ctx))
+        self.ctx.step_async(np.array([sim_t]), dt, self.acc)
+
+    def finish(self) -> tuple[int, int]:
+        return self.ctx.step_finish(self.counters)
+
+    def owned_state(self):
+        m = self.shard.n_owned
+        n = len(self.shard.local_to_global)
+        pos, vel = np.zeros((n, 3)), np.zeros((n, 3))
+        self.ctx.download_masses(pos, vel)
+        alive = np.zeros(len(self.shard.spring_slots), np.uint8)
+        self.ctx.download_springs(alive)
+        return pos[:m], vel[:m], alive
+
+    def close(self):
+        self.ctx.close()
+
+
+def nccl_halo(plan: HaloPlan, pos, group=None):
+    """Halo exchange over torch.distributed (NCCL between GPUs)."""
+    return exchange(plan, pos, group=group)
+
+
+def run_partitioned(case: dict, cuts: list[int], steps: int, dt: float,
+                    precision: str = "fp64", device: int | None = None):
+    """Multi-process driver (one rank per GPU, torchrun): this rank's shard
+    of ``case`` stepped ``steps`` times with NCCL halo exchange.  Returns
+    (shard, owned positions, owned velocities, spring alive flags,
+    counters, device seconds)."""
+    import torch
+    import torch.distributed as dist
+    from .partition import halo_plans, partition_case
+    rank = dist.get_rank()
+    shards = partition_case(case, cuts)
+    plan = halo_plans(shards)[rank]
+    dev = torch.cuda.current_device() if device is None else device
+    run = PartitionedRun(shards[rank], plan, dev, precision)
+    times = np.arange(steps, dtype=np.float64) * dt
+    dist.barrier()
+    torch.cuda.synchronize()
+    run.ctx.timer_start()
+    for t in times:
+        run.step_async(float(t), dt, nccl_halo)
+    done, err = run.finish()
+    ms = run.ctx.timer_stop()
+    pos, vel, alive = run.owned_state()
+    return shards[rank], pos, vel, alive, run.counters.copy(), ms / 1e3
