@@ -44,7 +44,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="B", choices=["B", "D"],
+                    help="B: one 100^3 lattice per rank (batched instances);"
+                         " D: --robots actuated 5^3 robots sharded over "
+                         "the ranks (RL batch)")
     ap.add_argument("--n", type=int, default=100, help="lattice edge")
+    ap.add_argument("--robots", type=int, default=4096)
     ap.add_argument("--precision", default="fp32",
                     choices=["fp32", "mixed", "fp64"])
     ap.add_argument("--accumulation", default="gather",
@@ -69,12 +74,50 @@ def build_workload(n: int):
     return st, env
 
 
-def algorithmic_bytes(springs: int, masses: int, precision: str) -> int:
-    """SURVEY.md 8(d): B = S*Bs + M*Bm.  Bs = int32 i,j + k, L0 words;
-    Bm = pos r+w, vel r+w, m r (words of the state precision)."""
+def build_robots(count: int, first: int = 0):
+    """Config D: 5^3 robots, spacing 0.05, E = 1e6,
+    worm-actuated (configure_worm), stacked along y as cmd_swarm does
+    (cli.py:323-331), on a ground plane k = 500 with drag 0.01.  ``first``
+    offsets this rank's shard so shards tile the global swarm."""
+    from paper_1911_10274_b200 import (ContactPlane, Environment, Material,
+                                       ObjectStore, Vec3)
+    from paper_1911_10274_b200.builder import LatticeSpec, build_robot_swarm
+    step = 4 * 0.05 + 2 * 0.05
+    st = ObjectStore()
+    build_robot_swarm(LatticeSpec(Vec3(0, first * step, 0), 5, 5, 5, 0.05,
+                                  Material(1e6, 1000.0)), st, count)
+    env = Environment(gravity=Vec3(0, 0, -9.81), drag_coeff=0.01,
+                      contacts=[ContactPlane(
+                          normal=Vec3(0, 0, 1), offset=0.0, stiffness=500.0,
+                          static_friction=1.0, kinetic_friction=0.8)])
+    return st, env
+
+
+def make_workload(args, rank: int, world: int):
+    """(store, env, description, scaling, per-spring extra words)."""
+    if args.config == "D":
+        per = args.robots // world
+        first = rank * per + min(rank, args.robots % world)
+        count = per + (1 if rank < args.robots % world else 0)
+        st, env = build_robots(count, first)
+        desc = (f"D: {args.robots} worm-actuated 5^3 robots (RL batch) on a "
+                f"friction ground plane, sharded over {world} rank(s), "
+                f"{args.precision}, {args.accumulation}")
+        return st, env, desc, ("strong" if world > 1 else "weak"), 1
+    st, env = build_workload(args.n)
+    desc = (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
+            f"x1.01 stretch, {args.precision}, {args.accumulation}")
+    return st, env, desc, "weak", 0
+
+
+def algorithmic_bytes(springs: int, masses: int, precision: str,
+                      extra_words: int = 0) -> int:
+    """B = S*Bs + M*Bm.  Bs = int32 i,j + k, L0 words (+ an
+    actuation phase word for actuated springs); Bm = pos r+w, vel r+w, m r
+    (words of the state precision)."""
     w_s = 8 if precision == "fp64" else 4
     w_m = 4 if precision == "fp32" else 8
-    return springs * (8 + 2 * w_s) + masses * 13 * w_m
+    return springs * (8 + (2 + extra_words) * w_s) + masses * 13 * w_m
 
 
 def store_case(st, env):
@@ -203,15 +246,13 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
 
-    workload = (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
-                f"x1.01 stretch, {args.precision}, {args.accumulation}")
     metric = "spring updates/sec"
     unit = "spring_updates/s"
 
     if args.impl == "reference":
         if rank != 0:
             return
-        st, env = build_workload(args.n)
+        st, env, workload, _, _ = make_workload(args, 0, 1)
         threads = os.cpu_count() or 1
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle
@@ -233,9 +274,10 @@ def main():
                 "cpu_baseline": {"value": v, "unit": unit, "cores": threads,
                                  "kind": "port",
                                  "sample": f"{steps} full steps of the "
-                                           f"{args.n}^3 lattice, oracle/ C "
-                                           f"restatement of kernels.py, "
-                                           f"slotted, {threads} threads"},
+                                           f"config-{args.config} workload, "
+                                           f"oracle/ C restatement of "
+                                           f"kernels.py, slotted, {threads} "
+                                           f"threads"},
                 "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -244,7 +286,7 @@ def main():
     from paper_1911_10274_b200 import StepConfig, engine
     from paper_1911_10274_b200.control import SimController
 
-    st, env = build_workload(args.n)
+    st, env, workload, scaling, extra = make_workload(args, rank, world)
     cfg = StepConfig(dt=1e-4, precision=args.precision, device=local,
                      accumulation=args.accumulation)
     springs, masses = st.spring_count, st.mass_count
@@ -287,15 +329,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         sec = float(t.item())
         dist.barrier()
-    value = world * springs * args.steps / sec
+    total_springs = springs * world
+    if dist is not None and args.config != "B":
+        import torch
+        t = torch.tensor([springs], device=f"cuda:{local}", dtype=torch.int64)
+        dist.all_reduce(t)
+        total_springs = int(t.item())
+    value = total_springs * args.steps / sec
     ms_per_step = 1e3 * sec / args.steps
 
     # roofline of the dominant kernel (the fused gather step: one launch per
     # step, so its average duration is the per-step device time)
-    algo = algorithmic_bytes(springs, masses, args.precision)
+    algo = algorithmic_bytes(springs, masses, args.precision, extra)
     peak, peak_kind = peak_hbm()
     achieved = algo / (sec / args.steps) / 1e9
-    key = f"{args.n}^3/{args.precision}/{args.accumulation}"
+    key = (f"{args.n}^3/{args.precision}/{args.accumulation}"
+           if args.config == "B" else
+           f"D{args.robots}/{args.precision}/{args.accumulation}")
     traffic = committed_traffic(key)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -339,13 +389,14 @@ def main():
             import oracle
             oracle.build()
             thr = oracle.max_threads()
-            st2, env2 = build_workload(args.n)
+            st2, env2, _, _, _ = make_workload(args, 0, 1)
             n_s, wall = time_oracle(st2, env2, 3, 1, thr, budget_s=30.0)
             cpu = {"value": st2.spring_count * n_s / wall, "unit": unit,
                    "cores": thr, "kind": "port",
-                   "sample": f"{n_s} steps of the same {args.n}^3 lattice "
-                             f"(fp64, slotted, oracle/ C restatement of "
-                             f"kernels.py, OpenMP {thr} threads)"}
+                   "sample": f"{n_s} steps of the same config-"
+                             f"{args.config} workload (fp64, slotted, "
+                             f"oracle/ C restatement of kernels.py, OpenMP "
+                             f"{thr} threads)"}
         except Exception as exc:  # baseline is reported, never fatal
             cpu = {"error": str(exc)}
 
@@ -353,15 +404,20 @@ def main():
         line = {"metric": metric, "value": value, "unit": unit,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": value / PAPER_RATE,
+                "scaling": scaling, "vs_baseline": value / PAPER_RATE,
                 "dtype": "f32" if args.precision == "fp32" else "f64",
                 "data": "synthetic",
                 "config": {"workload": workload, "masses": masses,
-                           "springs": springs, "per_gpu_instances": 1,
+                           "springs": springs,
+                           "total_springs": total_springs,
+                           "per_gpu_instances": (1 if args.config == "B"
+                                                 else "robot shard"),
                            "precision": args.precision,
                            "accumulation": args.accumulation,
-                           "l2": "working set > 126 MB L2 every step "
-                                 "(no flush needed)",
+                           "l2": ("working set > 126 MB L2 every step "
+                                  "(no flush needed)" if args.config == "B"
+                                  else "working set may fit L2 (config D "
+                                       "shards); no flush"),
                            "parallelism": f"batched instances x{world}"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk,

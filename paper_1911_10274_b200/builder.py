@@ -201,6 +201,39 @@ def build_swarm(spec: LatticeSpec, store: ObjectStore, count: int,
     return bodies
 
 
+def build_robot_swarm(spec: LatticeSpec, store: ObjectStore, count: int,
+                      worm: bool = True, gap: float | None = None):
+    """``count`` lattice robots stacked along +y (cmd_swarm layout,
+    cli.py:323-331) created in ONE bulk call, each worm-actuated like
+    ``configure_worm`` (actuation.py:72-111) when ``worm``.  Same arrays as
+    ``build_swarm`` + per-body ``configure_worm``, built vectorised (config
+    D: thousands of RL robots).  Returns per-body (mass slot range, spring
+    slot range)."""
+    from .actuation import WORM_AMPLITUDE, WORM_FREQUENCY, WORM_PERIOD
+    pos1, idx = _grid_positions(spec.corner, spec.nx, spec.ny, spec.nz,
+                                spec.spacing)
+    a1, b1 = grid_springs(spec.nx, spec.ny, spec.nz)
+    extent = (spec.ny - 1) * spec.spacing
+    step = extent + 2 * spec.spacing if gap is None else extent + gap
+    m1, s1 = len(pos1), len(a1)
+    shift = np.zeros((count, 1, 3))
+    shift[:, 0, 1] = np.arange(count) * step
+    positions = (pos1[None] + shift).reshape(-1, 3)
+    base = (np.arange(count) * m1)[:, None]
+    a = (a1[None] + base).reshape(-1)
+    b = (b1[None] + base).reshape(-1)
+    body = materialize(store, positions, a, b, spec.material, spec.diameter)
+    if worm:
+        x0 = pos1[:, 0]
+        off1 = np.minimum(x0[a1], x0[b1]) - x0.min()
+        store.set_actuation_bulk(body.spring_handles.slots, WORM_AMPLITUDE,
+                                 WORM_FREQUENCY, np.tile(off1, count),
+                                 WORM_PERIOD)
+    ms, ss = body.mass_handles.slots, body.spring_handles.slots
+    return [((int(ms[i * m1]), int(ms[i * m1]) + m1),
+             (int(ss[i * s1]), int(ss[i * s1]) + s1)) for i in range(count)]
+
+
 def build_cube_grid(grid_x: int, grid_y: int, cube_counts, spacing: float,
                     material: Material, store: ObjectStore,
                     corner: Vec3 = Vec3(0, 0, 0), diameter: float = 1e-3,
