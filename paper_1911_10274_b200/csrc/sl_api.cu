@@ -102,6 +102,9 @@ struct sl_ctx {
   DevBuf sp_j, sp_kl, sp_s, sp_w, sp_ekl, degB, sp_meta;
   SplitCfg scfg;
   int split_warps = 0, split_grid = 0;
+  // grouped sine actuation of the split layout's fast path (ActP)
+  ActP agrp;
+  DevBuf s_grp, s_aoff, sp_act;
   // partitioned runs
   DevBuf ghost;
   bool has_ghost = false;
@@ -313,12 +316,16 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
                                int64_t *m1g_o, int64_t *m2g_o, int8_t *mode_o,
                                double4 *act_o, uint8_t *degen_o,
                                double *custom_o, int params_only,
-                               int layout_valid) {
+                               int layout_valid, const uint8_t *grp_in,
+                               const float *aoff_in, uint8_t *grp_o,
+                               float *aoff_o) {
   using F = typename Tr<P>::F;
   using F2 = typename Tr<P>::F2;
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int64_t s = slots ? slots[r] : r;
+  grp_o[s] = grp_in[r];
+  aoff_o[s] = aoff_in[r];
   F2 kl;
   kl.x = (F)k[r];
   kl.y = (F)rest[r];
@@ -336,8 +343,10 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
     m2g_o[s] = m2gen[r];
     custom_o[s] = 1.0;
   } else if (layout_valid) {
-    // keep the incidence copies of (k, L0) and the special bit in sync
-    bool special = mode[r] != 0 || yield[r] != CUDART_INF;
+    // keep the incidence copies of (k, L0) and the special bit in sync;
+    // the split layout runs grouped sine actuation in its fast path
+    bool special = (mode[r] != 0 && !(S.split && grp_in[r] != 0)) ||
+                   yield[r] != CUDART_INF;
     int2 ab = S.ends[s];
     if (special && ab.x >= 0) {
       using R4 = typename Tr<P>::R4;
@@ -347,7 +356,12 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
       or_flags((R4 *)S.vel + ab.y, MF_SPECIAL);
     }
     if (S.split) {
-      if (ab.x >= 0 && S.e1[s] >= 0) ((F2 *)S.sp_kl)[S.sp_ekl[s]] = kl;
+      if (ab.x >= 0 && S.e1[s] >= 0) {
+        ((F2 *)S.sp_kl)[S.sp_ekl[s]] = kl;
+        if (S.sp_act)
+          ((float2 *)S.sp_act)[S.sp_ekl[s]] =
+              make_float2(aoff_in[r], __uint_as_float(grp_in[r]));
+      }
       return;
     }
     int64_t es[2] = {S.e1[s], S.e2[s]};
@@ -538,7 +552,9 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
                              const uint32_t *vals, uint32_t kbound,
                              const int64_t *start, KState S, uint32_t *sp_j,
                              void *sp_kl, int32_t *sp_s, uint32_t *sp_ekl,
-                             int64_t *e1, int64_t *e2, int pass) {
+                             int64_t *e1, int64_t *e2, int pass,
+                             float2 *sp_act, const uint8_t *grp,
+                             const float *aoff) {
   using F = typename Tr<P>::F;
   using F2 = typename Tr<P>::F2;
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -555,6 +571,8 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
     uint32_t kli = (uint32_t)((sl << (S.sp_a + 5)) | (r << 5) | lane);
     sp_j[e] = (uint32_t)ab.y;
     ((F2 *)sp_kl)[kli] = ((const F2 *)S.kL0)[s];
+    if (sp_act)
+      sp_act[kli] = make_float2(aoff[s], __uint_as_float((uint32_t)grp[s]));
     sp_s[e] = (int32_t)s;
     sp_ekl[s] = kli;
     e1[s] = e;
@@ -564,7 +582,8 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
     sp_s[e] = (int32_t)s;
     e2[s] = e;
   }
-  bool special = S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+  bool special = (S.mode[s] != 0 && grp[s] == 0) ||
+                 ((const F *)S.thr)[s] != (F)CUDART_INF;
   if (special) {
     S.xflags[owner] = 1;
     or_flags((typename Tr<P>::R4 *)S.vel + owner, MF_SPECIAL);
@@ -616,6 +635,7 @@ KState make_state(sl_ctx *c) {
     S.sp_s = c->sp_s.as<int32_t>();
     S.sp_w = c->sp_w.as<uint32_t>();
     S.sp_ekl = c->sp_ekl.as<uint32_t>();
+    S.sp_act = c->agrp.n > 1 ? c->sp_act.as<float2>() : nullptr;
   }
   return S;
 }
@@ -664,6 +684,8 @@ int ensure_springs(sl_ctx *c, int64_t s_n) {
   CK(c->custom.ensure(8 * s_n));
   CK(c->m1gen.ensure(8 * s_n));
   CK(c->m2gen.ensure(8 * s_n));
+  CK(c->s_grp.ensure(s_n));
+  CK(c->s_aoff.ensure(4 * s_n));
   return SL_OK;
 }
 
@@ -810,9 +832,13 @@ int build_exact_layout(sl_ctx *c) {
 void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->split_warps = 0;
   if (!c->tma_enabled || c->n_slices == 0) return;
-  const int cands_fp32[] = {4, 8, 13}, cands_mixed[] = {4, 8};
-  const int *cands = c->prec == PREC_FP32 ? cands_fp32 : cands_mixed;
-  const int n_cands = c->prec == PREC_FP32 ? 3 : 2;
+  const bool act = c->agrp.n > 1;
+  // fp64 state doubles the gather registers: batches of 4 (r1e sweep)
+  const int cands_fp32[] = {4, 8, 13}, cands_act[] = {4, 8}, cands_mixed[] = {4};
+  const int *cands = c->prec != PREC_FP32 ? cands_mixed
+                     : act                ? cands_act
+                                          : cands_fp32;
+  const int n_cands = c->prec != PREC_FP32 ? 1 : act ? 2 : 3;
   int best_u = 4;
   double best = 1e300;
   for (int q = 0; q < n_cands; q++) {
@@ -837,7 +863,8 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   const int64_t cap_a = (c->sp_wa + u - 1) / u * u;
   const int64_t cap_b = (c->sp_wb + u - 1) / u * u;
   const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(cap_a + cap_b) * 128 +
-                       (size_t)cap_a * 32 * 2 * c->fsz;
+                       (size_t)cap_a * 32 * 2 * c->fsz +
+                       (act ? (size_t)cap_a * 32 * 8 : 0);
   const size_t per_warp = 2 * stage + 16;
   int want = SPLIT_DEFAULT_WARPS;
   if (const char *ev = getenv("SL_SPLIT_WARPS"))  // tuning override
@@ -847,13 +874,14 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   if (warps < 2) return;
   c->scfg.n_slices = c->n_slices;
   c->scfg.u = u;
+  c->scfg.act = act;
   c->scfg.cap_a = (int)cap_a;
   c->scfg.cap_b = (int)cap_b;
   c->scfg.warps = warps;
   c->scfg.stage_bytes = (uint32_t)stage;
   int64_t ctas = (c->n_slices + warps - 1) / warps;
   c->split_grid = (int)std::min<int64_t>(ctas, c->sm_count);
-  if (launchers(c->prec).split_setup((int)(warps * per_warp), u, warps) !=
+  if (launchers(c->prec).split_setup((int)(warps * per_warp), u, act) !=
       0) {
     cudaGetLastError();
     return;
@@ -930,6 +958,11 @@ int build_split_layout(sl_ctx *c, bool *used) {
   CK(cudaMemsetAsync(c->e1.p, 0xFF, 8 * s_n, c->st));
   CK(cudaMemsetAsync(c->e2.p, 0xFF, 8 * s_n, c->st));
   CK(cudaMemsetAsync(c->sp_kl.p, 0, f2 * n_kl, c->st));
+  const bool act = c->agrp.n > 1;
+  if (act) {
+    CK(c->sp_act.ensure(8 * n_kl));
+    CK(cudaMemsetAsync(c->sp_act.p, 0, 8 * n_kl, c->st));
+  }
   CK(cudaMemsetAsync(c->sp_s.p, 0xFF, 4 * n_j, c->st));
   CK(cudaMemsetAsync(c->xflags.p, 0, m_n + 1, c->st));
   if (n_j > 0) {
@@ -974,7 +1007,8 @@ int build_split_layout(sl_ctx *c, bool *used) {
           (uint32_t)(2 * m_n), c->start.as<int64_t>(), S,
           c->sp_j.as<uint32_t>(), c->sp_kl.p, c->sp_s.as<int32_t>(),
           c->sp_ekl.as<uint32_t>(), c->e1.as<int64_t>(), c->e2.as<int64_t>(),
-          pass);
+          pass, act ? c->sp_act.as<float2>() : nullptr,
+          c->s_grp.as<uint8_t>(), c->s_aoff.as<float>());
       CKL();
     }
   }
@@ -1134,7 +1168,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
-                    &c->ghost};
+                    &c->ghost, &c->s_grp, &c->s_aoff, &c->sp_act};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -1270,7 +1304,44 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
                   (long long)(slots ? slots[r] : r));
     if (mode[r] != 0 || yield[r] != INFINITY) c->has_special = true;
   }
-  size_t need = align256(8 * n) * 16 + align256(n) * 3 + 2048;
+  // group plain-sine actuation (mode 1) by (amp, freq, per) for the split
+  // fast path; group 0 = not actuated, 0 also when the table is full (the
+  // spring then takes the exact path)
+  if (!params_only) {
+    memset(&c->agrp, 0, sizeof c->agrp);
+    c->agrp.n = 1;
+    c->agrp.per[0] = 1.0f;
+    c->agrp.perd[0] = 1.0;
+  }
+  const int groups_before = c->agrp.n;
+  std::vector<uint8_t> grp(n, 0);
+  std::vector<float> aoff(n, 0.0f);
+  for (int64_t r = 0; r < n; r++) {
+    if (mode[r] != 1) continue;
+    int g = 1;
+    for (; g < c->agrp.n; g++)
+      if (c->agrp.amp[g] == (float)amp[r] && c->agrp.freq[g] == (float)freq[r]
+          && c->agrp.perd[g] == per[r])
+        break;
+    if (g == c->agrp.n) {
+      if (g >= MAX_ACT_GROUPS) continue;
+      c->agrp.amp[g] = (float)amp[r];
+      c->agrp.freq[g] = (float)freq[r];
+      c->agrp.per[g] = (float)per[r];
+      c->agrp.perd[g] = per[r];
+      c->agrp.n++;
+    }
+    grp[r] = (uint8_t)g;
+    // Python floor-mod (kernels.py:58) of the offset, done once in fp64
+    double t = fmod(off_[r], per[r]);
+    if (t != 0.0 && ((t < 0.0) != (per[r] < 0.0))) t += per[r];
+    aoff[r] = (float)t;
+  }
+  // first actuated group on a live split layout: re-layout with act cells
+  if (params_only && groups_before <= 1 && c->agrp.n > 1 && c->split)
+    c->layout_valid = false;
+  size_t need = align256(8 * n) * 16 + align256(n) * 5 + align256(4 * n) +
+                2048;
   CK(c->stage.ensure(need));
   size_t off = 0;
   const int64_t *dsl = nullptr, *d1 = nullptr, *d2 = nullptr, *dg1 = nullptr,
@@ -1297,6 +1368,10 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
   if ((rc = stage_copy(c, off, freq, n, &df))) return rc;
   if ((rc = stage_copy(c, off, off_, n, &doff))) return rc;
   if ((rc = stage_copy(c, off, per, n, &dper))) return rc;
+  const uint8_t *dgrp;
+  const float *daoff;
+  if ((rc = stage_copy(c, off, grp.data(), n, &dgrp))) return rc;
+  if ((rc = stage_copy(c, off, aoff.data(), n, &daoff))) return rc;
   if (n > 0) {
     KState S = make_state(c);
     auto kk = c->prec == PREC_FP64   ? k_pack_springs<PREC_FP64>
@@ -1307,7 +1382,8 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
         dal, dde, S, c->m1gen.as<int64_t>(), c->m2gen.as<int64_t>(),
         c->mode.as<int8_t>(), c->act.as<double4>(),
         c->s_degen.as<uint8_t>(), c->custom.as<double>(), params_only,
-        c->layout_valid);
+        c->layout_valid, dgrp, daoff, c->s_grp.as<uint8_t>(),
+        c->s_aoff.as<float>());
     CKL();
     c->launches++;
   }
@@ -1551,9 +1627,9 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
         if (c->split_warps)
-          L.split_tma(S, c->env, T, c->scfg, c->split_grid, c->st);
+          L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
-          L.split(S, c->env, T, c->st);
+          L.split(S, c->env, T, c->agrp, c->st);
       } else if (c->tma_warps) {
         L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
       } else {
@@ -1596,7 +1672,7 @@ int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
   T.write_acc = 0;
   if (accumulation == SL_ACC_GATHER) {
     if (c->split)
-      L.split_force(S, c->env, T, c->st);
+      L.split_force(S, c->env, T, c->agrp, c->st);
     else
       L.force_only(S, c->env, T, c->st);
     c->launches++;
@@ -1754,9 +1830,9 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
         if (c->split_warps)
-          L.split_tma(S, c->env, T, c->scfg, c->split_grid, c->st);
+          L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
-          L.split(S, c->env, T, c->st);
+          L.split(S, c->env, T, c->agrp, c->st);
       } else if (c->tma_warps) {
         L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
       } else {

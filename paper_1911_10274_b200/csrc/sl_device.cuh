@@ -111,6 +111,7 @@ struct KState {
   const int32_t *sp_s;
   const uint32_t *sp_w;
   const uint32_t *sp_ekl;  // per spring: kl index of its A cell
+  const float2 *sp_act;    // actuation cell per kl cell (null: none)
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -849,7 +850,8 @@ __device__ __forceinline__ void bulk_stage_elect(
     uint64_t *bar, uint32_t tx, void *d0, const void *s0, uint32_t n0,
     void *d1, const void *s1, uint32_t n1, void *d2, const void *s2,
     uint32_t n2, void *d3, const void *s3, uint32_t n3, void *d4,
-    const void *s4, uint32_t n4) {
+    const void *s4, uint32_t n4, void *d5 = nullptr,
+    const void *s5 = nullptr, uint32_t n5 = 0) {
   asm volatile(
       "{\n"
       ".reg .pred E, Q;\n"
@@ -870,11 +872,14 @@ __device__ __forceinline__ void bulk_stage_elect(
       "setp.ne.and.u32 Q, %16, 0, E;\n"
       "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%14], [%15], %16, [%0];\n"
+      "setp.ne.and.u32 Q, %19, 0, E;\n"
+      "@Q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%17], [%18], %19, [%0];\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(tx), "r"(smem_u32(d0)), "l"(s0), "r"(n0), "r"(smem_u32(d1)),
       "l"(s1), "r"(n1), "r"(smem_u32(d2)), "l"(s2), "r"(n2),
       "r"(smem_u32(d3)), "l"(s3), "r"(n3), "r"(smem_u32(d4)), "l"(s4),
-      "r"(n4)
+      "r"(n4), "r"(smem_u32(d5 ? d5 : d4)), "l"(s5 ? s5 : s4), "r"(n5)
       : "memory");
 }
 
@@ -1097,13 +1102,15 @@ struct Launch {
   void (*spring_atomic)(const KState &, const StepP &, bool special,
                         cudaStream_t);
   void (*mass)(const KState &, const EnvP &, const StepP &, cudaStream_t);
-  // split layout (tolerance modes; null for fp64)
-  void (*split)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  // split layout (tolerance modes; no-ops for fp64)
+  void (*split)(const KState &, const EnvP &, const StepP &,
+                const struct ActP &, cudaStream_t);
   void (*split_force)(const KState &, const EnvP &, const StepP &,
-                      cudaStream_t);
+                      const struct ActP &, cudaStream_t);
   void (*split_tma)(const KState &, const EnvP &, const StepP &,
-                    const struct SplitCfg &, int grid, cudaStream_t);
-  int (*split_setup)(int smem_bytes, int u, int warps);
+                    const struct SplitCfg &, const struct ActP &, int grid,
+                    cudaStream_t);
+  int (*split_setup)(int smem_bytes, int u, int act);
 };
 
 const Launch &launchers(int prec);

@@ -11,65 +11,69 @@ namespace sl {
 // split-layout launchers; the fp64 parity mode never uses the split layout
 template <int P>
 struct SplitLaunch {
+  template <bool FO, bool ACT>
+  static void step_k(const KState &S, const EnvP &E, const StepP &T,
+                     const ActP &A, cudaStream_t st) {
+    k_split_step<P, FO, ACT><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T, A);
+  }
   static void step(const KState &S, const EnvP &E, const StepP &T,
-                   cudaStream_t st, bool force_only) {
+                   const ActP &A, cudaStream_t st, bool force_only) {
     if (S.m_n <= 0) return;
+    const bool act = A.n > 1;
     if (force_only)
-      k_split_step<P, true><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
+      act ? step_k<true, true>(S, E, T, A, st)
+          : step_k<true, false>(S, E, T, A, st);
     else
-      k_split_step<P, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T);
+      act ? step_k<false, true>(S, E, T, A, st)
+          : step_k<false, false>(S, E, T, A, st);
   }
-  template <int U, int MW>
+  template <int U, bool ACT>
   static void tma_u(const KState &S, const EnvP &E, const StepP &T,
-                    const SplitCfg &C, int grid, cudaStream_t st) {
+                    const SplitCfg &C, const ActP &A, int grid,
+                    cudaStream_t st) {
     size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
-    k_split_tma<P, U, MW><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);
-  }
-  template <int MW>
-  static void tma_w(const KState &S, const EnvP &E, const StepP &T,
-                    const SplitCfg &C, int grid, cudaStream_t st) {
-    switch (C.u) {
-      case 4: tma_u<4, MW>(S, E, T, C, grid, st); break;
-      case 8: tma_u<8, MW>(S, E, T, C, grid, st); break;
-      default:
-        if constexpr (P == PREC_FP32) tma_u<13, MW>(S, E, T, C, grid, st);
-        else tma_u<8, MW>(S, E, T, C, grid, st);
-    }
+    k_split_tma<P, U, ACT><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C, A);
   }
   static void tma(const KState &S, const EnvP &E, const StepP &T,
-                  const SplitCfg &C, int grid, cudaStream_t st) {
-    if (C.warps > 12)
-      tma_w<16>(S, E, T, C, grid, st);
-    else
-      tma_w<12>(S, E, T, C, grid, st);
-  }
-  template <int U, int MW>
-  static int setup_u(int smem_bytes) {
-    return (int)cudaFuncSetAttribute(
-        k_split_tma<P, U, MW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        smem_bytes);
-  }
-  template <int MW>
-  static int setup_w(int smem_bytes, int u) {
-    switch (u) {
-      case 4: return setup_u<4, MW>(smem_bytes);
-      case 8: return setup_u<8, MW>(smem_bytes);
+                  const SplitCfg &C, const ActP &A, int grid,
+                  cudaStream_t st) {
+    if (C.act) {  // actuated: more live registers per entry, U <= 8
+      if (C.u == 4) tma_u<4, true>(S, E, T, C, A, grid, st);
+      else tma_u<8, true>(S, E, T, C, A, grid, st);
+      return;
+    }
+    switch (C.u) {
+      case 4: tma_u<4, false>(S, E, T, C, A, grid, st); break;
+      case 8: tma_u<8, false>(S, E, T, C, A, grid, st); break;
       default:
-        if constexpr (P == PREC_FP32) return setup_u<13, MW>(smem_bytes);
-        else return setup_u<8, MW>(smem_bytes);
+        if constexpr (P == PREC_FP32) tma_u<13, false>(S, E, T, C, A, grid, st);
+        else tma_u<8, false>(S, E, T, C, A, grid, st);
     }
   }
-  static int setup(int smem_bytes, int u, int warps) {
-    return warps > 12 ? setup_w<16>(smem_bytes, u)
-                      : setup_w<12>(smem_bytes, u);
+  template <int U, bool ACT>
+  static int setup_u(int smem_bytes) {
+    return (int)cudaFuncSetAttribute(
+        k_split_tma<P, U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        smem_bytes);
+  }
+  static int setup(int smem_bytes, int u, int act) {
+    if (act) return u == 4 ? setup_u<4, true>(smem_bytes)
+                           : setup_u<8, true>(smem_bytes);
+    switch (u) {
+      case 4: return setup_u<4, false>(smem_bytes);
+      case 8: return setup_u<8, false>(smem_bytes);
+      default:
+        if constexpr (P == PREC_FP32) return setup_u<13, false>(smem_bytes);
+        else return setup_u<8, false>(smem_bytes);
+    }
   }
 };
 template <>
 struct SplitLaunch<PREC_FP64> {
-  static void step(const KState &, const EnvP &, const StepP &, cudaStream_t,
-                   bool) {}
+  static void step(const KState &, const EnvP &, const StepP &, const ActP &,
+                   cudaStream_t, bool) {}
   static void tma(const KState &, const EnvP &, const StepP &,
-                  const SplitCfg &, int, cudaStream_t) {}
+                  const SplitCfg &, const ActP &, int, cudaStream_t) {}
   static int setup(int, int, int) { return 1; }
 };
 }  // namespace sl
@@ -108,19 +112,20 @@ struct SplitLaunch<PREC_FP64> {
     if (S.m_n > 0) k_mass<PREC><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
   }                                                                          \
   void FN##_split(const KState &S, const EnvP &E, const StepP &T,           \
-                  cudaStream_t st) {                                         \
-    SplitLaunch<PREC>::step(S, E, T, st, false);                             \
+                  const ActP &A, cudaStream_t st) {                          \
+    SplitLaunch<PREC>::step(S, E, T, A, st, false);                          \
   }                                                                          \
   void FN##_split_force(const KState &S, const EnvP &E, const StepP &T,     \
-                        cudaStream_t st) {                                   \
-    SplitLaunch<PREC>::step(S, E, T, st, true);                              \
+                        const ActP &A, cudaStream_t st) {                    \
+    SplitLaunch<PREC>::step(S, E, T, A, st, true);                           \
   }                                                                          \
   void FN##_split_tma(const KState &S, const EnvP &E, const StepP &T,       \
-                      const SplitCfg &C, int grid, cudaStream_t st) {        \
-    SplitLaunch<PREC>::tma(S, E, T, C, grid, st);                            \
+                      const SplitCfg &C, const ActP &A, int grid,            \
+                      cudaStream_t st) {                                     \
+    SplitLaunch<PREC>::tma(S, E, T, C, A, grid, st);                         \
   }                                                                          \
-  int FN##_split_setup(int smem_bytes, int u, int warps) {                   \
-    return SplitLaunch<PREC>::setup(smem_bytes, u, warps);                   \
+  int FN##_split_setup(int smem_bytes, int u, int act) {                     \
+    return SplitLaunch<PREC>::setup(smem_bytes, u, act);                     \
   }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \

@@ -43,13 +43,14 @@
 
 namespace sl {
 
-constexpr int SPLIT_MAX_WARPS = 16;  // warps per CTA, upper bound
-constexpr int SPLIT_DEFAULT_WARPS = 12;  // default (register budget)
+constexpr int SPLIT_MAX_WARPS = 12;  // warps per CTA (register budget)
+constexpr int SPLIT_DEFAULT_WARPS = 12;
 constexpr double SENTINEL_POS = 1.0e15;  // |d| finite, k = 0 => force 0
 
 struct SplitCfg {
   int64_t n_slices;
   int u;                 // gather batch (rows per batch; stage rows padded)
+  int act;               // actuated fast path (ActP groups in use)
   int cap_a, cap_b;      // stage capacity, rows (widest sections padded to u)
   int warps;             // warps per CTA
   uint32_t stage_bytes;  // pos + vel + A words + B words + A (k, L0)
@@ -59,11 +60,13 @@ __device__ __forceinline__ uint32_t split_partner(uint32_t w, int a) {
   return ((w >> a) & ~31u) | (w & 31u);
 }
 
-// Force on this mass from one entry, fast form (see header comment).
-template <int P>
+// Force on this mass from one entry, fast form (see header comment);
+// `factor` scales the rest length (actuation, 1 otherwise).
+template <int P, bool ACT>
 __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
                                            typename Tr<P>::R4 o,
                                            typename Tr<P>::F2 kl,
+                                           float factor,
                                            typename Tr<P>::R &fx,
                                            typename Tr<P>::R &fy,
                                            typename Tr<P>::R &fz) {
@@ -78,22 +81,61 @@ __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
     r = (double)rsqrtf((float)len2);
     r = r * (1.5 - 0.5 * len2 * r * r);  // one Newton step, ~1e-14
   }
-  const M sc = (M)kl.x * (len2 * r - (M)kl.y) * r;
+  M l0 = (M)kl.y;
+  if constexpr (ACT) l0 = (M)factor * l0;
+  const M sc = (M)kl.x * (len2 * r - l0) * r;
   fx += (R)(sc * dx);
   fy += (R)(sc * dy);
   fz += (R)(sc * dz);
 }
 
-// Fast spring forces of one mass.  ja / jb / kla point at the lane's first
-// A word, B word and A (k, L0) (lane-strided by 32; shared-memory stage or
-// global memory); wa / wb are the slice's section widths.
-template <int P, int U, bool PADDED>
+// ---------------------------------------------------------------------------
+// Sine actuation in the fast path (reference kernels.py:55-65 mode 1,
+// actuation.py:57-69): factor = 1 + amp sin(freq t), t = (T - off) mod per.
+// Springs are grouped by (amp, freq, per) -- a swarm of worm robots has
+// one group -- and each (k, L0) cell gets a companion act cell (off mod per,
+// group).  Per step every CTA computes the group phases (T mod per) once in
+// fp64; per entry t = phase - off, wrapped into [0, per), then a reduced
+// MUFU.SIN.  Group 0 is "not actuated" (amp 0: factor exactly 1).  Both
+// endpoints evaluate the same factor from the same bits.  Quiescent-before-
+// offset and callable waveforms stay on the exact per-entry path.
+constexpr int MAX_ACT_GROUPS = 64;
+struct ActP {
+  int n;  // groups in use (incl. group 0)
+  float amp[MAX_ACT_GROUPS], freq[MAX_ACT_GROUPS], per[MAX_ACT_GROUPS];
+  double perd[MAX_ACT_GROUPS];
+};
+
+// block-wide: (amp, freq, per, T mod per) of every group into shared memory
+__device__ __forceinline__ void act_table(const ActP &A, double sim_t,
+                                          float4 *tab) {
+  for (int g = threadIdx.x; g < A.n; g += blockDim.x)
+    tab[g] = make_float4(A.amp[g], A.freq[g], A.per[g],
+                         (float)py_mod(sim_t, A.perd[g]));
+  __syncthreads();
+}
+
+__device__ __forceinline__ float act_fast(const float4 *tab, float2 ac) {
+  const float4 G = tab[__float_as_uint(ac.y)];  // amp, freq, per, phase
+  float t = G.w - ac.x;
+  t = t < 0.f ? t + G.z : t;
+  float x = G.y * t;
+  x = fmaf(-6.28318530717958647692f, rintf(x * 0.15915494309189533577f), x);
+  return fmaf(G.x, __sinf(x), 1.0f);
+}
+
+// Fast spring forces of one mass.  ja / jb / kla (/ kaa) point at the lane's
+// first A word, B word, A (k, L0) (and A act cell), lane-strided by 32
+// (shared-memory stage or global memory); wa / wb are the slice's section
+// widths; tab is the block's actuation table (ACT only).
+template <int P, int U, bool PADDED, bool ACT>
 __device__ __forceinline__ void split_fast(const KState &S,
                                            const typename Tr<P>::R4 *pos,
                                            const uint32_t *ja,
                                            const uint32_t *jb,
                                            const typename Tr<P>::F2 *kla,
-                                           int wa, int wb,
+                                           const float2 *kaa,
+                                           const float4 *tab, int wa, int wb,
                                            typename Tr<P>::R4 me,
                                            typename Tr<P>::R &fx,
                                            typename Tr<P>::R &fy,
@@ -102,7 +144,11 @@ __device__ __forceinline__ void split_fast(const KState &S,
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S.sp_kl;
+  const float2 *gact = S.sp_act;
   const int a = S.sp_a;
+  auto fa = [&](int row) {
+    return ACT ? act_fast(tab, kaa[32 * row]) : 1.0f;
+  };
   if constexpr (PADDED) {
     // stage rows are padded to whole batches: batch t of section A and
     // batch t of section B issue all their gathers together (one exposed L2
@@ -112,6 +158,7 @@ __device__ __forceinline__ void split_fast(const KState &S,
     for (int t = 0; t < wa || t < wb; t += U) {
       R4 oa[U], ob[U];
       F2 kb[U];
+      float2 ab[U];
       const bool has_a = t < wa, has_b = t < wb;  // warp-uniform
       if (has_a) {
 #pragma unroll
@@ -122,17 +169,21 @@ __device__ __forceinline__ void split_fast(const KState &S,
         for (int u = 0; u < U; u++) {
           const uint32_t w = jb[32 * (t + u)];
           kb[u] = __ldg(gkl + w);
+          if constexpr (ACT) ab[u] = __ldg(gact + w);
           ob[u] = ldg4(pos + split_partner(w, a));
         }
       }
       if (has_a) {
 #pragma unroll
         for (int u = 0; u < U; u++)
-          split_body<P>(me, oa[u], kla[32 * (t + u)], fx, fy, fz);
+          split_body<P, ACT>(me, oa[u], kla[32 * (t + u)], fa(t + u), fx, fy,
+                             fz);
       }
       if (has_b) {
 #pragma unroll
-        for (int u = 0; u < U; u++) split_body<P>(me, ob[u], kb[u], bx, by, bz);
+        for (int u = 0; u < U; u++)
+          split_body<P, ACT>(me, ob[u], kb[u],
+                             ACT ? act_fast(tab, ab[u]) : 1.0f, bx, by, bz);
       }
     }
     fx += bx;
@@ -148,22 +199,28 @@ __device__ __forceinline__ void split_fast(const KState &S,
       if (t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wa) split_body<P>(me, o[u], kla[32 * (t + u)], fx, fy, fz);
+      if (t + u < wa)
+        split_body<P, ACT>(me, o[u], kla[32 * (t + u)], fa(t + u), fx, fy,
+                           fz);
   }
   // section B: (k, L0) gathered from the partner's A cell (L2)
   for (int t = 0; t < wb; t += U) {
     R4 o[U];
     F2 kl[U];
+    float2 ab[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (t + u < wb) {
         const uint32_t w = jb[32 * (t + u)];
         kl[u] = __ldg(gkl + w);
+        if constexpr (ACT) ab[u] = __ldg(gact + w);
         o[u] = ldg4(pos + split_partner(w, a));
       }
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wb) split_body<P>(me, o[u], kl[u], fx, fy, fz);
+      if (t + u < wb)
+        split_body<P, ACT>(me, o[u], kl[u], ACT ? act_fast(tab, ab[u]) : 1.0f,
+                           fx, fy, fz);
   }
 }
 
@@ -247,17 +304,18 @@ __device__ __noinline__ Vec3R<typename Tr<P>::R> split_special(
   return {fx, fy, fz};
 }
 
-template <int P, int U, bool PADDED>
+template <int P, int U, bool PADDED, bool ACT>
 __device__ __forceinline__ void split_forces(
     const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
-    const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
-    int64_t ea, int64_t eb, uint32_t fl, typename Tr<P>::R4 me,
-    double sim_t, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
-    typename Tr<P>::R &fz) {
+    const uint32_t *jb, const typename Tr<P>::F2 *kla, const float2 *kaa,
+    const float4 *tab, int wa, int wb, int64_t ea, int64_t eb, uint32_t fl,
+    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   if (!(fl & MF_SPECIAL)) {
     R gx = fx, gy = fy, gz = fz;
-    split_fast<P, U, PADDED>(S, pos, ja, jb, kla, wa, wb, me, gx, gy, gz);
+    split_fast<P, U, PADDED, ACT>(S, pos, ja, jb, kla, kaa, tab, wa, wb, me,
+                                  gx, gy, gz);
     if (isfinite(gx + gy + gz)) {
       fx = gx;
       fy = gy;
@@ -274,15 +332,17 @@ __device__ __forceinline__ void split_forces(
 
 // Plain variant: one thread per mass, entries read from global memory.
 // Serves spring_pass (FORCE_ONLY) and layouts too wide for the TMA stages.
-template <int P, bool FORCE_ONLY>
+template <int P, bool FORCE_ONLY, bool ACT>
 __global__ void __launch_bounds__(256)
-    k_split_step(const KState S, const EnvP E, const StepP T) {
+    k_split_step(const KState S, const EnvP E, const StepP T, const ActP A) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
+  __shared__ float4 tab[ACT ? MAX_ACT_GROUPS : 1];
+  if (!FORCE_ONLY && stopped(S, T.step)) return;  // uniform
+  if constexpr (ACT) act_table(A, T.sim_t, tab);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S.m_n) return;
-  if (!FORCE_ONLY && stopped(S, T.step)) return;
   const R4 *pos = (const R4 *)S.pos[T.cur];
   const R4 v = ((const R4 *)S.vel)[i];
   const uint32_t fl = flags_of(v.w);
@@ -294,9 +354,12 @@ __global__ void __launch_bounds__(256)
   const uint32_t wd = __ldg(S.sp_w + w);
   const int64_t ea = w * S.sp_rows * 32 + (i & 31);
   const int64_t eb = ea + ((int64_t)32 << S.sp_a);
-  const F2 *kla = (const F2 *)S.sp_kl + ((w << (S.sp_a + 5)) | (i & 31));
-  split_forces<P, 4, false>(S, pos, S.sp_j + ea, S.sp_j + eb, kla, wd & 0xFFFF,
-                     wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
+  const int64_t kc = (w << (S.sp_a + 5)) | (i & 31);
+  split_forces<P, 4, false, ACT>(S, pos, S.sp_j + ea, S.sp_j + eb,
+                                 (const F2 *)S.sp_kl + kc,
+                                 ACT ? S.sp_act + kc : nullptr, tab,
+                                 wd & 0xFFFF, wd >> 16, ea, eb, fl, me,
+                                 T.sim_t, fx, fy, fz);
   finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
 }
 
@@ -306,15 +369,17 @@ __global__ void __launch_bounds__(256)
 // shared-memory ring; lane 0 streams the next slice (pos, vel, A words,
 // B words, A (k, L0): five bulk async copies on one mbarrier) while the warp
 // computes the current one.
-template <int P, int U, int MW>
-__global__ void __launch_bounds__(MW * 32)
+template <int P, int U, bool ACT>
+__global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
     k_split_tma(const KState S, const EnvP E, const StepP T,
-                const SplitCfg C) {
+                const SplitCfg C, const ActP A) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ float4 tab[ACT ? MAX_ACT_GROUPS : 1];
   if (stopped(S, T.step)) return;  // uniform across the grid
+  if constexpr (ACT) act_table(A, T.sim_t, tab);
   // warp index broadcast from lane 0: provably warp-uniform for ptxas, so
   // the stage addresses below live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
@@ -326,6 +391,7 @@ __global__ void __launch_bounds__(MW * 32)
   const uint32_t ja_off = 2 * MB;
   const uint32_t jb_off = ja_off + (uint32_t)C.cap_a * 128u;
   const uint32_t kl_off = jb_off + (uint32_t)C.cap_b * 128u;
+  const uint32_t ac_off = kl_off + (uint32_t)C.cap_a * 32u * sizeof(F2);
   if (lane == 0) {
     mbar_init(bars + 0, 1);
     mbar_init(bars + 1, 1);
@@ -347,12 +413,14 @@ __global__ void __launch_bounds__(MW * 32)
     unsigned char *dst = ring + (stage ? C.stage_bytes : 0u);
     const uint32_t *jsl = S.sp_j + su * rows32u;
     const uint32_t kb = wa * 32u * (uint32_t)sizeof(F2);
-    bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb, dst,
+    const uint32_t ab = ACT ? wa * 32u * 8u : 0u;
+    bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb + ab, dst,
                      pos + su * 32u, MB, dst + MB,
                      (const R4 *)S.vel + su * 32u, MB, dst + ja_off, jsl,
                      wa * 128u, dst + kl_off,
                      (const F2 *)S.sp_kl + (su << (a + 5)), kb, dst + jb_off,
-                     jsl + jb_rel, wb * 128u);
+                     jsl + jb_rel, wb * 128u, dst + ac_off,
+                     S.sp_act + (su << (a + 5)), ab);
   };
   // slice widths, loaded by every lane (one transaction) and broadcast
   auto widths = [&](int64_t sl) {
@@ -383,11 +451,14 @@ __global__ void __launch_bounds__(MW * 32)
       uint32_t *sja = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
                                    ja_off) + lane;
       F2 *skl = (F2 *)(ring + (size_t)stage * C.stage_bytes + kl_off) + lane;
+      float2 *sac = (float2 *)(ring + (size_t)stage * C.stage_bytes + ac_off) +
+                    lane;
       F2 zero;
       zero.x = zero.y = 0;
       for (int r = wa; r < (wa + U - 1) / U * U; r++) {
         sja[32 * r] = S.sp_sent;
         skl[32 * r] = zero;
+        if (ACT) sac[32 * r] = make_float2(0.f, 0.f);
       }
       uint32_t *sjb = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
                                    jb_off) + lane;
@@ -403,10 +474,12 @@ __global__ void __launch_bounds__(MW * 32)
         initial_force<P>(S, i, fl, false, fx, fy, fz);
         const int64_t ea = s * rows32 + lane;
         const int64_t eb = ea + ((int64_t)32 << a);
-        split_forces<P, U, true>(S, pos, (const uint32_t *)(st + ja_off) + lane,
-                           (const uint32_t *)(st + jb_off) + lane,
-                           (const F2 *)(st + kl_off) + lane, wd & 0xFFFF,
-                           wd >> 16, ea, eb, fl, me, T.sim_t, fx, fy, fz);
+        split_forces<P, U, true, ACT>(
+            S, pos, (const uint32_t *)(st + ja_off) + lane,
+            (const uint32_t *)(st + jb_off) + lane,
+            (const F2 *)(st + kl_off) + lane,
+            (const float2 *)(st + ac_off) + lane, tab, wd & 0xFFFF, wd >> 16,
+            ea, eb, fl, me, T.sim_t, fx, fy, fz);
         finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
       }
     }
