@@ -27,7 +27,6 @@ import os
 import statistics
 import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -163,54 +162,75 @@ def time_oracle(st, env, steps: int, warmup: int, threads: int,
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        self.proc = None
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    NVML (nvidia_ml_py) polled every ~2 ms from a thread: the step call
+    releases the GIL (ctypes), so the samples land inside the region even
+    when it lasts only a few tens of ms.  Falls back to one nvidia-smi
+    query after the region when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40,
+               "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        import threading
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop_evt = threading.Event()
+        self.thread = None
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
-                stdout=self.fh, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(
+                self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.nv = None
+            return
+        self.period = period_s
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _sample(self):
+        nv = self.nv
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h,
+                                                       nv.NVML_CLOCK_SM)))
+        self.mx.append(float(self.max_mhz))
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for nm, b in self.REASONS.items():
+            if bits & b:
+                self.reasons.add(nm)
+
+    def _run(self):
+        while not self.stop_evt.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.stop_evt.wait(self.period)
 
     def stop(self) -> dict | None:
-        if self.proc is None:
-            return None
-        self.proc.terminate()
+        if self.thread is None:
+            return self._smi_once()
+        self.stop_evt.set()
+        self.thread.join(timeout=5)
+        if not self.sm:
+            return self._smi_once()
+        return {"sm_mhz": statistics.median(self.sm),
+                "sm_max_mhz": max(self.mx), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml, 2 ms"}
+
+    @staticmethod
+    def _smi_once():
         try:
-            self.proc.wait(timeout=5)
+            out = subprocess.run(
+                ["nvidia-smi", "-i", "0", "--query-gpu=clocks.sm,clocks.max.sm",
+                 "--format=csv,noheader,nounits"], capture_output=True,
+                text=True, timeout=10).stdout.split(",")
+            return {"sm_mhz": float(out[0]), "sm_max_mhz": float(out[1]),
+                    "reasons": [], "samples": 1,
+                    "source": "nvidia-smi after the region"}
         except Exception:
-            self.proc.kill()
-        self.fh.close()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                 "sw_power_cap"]
-        with open(self.path) as fh:
-            for line in fh:
-                p = [x.strip() for x in line.split(",")]
-                if len(p) < 8:
-                    continue
-                try:
-                    sm.append(float(p[0]))
-                    mx.append(float(p[1]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, p[4:8]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-        os.unlink(self.path)
-        if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
 
 
 def peak_hbm():

@@ -104,7 +104,7 @@ struct sl_ctx {
   int split_warps = 0, split_grid = 0;
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
-  DevBuf s_grp, s_aoff, sp_act;
+  DevBuf s_grp, sp_actc, sp_acto;
   // partitioned runs
   DevBuf ghost;
   bool has_ghost = false;
@@ -317,15 +317,13 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
                                double4 *act_o, uint8_t *degen_o,
                                double *custom_o, int params_only,
                                int layout_valid, const uint8_t *grp_in,
-                               const float *aoff_in, uint8_t *grp_o,
-                               float *aoff_o) {
+                               uint8_t *grp_o) {
   using F = typename Tr<P>::F;
   using F2 = typename Tr<P>::F2;
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   int64_t s = slots ? slots[r] : r;
   grp_o[s] = grp_in[r];
-  aoff_o[s] = aoff_in[r];
   F2 kl;
   kl.x = (F)k[r];
   kl.y = (F)rest[r];
@@ -358,9 +356,10 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
     if (S.split) {
       if (ab.x >= 0 && S.e1[s] >= 0) {
         ((F2 *)S.sp_kl)[S.sp_ekl[s]] = kl;
-        if (S.sp_act)
-          ((float2 *)S.sp_act)[S.sp_ekl[s]] =
-              make_float2(aoff_in[r], __uint_as_float(grp_in[r]));
+        if (S.sp_actc) {
+          S.sp_actc[S.sp_ekl[s]] = act_cell(off[r], freq[r], per[r], grp_in[r]);
+          S.sp_acto[S.sp_ekl[s]] = off[r];
+        }
       }
       return;
     }
@@ -553,8 +552,8 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
                              const int64_t *start, KState S, uint32_t *sp_j,
                              void *sp_kl, int32_t *sp_s, uint32_t *sp_ekl,
                              int64_t *e1, int64_t *e2, int pass,
-                             float2 *sp_act, const uint8_t *grp,
-                             const float *aoff) {
+                             float4 *sp_actc, double *sp_acto,
+                             const uint8_t *grp) {
   using F = typename Tr<P>::F;
   using F2 = typename Tr<P>::F2;
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -571,8 +570,11 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
     uint32_t kli = (uint32_t)((sl << (S.sp_a + 5)) | (r << 5) | lane);
     sp_j[e] = (uint32_t)ab.y;
     ((F2 *)sp_kl)[kli] = ((const F2 *)S.kL0)[s];
-    if (sp_act)
-      sp_act[kli] = make_float2(aoff[s], __uint_as_float((uint32_t)grp[s]));
+    if (sp_actc) {
+      const double4 ac = S.act[s];
+      sp_actc[kli] = act_cell(ac.z, ac.y, ac.w, grp[s]);
+      sp_acto[kli] = ac.z;
+    }
     sp_s[e] = (int32_t)s;
     sp_ekl[s] = kli;
     e1[s] = e;
@@ -635,7 +637,9 @@ KState make_state(sl_ctx *c) {
     S.sp_s = c->sp_s.as<int32_t>();
     S.sp_w = c->sp_w.as<uint32_t>();
     S.sp_ekl = c->sp_ekl.as<uint32_t>();
-    S.sp_act = c->agrp.n > 1 ? c->sp_act.as<float2>() : nullptr;
+    const bool act = c->agrp.n > 1;
+    S.sp_actc = act ? c->sp_actc.as<float4>() : nullptr;
+    S.sp_acto = act ? c->sp_acto.as<double>() : nullptr;
   }
   return S;
 }
@@ -685,7 +689,6 @@ int ensure_springs(sl_ctx *c, int64_t s_n) {
   CK(c->m1gen.ensure(8 * s_n));
   CK(c->m2gen.ensure(8 * s_n));
   CK(c->s_grp.ensure(s_n));
-  CK(c->s_aoff.ensure(4 * s_n));
   return SL_OK;
 }
 
@@ -864,7 +867,7 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   const int64_t cap_b = (c->sp_wb + u - 1) / u * u;
   const size_t stage = 2 * 32 * 4 * c->rsz + (size_t)(cap_a + cap_b) * 128 +
                        (size_t)cap_a * 32 * 2 * c->fsz +
-                       (act ? (size_t)cap_a * 32 * 8 : 0);
+                       (act ? (size_t)cap_a * 32 * 16 : 0);
   const size_t per_warp = 2 * stage + 16;
   int want = SPLIT_DEFAULT_WARPS;
   if (const char *ev = getenv("SL_SPLIT_WARPS"))  // tuning override
@@ -960,8 +963,11 @@ int build_split_layout(sl_ctx *c, bool *used) {
   CK(cudaMemsetAsync(c->sp_kl.p, 0, f2 * n_kl, c->st));
   const bool act = c->agrp.n > 1;
   if (act) {
-    CK(c->sp_act.ensure(8 * n_kl));
-    CK(cudaMemsetAsync(c->sp_act.p, 0, 8 * n_kl, c->st));
+    CK(c->sp_actc.ensure(16 * n_kl));
+    CK(c->sp_acto.ensure(8 * n_kl));
+    // zero cells = group 0 (factor exactly 1: amp 0)
+    CK(cudaMemsetAsync(c->sp_actc.p, 0, 16 * n_kl, c->st));
+    CK(cudaMemsetAsync(c->sp_acto.p, 0, 8 * n_kl, c->st));
   }
   CK(cudaMemsetAsync(c->sp_s.p, 0xFF, 4 * n_j, c->st));
   CK(cudaMemsetAsync(c->xflags.p, 0, m_n + 1, c->st));
@@ -1007,8 +1013,8 @@ int build_split_layout(sl_ctx *c, bool *used) {
           (uint32_t)(2 * m_n), c->start.as<int64_t>(), S,
           c->sp_j.as<uint32_t>(), c->sp_kl.p, c->sp_s.as<int32_t>(),
           c->sp_ekl.as<uint32_t>(), c->e1.as<int64_t>(), c->e2.as<int64_t>(),
-          pass, act ? c->sp_act.as<float2>() : nullptr,
-          c->s_grp.as<uint8_t>(), c->s_aoff.as<float>());
+          pass, act ? c->sp_actc.as<float4>() : nullptr,
+          c->sp_acto.as<double>(), c->s_grp.as<uint8_t>());
       CKL();
     }
   }
@@ -1168,7 +1174,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
-                    &c->ghost, &c->s_grp, &c->s_aoff, &c->sp_act};
+                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -1304,44 +1310,43 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
                   (long long)(slots ? slots[r] : r));
     if (mode[r] != 0 || yield[r] != INFINITY) c->has_special = true;
   }
-  // group plain-sine actuation (mode 1) by (amp, freq, per) for the split
-  // fast path; group 0 = not actuated, 0 also when the table is full (the
-  // spring then takes the exact path)
+  // group sine actuation (modes 1, 2) by (mode, amp, freq, per) for the
+  // split fast path of the fp32 mode; group 0 = not actuated, 0 also when
+  // the table is full (the spring then takes the exact path).  The mixed
+  // mode keeps actuated springs on the exact path: its fp64 sin holds the
+  // 1e-9 split-vs-exact bar that the fast path's fp32 sin cannot.
   if (!params_only) {
     memset(&c->agrp, 0, sizeof c->agrp);
     c->agrp.n = 1;
-    c->agrp.per[0] = 1.0f;
-    c->agrp.perd[0] = 1.0;
+    c->agrp.per[0] = 1.0;
+    c->agrp.inv_per[0] = 1.0;
   }
   const int groups_before = c->agrp.n;
   std::vector<uint8_t> grp(n, 0);
-  std::vector<float> aoff(n, 0.0f);
   for (int64_t r = 0; r < n; r++) {
-    if (mode[r] != 1) continue;
+    if ((mode[r] != 1 && mode[r] != 2) || c->prec != PREC_FP32) continue;
+    if (!(per[r] > 0.0) || !std::isfinite(per[r]) || !std::isfinite(freq[r]))
+      continue;
     int g = 1;
     for (; g < c->agrp.n; g++)
-      if (c->agrp.amp[g] == (float)amp[r] && c->agrp.freq[g] == (float)freq[r]
-          && c->agrp.perd[g] == per[r])
+      if (c->agrp.mode[g] == mode[r] && c->agrp.amp[g] == (float)amp[r] &&
+          c->agrp.freq[g] == freq[r] && c->agrp.per[g] == per[r])
         break;
     if (g == c->agrp.n) {
       if (g >= MAX_ACT_GROUPS) continue;
+      c->agrp.mode[g] = mode[r];
       c->agrp.amp[g] = (float)amp[r];
-      c->agrp.freq[g] = (float)freq[r];
-      c->agrp.per[g] = (float)per[r];
-      c->agrp.perd[g] = per[r];
+      c->agrp.freq[g] = freq[r];
+      c->agrp.per[g] = per[r];
+      c->agrp.inv_per[g] = 1.0 / per[r];
       c->agrp.n++;
     }
     grp[r] = (uint8_t)g;
-    // Python floor-mod (kernels.py:58) of the offset, done once in fp64
-    double t = fmod(off_[r], per[r]);
-    if (t != 0.0 && ((t < 0.0) != (per[r] < 0.0))) t += per[r];
-    aoff[r] = (float)t;
   }
   // first actuated group on a live split layout: re-layout with act cells
   if (params_only && groups_before <= 1 && c->agrp.n > 1 && c->split)
     c->layout_valid = false;
-  size_t need = align256(8 * n) * 16 + align256(n) * 5 + align256(4 * n) +
-                2048;
+  size_t need = align256(8 * n) * 16 + align256(n) * 5 + 2048;
   CK(c->stage.ensure(need));
   size_t off = 0;
   const int64_t *dsl = nullptr, *d1 = nullptr, *d2 = nullptr, *dg1 = nullptr,
@@ -1369,9 +1374,7 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
   if ((rc = stage_copy(c, off, off_, n, &doff))) return rc;
   if ((rc = stage_copy(c, off, per, n, &dper))) return rc;
   const uint8_t *dgrp;
-  const float *daoff;
   if ((rc = stage_copy(c, off, grp.data(), n, &dgrp))) return rc;
-  if ((rc = stage_copy(c, off, aoff.data(), n, &daoff))) return rc;
   if (n > 0) {
     KState S = make_state(c);
     auto kk = c->prec == PREC_FP64   ? k_pack_springs<PREC_FP64>
@@ -1382,8 +1385,7 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
         dal, dde, S, c->m1gen.as<int64_t>(), c->m2gen.as<int64_t>(),
         c->mode.as<int8_t>(), c->act.as<double4>(),
         c->s_degen.as<uint8_t>(), c->custom.as<double>(), params_only,
-        c->layout_valid, dgrp, daoff, c->s_grp.as<uint8_t>(),
-        c->s_aoff.as<float>());
+        c->layout_valid, dgrp, c->s_grp.as<uint8_t>());
     CKL();
     c->launches++;
   }

@@ -111,7 +111,8 @@ struct KState {
   const int32_t *sp_s;
   const uint32_t *sp_w;
   const uint32_t *sp_ekl;  // per spring: kl index of its A cell
-  const float2 *sp_act;    // actuation cell per kl cell (null: none)
+  float4 *sp_actc;         // act cell per kl cell (null: no groups)
+  double *sp_acto;         // exact fp64 act offset per kl cell
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };

@@ -90,42 +90,108 @@ __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
 }
 
 // ---------------------------------------------------------------------------
-// Sine actuation in the fast path (reference kernels.py:55-65 mode 1,
-// actuation.py:57-69): factor = 1 + amp sin(freq t), t = (T - off) mod per.
-// Springs are grouped by (amp, freq, per) -- a swarm of worm robots has
-// one group -- and each (k, L0) cell gets a companion act cell (off mod per,
-// group).  Per step every CTA computes the group phases (T mod per) once in
-// fp64; per entry t = phase - off, wrapped into [0, per), then a reduced
-// MUFU.SIN.  Group 0 is "not actuated" (amp 0: factor exactly 1).  Both
-// endpoints evaluate the same factor from the same bits.  Quiescent-before-
-// offset and callable waveforms stay on the exact per-entry path.
+// Sine actuation in the fast path of the fp32 mode (reference
+// kernels.py:55-65 modes 1 and 2, actuation.py:57-69):
+// factor = 1 + amp sin(freq t), t = (T - off) mod per (Python floor-mod),
+// mode 2 only once T >= off.  Springs are grouped by (mode, amp, freq, per)
+// -- a swarm of worm robots has one group -- and each (k, L0) cell gets a
+// companion 16-byte act cell (o, sin B, cos B, group) with o = off mod per
+// and B = freq o, computed once in fp64 when the layout is built.  Per step
+// every CTA computes each group's phase P = T mod per and the angles
+// A = freq P, A' = freq (P + per) in fp64, as (sin, cos) pairs in shared
+// memory.  Per entry t = P - o (+ per when negative), and
+//   sin(freq t) = sin(A - B) = sin A cos B - cos A sin B   (A' if wrapped),
+// two FMAs instead of a range reduction and a polynomial.
+//
+// The waveform is discontinuous at every wrap (freq per is not a multiple
+// of 2 pi), so the wrap DECISION must be the reference's: an entry whose
+// fp32 t lies within eps = 1e-6 per of 0 or per (the fp32 path's error is
+// < 3e-7 per), and every mode-2 entry, is recomputed from the spring's exact
+// fp64 offset (sp_acto) with the reference's own arithmetic: d = T - off,
+// then a floor-mod whose quotient is corrected to the exact one.  Group 0 is
+// "not actuated" (amp 0: factor exactly 1).  Both endpoints evaluate the
+// same factor from the same bits.  Callable waveforms stay on the exact
+// per-entry path.
 constexpr int MAX_ACT_GROUPS = 64;
 struct ActP {
   int n;  // groups in use (incl. group 0)
-  float amp[MAX_ACT_GROUPS], freq[MAX_ACT_GROUPS], per[MAX_ACT_GROUPS];
-  double perd[MAX_ACT_GROUPS];
+  int8_t mode[MAX_ACT_GROUPS];
+  float amp[MAX_ACT_GROUPS];
+  double freq[MAX_ACT_GROUPS], per[MAX_ACT_GROUPS], inv_per[MAX_ACT_GROUPS];
+};
+struct ActG {  // one group, shared-memory copy for the current step
+  float sa, ca, saw, caw;  // sin/cos of A = freq P and A' = freq (P + per)
+  float phase, per, eps, amp;
+  uint32_t quiescent, pad_;  // mode 2: factor 1 while T < off (slow path)
+  double freqd, perd, inv_per;
 };
 
-// block-wide: (amp, freq, per, T mod per) of every group into shared memory
+// act cell of one spring (device: py_mod lives in sl_device.cuh)
+__device__ __forceinline__ float4 act_cell(double off, double freq,
+                                           double per, uint32_t grp) {
+  if (grp == 0) return make_float4(0.f, 0.f, 1.f, 0.f);
+  const double o = py_mod(off, per);
+  double sb, cb;
+  sincos(freq * o, &sb, &cb);
+  return make_float4((float)o, (float)sb, (float)cb, __uint_as_float(grp));
+}
+
+// block-wide: the group table for step time sim_t into shared memory
 __device__ __forceinline__ void act_table(const ActP &A, double sim_t,
-                                          float4 *tab) {
-  for (int g = threadIdx.x; g < A.n; g += blockDim.x)
-    tab[g] = make_float4(A.amp[g], A.freq[g], A.per[g],
-                         (float)py_mod(sim_t, A.perd[g]));
+                                          ActG *tab) {
+  for (int g = threadIdx.x; g < A.n; g += blockDim.x) {
+    const double p = py_mod(sim_t, A.per[g]);
+    double sa, ca, saw, caw;
+    sincos(A.freq[g] * p, &sa, &ca);
+    sincos(A.freq[g] * (p + A.per[g]), &saw, &caw);
+    const float per = (float)A.per[g];
+    tab[g] = ActG{(float)sa, (float)ca, (float)saw, (float)caw, (float)p,
+                  per, per * 1e-6f, A.amp[g], A.mode[g] == 2 ? 1u : 0u, 0u,
+                  A.freq[g], A.per[g], A.inv_per[g]};
+  }
   __syncthreads();
 }
 
-__device__ __forceinline__ float act_fast(const float4 *tab, float2 ac) {
-  const float4 G = tab[__float_as_uint(ac.y)];  // amp, freq, per, phase
-  float t = G.w - ac.x;
-  t = t < 0.f ? t + G.z : t;
-  float x = G.y * t;
-  x = fmaf(-6.28318530717958647692f, rintf(x * 0.15915494309189533577f), x);
-  return fmaf(G.x, __sinf(x), 1.0f);
+// Exact-phase factor (rare: near a wrap, or mode 2).  floor-mod: r = d -
+// q per for q = floor(d / per) exactly; the estimate is off by at most one
+// and corrected by the sign of the exact residual (fma rounds once, never
+// across zero), so r is the correctly rounded d - q per -- the value
+// Python's fmod-then-add produces (kernels.py:58, SURVEY.md 7 hard part 2).
+static __device__ __noinline__ float act_slow(const ActG *G, double off,
+                                              double sim_t) {
+  if (G->quiescent && !(sim_t >= off)) return 1.0f;  // kernels.py:61
+  const double d = sim_t - off;
+  const double per = G->perd;
+  const double q = floor(d * G->inv_per);
+  double r = fma(-q, per, d);
+  if (r < 0.0) {
+    r = fma(-(q - 1.0), per, d);
+  } else {
+    const double r2 = fma(-(q + 1.0), per, d);
+    r = r2 >= 0.0 ? r2 : r;
+  }
+  return (float)(1.0 + (double)G->amp * sin(G->freqd * r));
+}
+
+// factor of act cell c; kli() yields its kl index (slow path only)
+template <class K>
+__device__ __forceinline__ float act_fast(const ActG *tab, float4 c,
+                                          const double *acto, K kli,
+                                          double sim_t) {
+  const ActG *G = tab + __float_as_uint(c.w);
+  const float4 sc = *(const float4 *)G;  // sa, ca, saw, caw
+  const float4 pp = *(const float4 *)&G->phase;  // phase, per, eps, amp
+  const float d = pp.x - c.x;
+  const bool wrap = d < 0.f;
+  const float t = wrap ? d + pp.y : d;
+  if ((t < pp.z) | (t > pp.y - pp.z) | (G->quiescent != 0u))
+    return act_slow(G, acto[kli()], sim_t);
+  const float sa = wrap ? sc.z : sc.x, ca = wrap ? sc.w : sc.y;
+  return fmaf(pp.w, fmaf(sa, c.z, -ca * c.y), 1.0f);
 }
 
 // Fast spring forces of one mass.  ja / jb / kla (/ kaa) point at the lane's
-// first A word, B word, A (k, L0) (and A act cell), lane-strided by 32
+// first A word, B word, A (k, L0) (and A act key), lane-strided by 32
 // (shared-memory stage or global memory); wa / wb are the slice's section
 // widths; tab is the block's actuation table (ACT only).
 template <int P, int U, bool PADDED, bool ACT>
@@ -134,8 +200,10 @@ __device__ __forceinline__ void split_fast(const KState &S,
                                            const uint32_t *ja,
                                            const uint32_t *jb,
                                            const typename Tr<P>::F2 *kla,
-                                           const float2 *kaa,
-                                           const float4 *tab, int wa, int wb,
+                                           const float4 *kaa,
+                                           uint32_t kc0, const ActG *tab,
+                                           double sim_t,
+                                           int wa, int wb,
                                            typename Tr<P>::R4 me,
                                            typename Tr<P>::R &fx,
                                            typename Tr<P>::R &fy,
@@ -144,10 +212,13 @@ __device__ __forceinline__ void split_fast(const KState &S,
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S.sp_kl;
-  const float2 *gact = S.sp_act;
+  const float4 *gact = S.sp_actc;
+  const double *acto = S.sp_acto;
   const int a = S.sp_a;
   auto fa = [&](int row) {
-    return ACT ? act_fast(tab, kaa[32 * row]) : 1.0f;
+    return ACT ? act_fast(tab, kaa[32 * row], acto,
+                          [&] { return kc0 + 32u * row; }, sim_t)
+               : 1.0f;
   };
   if constexpr (PADDED) {
     // stage rows are padded to whole batches: batch t of section A and
@@ -158,7 +229,7 @@ __device__ __forceinline__ void split_fast(const KState &S,
     for (int t = 0; t < wa || t < wb; t += U) {
       R4 oa[U], ob[U];
       F2 kb[U];
-      float2 ab[U];
+      float4 ab[U];
       const bool has_a = t < wa, has_b = t < wb;  // warp-uniform
       if (has_a) {
 #pragma unroll
@@ -183,7 +254,11 @@ __device__ __forceinline__ void split_fast(const KState &S,
 #pragma unroll
         for (int u = 0; u < U; u++)
           split_body<P, ACT>(me, ob[u], kb[u],
-                             ACT ? act_fast(tab, ab[u]) : 1.0f, bx, by, bz);
+                             ACT ? act_fast(tab, ab[u], acto,
+                                            [&] { return jb[32 * (t + u)]; },
+                                            sim_t)
+                                 : 1.0f,
+                             bx, by, bz);
       }
     }
     fx += bx;
@@ -207,7 +282,7 @@ __device__ __forceinline__ void split_fast(const KState &S,
   for (int t = 0; t < wb; t += U) {
     R4 o[U];
     F2 kl[U];
-    float2 ab[U];
+    float4 ab[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (t + u < wb) {
@@ -219,7 +294,11 @@ __device__ __forceinline__ void split_fast(const KState &S,
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (t + u < wb)
-        split_body<P, ACT>(me, o[u], kl[u], ACT ? act_fast(tab, ab[u]) : 1.0f,
+        split_body<P, ACT>(me, o[u], kl[u],
+                           ACT ? act_fast(tab, ab[u], acto,
+                                          [&] { return jb[32 * (t + u)]; },
+                                          sim_t)
+                               : 1.0f,
                            fx, fy, fz);
   }
 }
@@ -307,15 +386,15 @@ __device__ __noinline__ Vec3R<typename Tr<P>::R> split_special(
 template <int P, int U, bool PADDED, bool ACT>
 __device__ __forceinline__ void split_forces(
     const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
-    const uint32_t *jb, const typename Tr<P>::F2 *kla, const float2 *kaa,
-    const float4 *tab, int wa, int wb, int64_t ea, int64_t eb, uint32_t fl,
+    const uint32_t *jb, const typename Tr<P>::F2 *kla, const float4 *kaa,
+    uint32_t kc0, const ActG *tab, int wa, int wb, int64_t ea, int64_t eb, uint32_t fl,
     typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
     typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   if (!(fl & MF_SPECIAL)) {
     R gx = fx, gy = fy, gz = fz;
-    split_fast<P, U, PADDED, ACT>(S, pos, ja, jb, kla, kaa, tab, wa, wb, me,
-                                  gx, gy, gz);
+    split_fast<P, U, PADDED, ACT>(S, pos, ja, jb, kla, kaa, kc0, tab, sim_t, wa,
+                                  wb, me, gx, gy, gz);
     if (isfinite(gx + gy + gz)) {
       fx = gx;
       fy = gy;
@@ -338,7 +417,7 @@ __global__ void __launch_bounds__(256)
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
-  __shared__ float4 tab[ACT ? MAX_ACT_GROUPS : 1];
+  __shared__ ActG tab[ACT ? MAX_ACT_GROUPS : 1];
   if (!FORCE_ONLY && stopped(S, T.step)) return;  // uniform
   if constexpr (ACT) act_table(A, T.sim_t, tab);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -357,7 +436,8 @@ __global__ void __launch_bounds__(256)
   const int64_t kc = (w << (S.sp_a + 5)) | (i & 31);
   split_forces<P, 4, false, ACT>(S, pos, S.sp_j + ea, S.sp_j + eb,
                                  (const F2 *)S.sp_kl + kc,
-                                 ACT ? S.sp_act + kc : nullptr, tab,
+                                 ACT ? S.sp_actc + kc : nullptr,
+                                 (uint32_t)kc, tab,
                                  wd & 0xFFFF, wd >> 16, ea, eb, fl, me,
                                  T.sim_t, fx, fy, fz);
   finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
@@ -377,7 +457,7 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ float4 tab[ACT ? MAX_ACT_GROUPS : 1];
+  __shared__ ActG tab[ACT ? MAX_ACT_GROUPS : 1];
   if (stopped(S, T.step)) return;  // uniform across the grid
   if constexpr (ACT) act_table(A, T.sim_t, tab);
   // warp index broadcast from lane 0: provably warp-uniform for ptxas, so
@@ -413,14 +493,14 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
     unsigned char *dst = ring + (stage ? C.stage_bytes : 0u);
     const uint32_t *jsl = S.sp_j + su * rows32u;
     const uint32_t kb = wa * 32u * (uint32_t)sizeof(F2);
-    const uint32_t ab = ACT ? wa * 32u * 8u : 0u;
+    const uint32_t ab = ACT ? wa * 32u * 16u : 0u;
     bulk_stage_elect(bars + stage, 2 * MB + (wa + wb) * 128u + kb + ab, dst,
                      pos + su * 32u, MB, dst + MB,
                      (const R4 *)S.vel + su * 32u, MB, dst + ja_off, jsl,
                      wa * 128u, dst + kl_off,
                      (const F2 *)S.sp_kl + (su << (a + 5)), kb, dst + jb_off,
                      jsl + jb_rel, wb * 128u, dst + ac_off,
-                     S.sp_act + (su << (a + 5)), ab);
+                     S.sp_actc + (su << (a + 5)), ab);
   };
   // slice widths, loaded by every lane (one transaction) and broadcast
   auto widths = [&](int64_t sl) {
@@ -451,14 +531,14 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
       uint32_t *sja = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
                                    ja_off) + lane;
       F2 *skl = (F2 *)(ring + (size_t)stage * C.stage_bytes + kl_off) + lane;
-      float2 *sac = (float2 *)(ring + (size_t)stage * C.stage_bytes + ac_off) +
-                    lane;
+      float4 *sac = (float4 *)(ring + (size_t)stage * C.stage_bytes +
+                                 ac_off) + lane;
       F2 zero;
       zero.x = zero.y = 0;
       for (int r = wa; r < (wa + U - 1) / U * U; r++) {
         sja[32 * r] = S.sp_sent;
         skl[32 * r] = zero;
-        if (ACT) sac[32 * r] = make_float2(0.f, 0.f);
+        if (ACT) sac[32 * r] = make_float4(0.f, 0.f, 1.f, 0.f);
       }
       uint32_t *sjb = (uint32_t *)(ring + (size_t)stage * C.stage_bytes +
                                    jb_off) + lane;
@@ -478,7 +558,9 @@ __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
             S, pos, (const uint32_t *)(st + ja_off) + lane,
             (const uint32_t *)(st + jb_off) + lane,
             (const F2 *)(st + kl_off) + lane,
-            (const float2 *)(st + ac_off) + lane, tab, wd & 0xFFFF, wd >> 16,
+            (const float4 *)(st + ac_off) + lane,
+            ((uint32_t)s << (a + 5)) | (uint32_t)lane, tab, wd & 0xFFFF,
+            wd >> 16,
             ea, eb, fl, me, T.sim_t, fx, fy, fz);
         finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
       }
