@@ -45,7 +45,7 @@ class SlStats(C.Structure):
                 ("step_path", C.c_int32), ("split_batch", C.c_int32)]
 
 STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
-              3: "k_split_step", 4: "k_split_tma"}
+              3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma"}
 
 
 _lib = None

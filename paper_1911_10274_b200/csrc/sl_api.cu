@@ -23,6 +23,7 @@
 #include "../../include/softlat_cuda.h"
 #include "sl_device.cuh"
 #include "sl_split.cuh"
+#include "sl_window.cuh"
 
 namespace sl {
 const Launch &launch_fp64();
@@ -102,6 +103,12 @@ struct sl_ctx {
   DevBuf sp_j, sp_kl, sp_s, sp_w, sp_ekl, degB, sp_meta;
   SplitCfg scfg;
   int split_warps = 0, split_grid = 0;
+  // tiled window kernel over the split layout (fp32, sl_window.cuh)
+  bool win_enabled = true;  // SL_DISABLE_WIN=1 keeps the split kernel
+  bool win = false;
+  WinCfg wcfg;
+  int win_grid = 0;
+  DevBuf win_rec, sp_a16, win_fail;
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -892,6 +899,70 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->split_warps = warps;
 }
 
+// Tile/window geometry of the fp32 split layout (sl_window.cuh); c->win stays
+// false when a tile does not fit (the split kernel then runs).
+int build_window_layout(sl_ctx *c) {
+  c->win = false;
+  if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP32 ||
+      c->agrp.n > 1 || c->n_slices == 0 || c->sp_wa > 64 || c->sp_wb > 64)
+    return SL_OK;
+  const int tt = WIN_T;
+  const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
+  WinCfg w{};
+  w.n_tiles = n_tiles;
+  w.tile_slices = tt;
+  w.ub = c->sp_wb <= 4 ? 4 : c->sp_wb <= 8 ? 8 : 13;
+  w.cap_a = (int)std::max<int64_t>(c->sp_wa, 1);
+  w.cap_b = (int)std::max<int64_t>(c->sp_wb, 1);
+  // slice block: A indices | A (k, L0) | B words; the guard-free batches
+  // may read up to UB rows past a section (discarded): keep them in bounds
+  const int ra = std::max(w.cap_a, w.ub), rb = std::max(w.cap_b, w.ub);
+  w.off_kl = (uint32_t)(ra * 64);
+  w.off_b = w.off_kl + (uint32_t)(ra * 32 * 8);
+  w.slice_bytes = (w.off_b + (uint32_t)(rb * 128) + 127) / 128 * 128;
+  const int64_t n_kl = (c->n_slices + 1) << (c->sp_a + 5);
+  CK(c->win_rec.ensure(128 * n_tiles));
+  CK(c->sp_a16.ensure(2 * n_kl));
+  CK(c->win_fail.ensure(16));
+  CK(cudaMemsetAsync(c->win_fail.p, 0, 16, c->st));
+  const int64_t m_pad = c->n_slices * 32;
+  k_win_build<<<(unsigned)n_tiles, 256, 0, c->st>>>(
+      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->n_slices, c->m_n,
+      c->sp_a, c->sp_rows, (uint32_t)m_pad,
+      (uint32_t)(c->n_slices << (c->sp_a + 5)), 0xFFFFu, tt,
+      c->win_rec.as<TileRec>(), c->sp_a16.as<uint16_t>(),
+      c->win_fail.as<unsigned long long>());
+  CKL();
+  unsigned long long res[2] = {0, 0};
+  CK(cudaMemcpyAsync(res, c->win_fail.p, 16, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->launches++;
+  if (res[0]) return SL_OK;
+  // stage: record | windows (sized to the widest tile) | TT slice blocks
+  w.cap_rec = (uint32_t)((res[1] + 7) / 8 * 8);
+  w.off_win = 128;
+  w.off_slice = (w.off_win + 16 * w.cap_rec + 127) / 128 * 128;
+  w.stage_bytes = w.off_slice + (uint32_t)tt * w.slice_bytes;
+  const int64_t bar = 8 * 2 * WIN_MAXST;
+  int nst = (int)std::min<int64_t>(
+      WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
+  if (const char *ev = getenv("SL_WIN_STAGES"))  // tuning override
+    nst = std::min(nst, atoi(ev));
+  if (nst < 2) return SL_OK;
+  w.nst = nst;
+  if (const char *ev = getenv("SL_WIN_DBG")) w.dbg_nocompute = atoi(ev);
+  w.rec = c->win_rec.as<TileRec>();
+  w.a16 = c->sp_a16.as<uint16_t>();
+  if (launchers(c->prec).win_setup(w) != 0) {
+    cudaGetLastError();
+    return SL_OK;
+  }
+  c->wcfg = w;
+  c->win_grid = (int)std::min<int64_t>(n_tiles, c->sm_count);
+  c->win = true;
+  return SL_OK;
+}
+
 // Device build of the split layout (sl_split.cuh).  *used = false when the
 // mesh does not fit its index encoding (the caller falls back to the exact
 // layout).
@@ -1028,6 +1099,7 @@ int build_split_layout(sl_ctx *c, bool *used) {
   c->max_width = 0;
   c->tma_warps = 0;
   configure_split_tma(c, widths);
+  if (int rc = build_window_layout(c)) return rc;
   c->layout_valid = true;
   c->layout_builds++;
   c->launches += 8;
@@ -1125,6 +1197,7 @@ int sl_create(int device, int precision, sl_ctx **out) {
   c->rsz = precision == PREC_FP32 ? 4 : 8;
   c->fsz = precision == PREC_FP64 ? 8 : 4;
   if (const char *ev = getenv("SL_DISABLE_TMA")) c->tma_enabled = ev[0] == '0';
+  if (const char *ev = getenv("SL_DISABLE_WIN")) c->win_enabled = ev[0] == '0';
   if (const char *ev = getenv("SL_DISABLE_SPLIT"))
     c->split_enabled = ev[0] == '0';
   memset(&c->env, 0, sizeof c->env);
@@ -1174,7 +1247,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
-                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto};
+                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->sp_a16, &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -1200,8 +1273,9 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
   o->precision = c->prec;
   o->device = c->device;
   o->step_path = !c->layout_valid ? SL_PATH_NONE
-                 : c->split       ? (c->split_warps ? SL_PATH_SPLIT_TMA
-                                                    : SL_PATH_SPLIT)
+                 : c->split       ? (c->win           ? SL_PATH_WINDOW_TMA
+                                     : c->split_warps ? SL_PATH_SPLIT_TMA
+                                                      : SL_PATH_SPLIT)
                  : (c->tma_warps ? SL_PATH_EXACT_TMA : SL_PATH_EXACT);
   o->split_batch = c->split && c->split_warps ? c->scfg.u : 0;
   const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc,
@@ -1628,7 +1702,9 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     T.write_acc = n == n_steps - 1;
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
-        if (c->split_warps)
+        if (c->win)
+          L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);
+        else if (c->split_warps)
           L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
           L.split(S, c->env, T, c->agrp, c->st);
@@ -1831,7 +1907,9 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
     T.write_acc = 1;
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
-        if (c->split_warps)
+        if (c->win)
+          L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);
+        else if (c->split_warps)
           L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
           L.split(S, c->env, T, c->agrp, c->st);

@@ -1112,6 +1112,10 @@ struct Launch {
                     const struct SplitCfg &, const struct ActP &, int grid,
                     cudaStream_t);
   int (*split_setup)(int smem_bytes, int u, int act);
+  // tiled window kernel (fp32 split layout, sl_window.cuh)
+  void (*win)(const KState &, const EnvP &, const StepP &,
+              const struct WinCfg &, int grid, cudaStream_t);
+  int (*win_setup)(const struct WinCfg &);
 };
 
 const Launch &launchers(int prec);

@@ -5,6 +5,7 @@
 #pragma once
 #include "sl_device.cuh"
 #include "sl_split.cuh"
+#include "sl_window.cuh"
 
 
 namespace sl {
@@ -50,6 +51,40 @@ struct SplitLaunch {
         else tma_u<8, false>(S, E, T, C, A, grid, st);
     }
   }
+  // tiled window kernel (fp32 only)
+  static void win(const KState &S, const EnvP &E, const StepP &T,
+                  const WinCfg &C, int grid, cudaStream_t st) {
+    if constexpr (P == PREC_FP32) {
+      const size_t sm = win_smem(C);
+      win_dispatch(C.ub, [&](auto kern) {
+        kern<<<grid, (WIN_T + 1) * 32, sm, st>>>(S, E, T, C);
+      });
+    }
+  }
+  static size_t win_smem(const WinCfg &C) {
+    return (size_t)C.nst * C.stage_bytes + 8 * 2 * WIN_MAXST;
+  }
+  // call f(kernel) for the instantiation of the B batch UB
+  template <class Fn>
+  static void win_dispatch(int ub, Fn f) {
+    if constexpr (P == PREC_FP32) {
+      switch (ub) {
+        case 4: f(k_win_tma<P, WIN_T, 4>); return;
+        case 8: f(k_win_tma<P, WIN_T, 8>); return;
+        default: f(k_win_tma<P, WIN_T, 13>); return;
+      }
+    }
+  }
+  static int win_setup(const WinCfg &C) {
+    int rc = 1;
+    if constexpr (P == PREC_FP32)
+      win_dispatch(C.ub, [&](auto kern) {
+        rc = (int)cudaFuncSetAttribute(
+            kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)win_smem(C));
+      });
+    return rc;
+  }
   template <int U, bool ACT>
   static int setup_u(int smem_bytes) {
     return (int)cudaFuncSetAttribute(
@@ -75,6 +110,9 @@ struct SplitLaunch<PREC_FP64> {
   static void tma(const KState &, const EnvP &, const StepP &,
                   const SplitCfg &, const ActP &, int, cudaStream_t) {}
   static int setup(int, int, int) { return 1; }
+  static void win(const KState &, const EnvP &, const StepP &,
+                  const WinCfg &, int, cudaStream_t) {}
+  static int win_setup(const WinCfg &) { return 1; }
 };
 }  // namespace sl
 
@@ -127,12 +165,20 @@ struct SplitLaunch<PREC_FP64> {
   int FN##_split_setup(int smem_bytes, int u, int act) {                     \
     return SplitLaunch<PREC>::setup(smem_bytes, u, act);                     \
   }                                                                          \
+  void FN##_win(const KState &S, const EnvP &E, const StepP &T,             \
+                const WinCfg &C, int grid, cudaStream_t st) {                \
+    SplitLaunch<PREC>::win(S, E, T, C, grid, st);                            \
+  }                                                                          \
+  int FN##_win_setup(const WinCfg &C) {                                      \
+    return SplitLaunch<PREC>::win_setup(C);                                  \
+  }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \
     static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
                              FN##_force, FN##_spring, FN##_mass,             \
                              FN##_split, FN##_split_force, FN##_split_tma,   \
-                             FN##_split_setup};                              \
+                             FN##_split_setup, FN##_win,                     \
+                             FN##_win_setup};                                \
     return L;                                                                \
   }                                                                          \
   }

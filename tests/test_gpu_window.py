@@ -1,0 +1,147 @@
+"""Tiled window kernel (csrc/sl_window.cuh, k_win_tma) -- the fp32
+production path for banded meshes -- against the split kernel it replaces
+(SL_DISABLE_WIN=1) and against the reference oracle, through the C ABI.
+
+The window kernel reads partner positions from shared-memory copies of each
+tile's index windows instead of gathering them from L2; the force
+arithmetic and the order of the per-mass sums are the split kernel's, so
+the two must agree to the last bit on the same inputs.  Connectivity
+(alive / zero-length flags, counters) must be bit-exact in every case.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from conftest import case_context, case_times, load_golden, rel_maxnorm
+
+pytestmark = pytest.mark.gpu
+
+PATH_SPLIT_TMA, PATH_WINDOW_TMA = 4, 5
+
+
+def _ctx(case, precision="fp32", win=True):
+    old = os.environ.get("SL_DISABLE_WIN")
+    os.environ["SL_DISABLE_WIN"] = "0" if win else "1"
+    try:
+        return case_context(case, precision)
+    finally:
+        if old is None:
+            del os.environ["SL_DISABLE_WIN"]
+        else:
+            os.environ["SL_DISABLE_WIN"] = old
+
+
+def _run(case, times, dt, win, precision="fp32", kill=None, kill_at=None):
+    ctx = _ctx(case, precision, win)
+    c = np.zeros(3, np.int64)
+    if kill is not None:
+        done, err = ctx.step(times[:kill_at], dt, 0, c)
+        assert err == 0
+        ctx.kill_springs(kill.astype(np.int64))
+        done, err = ctx.step(times[kill_at:], dt, 0, c)
+    else:
+        done, err = ctx.step(times, dt, 0, c)
+    st = ctx.stats()
+    m, s = len(case["m_mass"]), len(case["s_m1"])
+    pos, vel = np.zeros((m, 3)), np.zeros((m, 3))
+    ctx.download_masses(pos, vel)
+    alive = np.zeros(s, np.uint8)
+    degen = np.zeros(s, np.uint8)
+    ctx.download_springs(alive, degen)
+    ctx.close()
+    return dict(pos=pos, vel=vel, alive=alive, degen=degen, c=c, err=err,
+                path=st["step_path"])
+
+
+def _both(case, times, dt, **kw):
+    w = _run(case, times, dt, True, **kw)
+    s = _run(case, times, dt, False, **kw)
+    assert w["path"] == PATH_WINDOW_TMA, w["path"]
+    assert s["path"] == PATH_SPLIT_TMA, s["path"]
+    assert w["err"] == s["err"]
+    assert np.array_equal(w["alive"], s["alive"])
+    assert np.array_equal(w["degen"], s["degen"])
+    assert w["c"].tolist() == s["c"].tolist()
+    assert rel_maxnorm(w["pos"], s["pos"]) < 1e-6
+    assert rel_maxnorm(w["vel"], s["vel"]) < 1e-5
+    return w, s
+
+
+@pytest.mark.parametrize("name", ["cube10_drop", "cube10_contact",
+                                  "lat3_contact_drag", "constraints_contacts",
+                                  "topology_edits", "yield_break"])
+def test_window_matches_split_kernel(name):
+    g = load_golden(name)
+    n = min(100, int(g["n_steps"]))
+    _both(g, case_times(g)[:n], float(g["dt"]))
+
+
+def _lattice_case(nx, ny, nz, contact=True, robots=0):
+    """A builder lattice (or a stack of 5^3 robots) in the golden case
+    format: the reference bench recipe (cli.py:263-271), x1.01 stretch,
+    bottom layer on a friction ground plane."""
+    from paper_1911_10274_b200 import (ContactPlane, Environment, Material,
+                                       ObjectStore, Vec3, engine)
+    from paper_1911_10274_b200.builder import LatticeSpec, build_lattice
+    st = ObjectStore()
+    if robots:
+        for r in range(robots):
+            build_lattice(LatticeSpec(Vec3(0, 0.3 * r, 0), 5, 5, 5, 0.05,
+                                      Material(1e6, 1000.0)), st)
+    else:
+        build_lattice(LatticeSpec(Vec3(0, 0, 0), nx, ny, nz, 0.05,
+                                  Material(1e5, 1000.0)), st)
+    m, s = st.mass_slot_count, st.spring_slot_count
+    st._m_pos[:m] *= 1.01
+    env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
+        normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
+        static_friction=1.0, kinetic_friction=0.8)] if contact else [])
+    case = {k: getattr(st, "_" + k)[:m].copy() for k in
+            ("m_pos", "m_vel", "m_acc", "m_fext", "m_load", "m_mass",
+             "m_fixed", "m_alive", "m_gen")}
+    for k in ("s_m1", "s_m2", "s_m1gen", "s_m2gen", "s_rest", "s_k",
+              "s_diam", "s_yield", "s_alive", "s_degen"):
+        case[k] = getattr(st, "_" + k)[:s].copy()
+    for k in ("mode", "amp", "freq", "off", "per"):
+        case["s_" + k] = getattr(st, "_s_act_" + k)[:s].copy()
+    planes, balls = engine.flatten_contacts(env)
+    case.update(gravity=env.gravity.as_array(), drag=0.0, planes=planes,
+                balls=balls, gc_kind=np.zeros(0, np.int8),
+                gc_vec=np.zeros((0, 3)), lc_off=np.zeros(m + 1, np.int64),
+                lc_kind=np.zeros(0, np.int8), lc_vec=np.zeros((0, 3)))
+    return case
+
+
+@pytest.mark.parametrize("shape", [(17, 9, 13), (30, 30, 30), (12, 40, 7)])
+def test_window_lattices_match_split_and_oracle(shape):
+    case = _lattice_case(*shape)
+    dt, n = 1e-4, 60
+    times = np.arange(n, dtype=np.float64) * dt
+    w, _ = _both(case, times, dt)
+    ref = orc.OracleSim(case, nthreads=orc.max_threads())
+    for k in range(n):
+        ref.step(float(times[k]), dt)
+    assert rel_maxnorm(w["pos"], ref.c["m_pos"]) < 1e-4
+    assert rel_maxnorm(w["vel"], ref.c["m_vel"]) < 1e-3
+    assert np.array_equal(w["alive"], ref.c["s_alive"])
+
+
+def test_window_robot_stack_and_kills():
+    """Stacked 5^3 robots (config D layout, unactuated) with springs killed
+    at a pause point: dead A entries must add exactly nothing."""
+    case = _lattice_case(0, 0, 0, robots=9)
+    dt, n = 1e-4, 80
+    times = np.arange(n, dtype=np.float64) * dt
+    rng = np.random.default_rng(1)
+    kill = np.sort(rng.choice(len(case["s_m1"]), 500, replace=False))
+    w, _ = _both(case, times, dt, kill=kill, kill_at=30)
+    ref = orc.OracleSim(case)
+    for k in range(30):
+        ref.step(float(times[k]), dt)
+    ref.c["s_alive"][kill] = 0
+    for k in range(30, n):
+        ref.step(float(times[k]), dt)
+    assert np.array_equal(w["alive"], ref.c["s_alive"])
+    assert rel_maxnorm(w["pos"], ref.c["m_pos"]) < 1e-4
