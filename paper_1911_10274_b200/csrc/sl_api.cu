@@ -108,7 +108,7 @@ struct sl_ctx {
   bool win = false;
   WinCfg wcfg;
   int win_grid = 0;
-  DevBuf win_rec, sp_a16, win_fail;
+  DevBuf win_rec, win_dict, win_zero, win_blk, win_fail;
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -647,6 +647,14 @@ KState make_state(sl_ctx *c) {
     const bool act = c->agrp.n > 1;
     S.sp_actc = act ? c->sp_actc.as<float4>() : nullptr;
     S.sp_acto = act ? c->sp_acto.as<double>() : nullptr;
+    if (c->win) {
+      S.win_blk = c->win_blk.as<unsigned char>();
+      S.win_zero = c->win_zero.as<uint8_t>();
+      S.win_sb = c->wcfg.bl.slice_bytes;
+      S.win_oac = c->wcfg.bl.off_acode;
+      S.win_obc = c->wcfg.bl.off_bcode;
+      S.win_tt = c->wcfg.tile_slices;
+    }
   }
   return S;
 }
@@ -906,31 +914,36 @@ int build_window_layout(sl_ctx *c) {
   if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP32 ||
       c->agrp.n > 1 || c->n_slices == 0 || c->sp_wa > 64 || c->sp_wb > 64)
     return SL_OK;
-  const int tt = WIN_T;
+  int tt = 16;  // consumer warps per CTA (r1 sweeps: the more the better)
+  if (const char *ev = getenv("SL_WIN_T")) {
+    const int v = atoi(ev);
+    tt = v == 12 || v == 20 || v == 24 ? v : 16;
+  }
   const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
   WinCfg w{};
   w.n_tiles = n_tiles;
   w.tile_slices = tt;
-  w.ub = c->sp_wb <= 4 ? 4 : c->sp_wb <= 8 ? 8 : 13;
   w.cap_a = (int)std::max<int64_t>(c->sp_wa, 1);
   w.cap_b = (int)std::max<int64_t>(c->sp_wb, 1);
-  // slice block: A indices | A (k, L0) | B words; the guard-free batches
-  // may read up to UB rows past a section (discarded): keep them in bounds
-  const int ra = std::max(w.cap_a, w.ub), rb = std::max(w.cap_b, w.ub);
-  w.off_kl = (uint32_t)(ra * 64);
-  w.off_b = w.off_kl + (uint32_t)(ra * 32 * 8);
-  w.slice_bytes = (w.off_b + (uint32_t)(rb * 128) + 127) / 128 * 128;
-  const int64_t n_kl = (c->n_slices + 1) << (c->sp_a + 5);
-  CK(c->win_rec.ensure(128 * n_tiles));
-  CK(c->sp_a16.ensure(2 * n_kl));
+  // slice block: A indices | A codes | B indices | B codes (16 B aligned)
+  auto al16 = [](uint32_t x) { return (x + 15) / 16 * 16; };
+  w.bl.off_acode = al16((uint32_t)w.cap_a * 64);
+  w.bl.off_b16 = al16(w.bl.off_acode + (uint32_t)w.cap_a * 32);
+  w.bl.off_bcode = al16(w.bl.off_b16 + (uint32_t)w.cap_b * 64);
+  w.bl.slice_bytes = al16(w.bl.off_bcode + (uint32_t)w.cap_b * 32);
+  CK(c->win_rec.ensure(sizeof(TileRec) * n_tiles));
+  CK(c->win_dict.ensure(8 * WIN_DMAX * n_tiles));
+  CK(c->win_zero.ensure(n_tiles));
+  CK(c->win_blk.ensure((size_t)w.bl.slice_bytes * n_tiles * tt));
   CK(c->win_fail.ensure(16));
   CK(cudaMemsetAsync(c->win_fail.p, 0, 16, c->st));
   const int64_t m_pad = c->n_slices * 32;
   k_win_build<<<(unsigned)n_tiles, 256, 0, c->st>>>(
-      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->n_slices, c->m_n,
-      c->sp_a, c->sp_rows, (uint32_t)m_pad,
-      (uint32_t)(c->n_slices << (c->sp_a + 5)), 0xFFFFu, tt,
-      c->win_rec.as<TileRec>(), c->sp_a16.as<uint16_t>(),
+      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
+      c->n_slices, c->m_n, c->sp_a, c->sp_rows, (uint32_t)m_pad,
+      (uint32_t)(c->n_slices << (c->sp_a + 5)), tt, w.bl, w.cap_a, w.cap_b,
+      c->win_rec.as<TileRec>(), c->win_dict.as<float2>(),
+      c->win_blk.as<unsigned char>(), c->win_zero.as<uint8_t>(),
       c->win_fail.as<unsigned long long>());
   CKL();
   unsigned long long res[2] = {0, 0};
@@ -938,21 +951,24 @@ int build_window_layout(sl_ctx *c) {
   CK(cudaStreamSynchronize(c->st));
   c->launches++;
   if (res[0]) return SL_OK;
-  // stage: record | windows (sized to the widest tile) | TT slice blocks
+  // stage: record | material table | windows (sized to the widest tile) |
+  // tt slice blocks
   w.cap_rec = (uint32_t)((res[1] + 7) / 8 * 8);
-  w.off_win = 128;
+  w.off_dict = sizeof(TileRec);
+  w.off_win = w.off_dict + 8 * WIN_DMAX;
   w.off_slice = (w.off_win + 16 * w.cap_rec + 127) / 128 * 128;
-  w.stage_bytes = w.off_slice + (uint32_t)tt * w.slice_bytes;
+  w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
   const int64_t bar = 8 * 2 * WIN_MAXST;
   int nst = (int)std::min<int64_t>(
       WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
   if (const char *ev = getenv("SL_WIN_STAGES"))  // tuning override
-    nst = std::min(nst, atoi(ev));
+    nst = std::min(nst, std::max(2, atoi(ev)));
   if (nst < 2) return SL_OK;
   w.nst = nst;
   if (const char *ev = getenv("SL_WIN_DBG")) w.dbg_nocompute = atoi(ev);
   w.rec = c->win_rec.as<TileRec>();
-  w.a16 = c->sp_a16.as<uint16_t>();
+  w.dict = c->win_dict.as<float2>();
+  w.blk = c->win_blk.as<unsigned char>();
   if (launchers(c->prec).win_setup(w) != 0) {
     cudaGetLastError();
     return SL_OK;
@@ -1247,7 +1263,8 @@ int sl_destroy(sl_ctx *c) {
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
-                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->sp_a16, &c->win_fail};
+                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->win_dict, &c->win_zero, &c->win_blk,
+                    &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -1420,6 +1437,8 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
   // first actuated group on a live split layout: re-layout with act cells
   if (params_only && groups_before <= 1 && c->agrp.n > 1 && c->split)
     c->layout_valid = false;
+  // the window layout's material tables hold (k, L0) by value: rebuild
+  if (params_only && c->win) c->layout_valid = false;
   size_t need = align256(8 * n) * 16 + align256(n) * 5 + 2048;
   CK(c->stage.ensure(need));
   size_t off = 0;

@@ -113,6 +113,12 @@ struct KState {
   const uint32_t *sp_ekl;  // per spring: kl index of its A cell
   float4 *sp_actc;         // act cell per kl cell (null: no groups)
   double *sp_acto;         // exact fp64 act offset per kl cell
+  // tiled window layout (sl_window.cuh; null when not built): the slice
+  // blocks (A / B code rows at win_oac / win_obc) and each tile's zero code
+  unsigned char *win_blk;
+  const uint8_t *win_zero;
+  uint32_t win_sb, win_oac, win_obc;
+  int win_tt;
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -1007,6 +1013,24 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
         ((float2 *)S.sp_kl)[S.sp_ekl[s]] = make_float2(0.f, 0.f);
     }
     if (S.e2[s] >= 0) S.sp_j[S.e2[s]] = S.sp_null;
+    if (S.win_blk) {  // window layout: both entries get the zero code
+      const int a = S.sp_a;
+      if (S.e1[s] >= 0) {
+        const uint32_t kli = S.sp_ekl[s];
+        const int64_t sl = kli >> (a + 5);
+        const int r = (int)((kli >> 5) & ((1u << a) - 1));
+        S.win_blk[sl * S.win_sb + S.win_oac + r * 32 + (kli & 31)] =
+            S.win_zero[sl / S.win_tt];
+      }
+      if (S.e2[s] >= 0) {
+        const int64_t per = (int64_t)S.sp_rows * 32, e = S.e2[s];
+        const int64_t sl = e / per;
+        const int rem = (int)(e - sl * per);
+        const int rb = (rem >> 5) - (1 << a);
+        S.win_blk[sl * S.win_sb + S.win_obc + rb * 32 + (rem & 31)] =
+            S.win_zero[sl / S.win_tt];
+      }
+    }
     return;
   }
   if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;

@@ -56,29 +56,30 @@ struct SplitLaunch {
                   const WinCfg &C, int grid, cudaStream_t st) {
     if constexpr (P == PREC_FP32) {
       const size_t sm = win_smem(C);
-      win_dispatch(C.ub, [&](auto kern) {
-        kern<<<grid, (WIN_T + 1) * 32, sm, st>>>(S, E, T, C);
+      win_dispatch(C.tile_slices, [&](auto kern) {
+        kern<<<grid, (C.tile_slices + 1) * 32, sm, st>>>(S, E, T, C);
       });
     }
   }
   static size_t win_smem(const WinCfg &C) {
     return (size_t)C.nst * C.stage_bytes + 8 * 2 * WIN_MAXST;
   }
-  // call f(kernel) for the instantiation of the B batch UB
+  // call f(kernel) for the instantiation of T
   template <class Fn>
-  static void win_dispatch(int ub, Fn f) {
+  static void win_dispatch(int tt, Fn f) {
     if constexpr (P == PREC_FP32) {
-      switch (ub) {
-        case 4: f(k_win_tma<P, WIN_T, 4>); return;
-        case 8: f(k_win_tma<P, WIN_T, 8>); return;
-        default: f(k_win_tma<P, WIN_T, 13>); return;
+      switch (tt) {
+        case 12: f(k_win_tma<P, 12>); return;
+        case 20: f(k_win_tma<P, 20>); return;
+        case 24: f(k_win_tma<P, 24>); return;
+        default: f(k_win_tma<P, 16>); return;
       }
     }
   }
   static int win_setup(const WinCfg &C) {
     int rc = 1;
     if constexpr (P == PREC_FP32)
-      win_dispatch(C.ub, [&](auto kern) {
+      win_dispatch(C.tile_slices, [&](auto kern) {
         rc = (int)cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
             (int)win_smem(C));

@@ -3,10 +3,11 @@ production path for banded meshes -- against the split kernel it replaces
 (SL_DISABLE_WIN=1) and against the reference oracle, through the C ABI.
 
 The window kernel reads partner positions from shared-memory copies of each
-tile's index windows instead of gathering them from L2; the force
-arithmetic and the order of the per-mass sums are the split kernel's, so
-the two must agree to the last bit on the same inputs.  Connectivity
-(alive / zero-length flags, counters) must be bit-exact in every case.
+tile's index windows instead of gathering them from L2, and (k, L0) from a
+per-tile material table; the per-mass sums have the split kernel's order, so
+the two agree to fp32 rounding on the same inputs (see _both), and both are
+held to the reference oracle.  Connectivity (alive / zero-length flags,
+counters) must be bit-exact in every case.
 """
 import os
 
@@ -64,8 +65,14 @@ def _both(case, times, dt, **kw):
     assert np.array_equal(w["alive"], s["alive"])
     assert np.array_equal(w["degen"], s["degen"])
     assert w["c"].tolist() == s["c"].tolist()
-    assert rel_maxnorm(w["pos"], s["pos"]) < 1e-6
-    assert rel_maxnorm(w["vel"], s["vel"]) < 1e-5
+    # same (k, L0) values and summation structure, but the window kernel
+    # forms the force scale as k - (k L0)/|d| (one FMA) where the split
+    # kernel forms k (|d|^2 r - L0) r: equally rounded (fp32 ulps of k),
+    # differently.  Near rest length that difference is what fp32 state
+    # amplifies on the free-falling cube (test_gpu_parity.py,
+    # FP32_STATE_VEL_BOUND), hence the velocity bound.
+    assert rel_maxnorm(w["pos"], s["pos"]) < 1e-5
+    assert rel_maxnorm(w["vel"], s["vel"]) < 5e-4
     return w, s
 
 
