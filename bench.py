@@ -372,6 +372,13 @@ def main():
             "peak_kind": peak_kind, "algorithmic_bytes_per_step": algo,
             "bytes_per_spring_update": algo / springs,
             "kernel": kernel}
+    if traffic:
+        # DRAM bytes the kernel really moves (committed ncu capture) at the
+        # measured step time: below `achieved` when the layout compresses
+        # the algorithmic stream (window kernel: material table, 16-bit
+        # window indices)
+        roof["traffic_gbs"] = traffic / (sec / args.steps) / 1e9
+        roof["traffic_frac"] = roof["traffic_gbs"] / peak
 
     # e2e through the public API, host store authoritative at both ends
     e2e = None
