@@ -108,7 +108,7 @@ struct sl_ctx {
   bool win = false;
   WinCfg wcfg;
   int win_grid = 0;
-  DevBuf win_rec, win_dict, win_zero, win_blk, win_fail;
+  DevBuf win_rec, win_dict, win_actb, win_zero, win_blk, win_fail;
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -912,7 +912,7 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
 int build_window_layout(sl_ctx *c) {
   c->win = false;
   if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP32 ||
-      c->agrp.n > 1 || c->n_slices == 0 || c->sp_wa > 64 || c->sp_wb > 64)
+      c->n_slices == 0 || c->sp_wa > 64 || c->sp_wb > 64)
     return SL_OK;
   int tt = 16;  // consumer warps per CTA (r1 sweeps: the more the better)
   if (const char *ev = getenv("SL_WIN_T")) {
@@ -933,6 +933,7 @@ int build_window_layout(sl_ctx *c) {
   w.bl.slice_bytes = al16(w.bl.off_bcode + (uint32_t)w.cap_b * 32);
   CK(c->win_rec.ensure(sizeof(TileRec) * n_tiles));
   CK(c->win_dict.ensure(8 * WIN_DMAX * n_tiles));
+  CK(c->win_actb.ensure((size_t)WIN_ACTB * n_tiles));
   CK(c->win_zero.ensure(n_tiles));
   CK(c->win_blk.ensure((size_t)w.bl.slice_bytes * n_tiles * tt));
   CK(c->win_fail.ensure(16));
@@ -942,8 +943,10 @@ int build_window_layout(sl_ctx *c) {
       c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
       c->n_slices, c->m_n, c->sp_a, c->sp_rows, (uint32_t)m_pad,
       (uint32_t)(c->n_slices << (c->sp_a + 5)), tt, w.bl, w.cap_a, w.cap_b,
-      c->win_rec.as<TileRec>(), c->win_dict.as<float2>(),
-      c->win_blk.as<unsigned char>(), c->win_zero.as<uint8_t>(),
+      c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
+      c->s_grp.as<uint8_t>(), c->win_rec.as<TileRec>(),
+      c->win_dict.as<float2>(), c->win_actb.as<unsigned char>(),
+      c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
       c->win_fail.as<unsigned long long>());
   CKL();
   unsigned long long res[2] = {0, 0};
@@ -955,19 +958,22 @@ int build_window_layout(sl_ctx *c) {
   // tt slice blocks
   w.cap_rec = (uint32_t)((res[1] + 7) / 8 * 8);
   w.off_dict = sizeof(TileRec);
-  w.off_win = w.off_dict + 8 * WIN_DMAX;
+  w.off_act = w.off_dict + 8 * WIN_DMAX;
+  w.off_win = w.off_act + WIN_ACTB;
   w.off_slice = (w.off_win + 16 * w.cap_rec + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
-  const int64_t bar = 8 * 2 * WIN_MAXST;
+  const int64_t bar = 8 * 2 * WIN_MAXST + 8 * WIN_MAXST * WIN_DMAX;
   int nst = (int)std::min<int64_t>(
       WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
   if (const char *ev = getenv("SL_WIN_STAGES"))  // tuning override
     nst = std::min(nst, std::max(2, atoi(ev)));
   if (nst < 2) return SL_OK;
   w.nst = nst;
+  w.off_eff = (uint32_t)nst * w.stage_bytes;
   if (const char *ev = getenv("SL_WIN_DBG")) w.dbg_nocompute = atoi(ev);
   w.rec = c->win_rec.as<TileRec>();
   w.dict = c->win_dict.as<float2>();
+  w.actb = c->win_actb.as<unsigned char>();
   w.blk = c->win_blk.as<unsigned char>();
   if (launchers(c->prec).win_setup(w) != 0) {
     cudaGetLastError();
@@ -1263,7 +1269,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->vals[1], &c->deg, &c->width, &c->start, &c->status,
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
-                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->win_dict, &c->win_zero, &c->win_blk,
+                    &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->win_dict, &c->win_actb, &c->win_zero, &c->win_blk,
                     &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);

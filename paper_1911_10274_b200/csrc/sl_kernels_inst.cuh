@@ -62,7 +62,7 @@ struct SplitLaunch {
     }
   }
   static size_t win_smem(const WinCfg &C) {
-    return (size_t)C.nst * C.stage_bytes + 8 * 2 * WIN_MAXST;
+    return (size_t)C.off_eff + WIN_MAXST * WIN_DMAX * 8 + 8 * 2 * WIN_MAXST;
   }
   // call f(kernel) for the instantiation of T
   template <class Fn>

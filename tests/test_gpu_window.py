@@ -78,14 +78,15 @@ def _both(case, times, dt, **kw):
 
 @pytest.mark.parametrize("name", ["cube10_drop", "cube10_contact",
                                   "lat3_contact_drag", "constraints_contacts",
-                                  "topology_edits", "yield_break"])
+                                  "topology_edits", "yield_break", "worm",
+                                  "actuated_quiescent"])
 def test_window_matches_split_kernel(name):
     g = load_golden(name)
     n = min(100, int(g["n_steps"]))
     _both(g, case_times(g)[:n], float(g["dt"]))
 
 
-def _lattice_case(nx, ny, nz, contact=True, robots=0):
+def _lattice_case(nx, ny, nz, contact=True, robots=0, worm=False):
     """A builder lattice (or a stack of 5^3 robots) in the golden case
     format: the reference bench recipe (cli.py:263-271), x1.01 stretch,
     bottom layer on a friction ground plane."""
@@ -94,9 +95,12 @@ def _lattice_case(nx, ny, nz, contact=True, robots=0):
     from paper_1911_10274_b200.builder import LatticeSpec, build_lattice
     st = ObjectStore()
     if robots:
+        from paper_1911_10274_b200.actuation import configure_worm
         for r in range(robots):
-            build_lattice(LatticeSpec(Vec3(0, 0.3 * r, 0), 5, 5, 5, 0.05,
-                                      Material(1e6, 1000.0)), st)
+            body = build_lattice(LatticeSpec(Vec3(0, 0.3 * r, 0), 5, 5, 5,
+                                             0.05, Material(1e6, 1000.0)), st)
+            if worm:
+                configure_worm(body, st)
     else:
         build_lattice(LatticeSpec(Vec3(0, 0, 0), nx, ny, nz, 0.05,
                                   Material(1e5, 1000.0)), st)
@@ -152,3 +156,20 @@ def test_window_robot_stack_and_kills():
         ref.step(float(times[k]), dt)
     assert np.array_equal(w["alive"], ref.c["s_alive"])
     assert rel_maxnorm(w["pos"], ref.c["m_pos"]) < 1e-4
+
+
+def test_window_actuated_robot_swarm():
+    """Config D shape: worm-actuated 5^3 robots.  The window kernel's
+    per-tile actuation table (factor computed once per material per step in
+    fp64, kernels.py:55-62) against the split kernel and the oracle over a
+    100-step horizon."""
+    case = _lattice_case(0, 0, 0, robots=12, worm=True)
+    assert (case["s_mode"] == 1).any()
+    dt, n = 1e-4, 100
+    times = np.arange(n, dtype=np.float64) * dt
+    w, _ = _both(case, times, dt)
+    ref = orc.OracleSim(case)
+    for k in range(n):
+        ref.step(float(times[k]), dt)
+    assert rel_maxnorm(w["pos"], ref.c["m_pos"]) < 1e-4
+    assert rel_maxnorm(w["vel"], ref.c["m_vel"]) < 1e-3
