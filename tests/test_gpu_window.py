@@ -173,3 +173,45 @@ def test_window_actuated_robot_swarm():
         ref.step(float(times[k]), dt)
     assert rel_maxnorm(w["pos"], ref.c["m_pos"]) < 1e-4
     assert rel_maxnorm(w["vel"], ref.c["m_vel"]) < 1e-3
+
+
+def test_window_param_edits_match_oracle():
+    """sl_write_spring_params at a pause (stiffness / rest length changes,
+    sine actuation switched on): the window layout's material and actuation
+    tables hold values, so the edit must rebuild them -- the trajectory
+    equals the oracle's with the same edits."""
+    case = _lattice_case(14, 9, 11)
+    dt = 1e-4
+    times = np.arange(80, dtype=np.float64) * dt
+    rng = np.random.default_rng(2)
+    sl = np.sort(rng.choice(len(case["s_m1"]), 400, replace=False))
+    rest = case["s_rest"][sl] * 0.98
+    k = case["s_k"][sl] * 1.5
+    mode = np.where(np.arange(len(sl)) % 2 == 0, 1, 0).astype(np.int8)
+    amp = np.full(len(sl), 0.1)
+    freq = np.full(len(sl), 30.0)
+    off = np.zeros(len(sl))
+    per = np.full(len(sl), 0.5)
+    ctx = _ctx(case)
+    c = np.zeros(3, np.int64)
+    assert ctx.step(times[:30], dt, 0, c)[1] == 0
+    assert ctx.stats()["step_path"] == PATH_WINDOW_TMA
+    ctx.write_spring_params(sl, rest, k, case["s_diam"][sl],
+                            case["s_yield"][sl], mode, amp, freq, off, per)
+    assert ctx.step(times[30:], dt, 0, c)[1] == 0
+    assert ctx.stats()["step_path"] == PATH_WINDOW_TMA
+    m = len(case["m_mass"])
+    pos, vel = np.zeros((m, 3)), np.zeros((m, 3))
+    ctx.download_masses(pos, vel)
+    ctx.close()
+    ref = orc.OracleSim(case)
+    for n in range(30):
+        ref.step(float(times[n]), dt)
+    for key, val in (("s_rest", rest), ("s_k", k), ("s_mode", mode),
+                     ("s_amp", amp), ("s_freq", freq), ("s_off", off),
+                     ("s_per", per)):
+        ref.c[key][sl] = val
+    for n in range(30, 80):
+        ref.step(float(times[n]), dt)
+    assert rel_maxnorm(pos, ref.c["m_pos"]) < 1e-4
+    assert rel_maxnorm(vel, ref.c["m_vel"]) < 1e-3
