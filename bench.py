@@ -259,12 +259,27 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        # one rank per GPU on the box; ranks beyond the device count (logic
+        # tests with BENCH_DIST_BACKEND=gloo on one GPU) share devices
+        from paper_1911_10274_b200 import _native
+        local %= max(1, _native.device_count())
     dist = None
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # nccl on the box (one rank per GPU); gloo lets the rank logic be
+        # exercised with several ranks on one device
+        dist.init_process_group(backend)
+
+    def reduce_(x, op, dtype):
+        import torch
+        dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+        t = torch.tensor([x], device=dev, dtype=dtype)
+        dist.all_reduce(t, op=op)
+        return t.item()
 
     metric = "spring updates/sec"
     unit = "spring_updates/s"
@@ -277,7 +292,8 @@ def main():
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle
         oracle.build()
-        threads = oracle.max_threads()
+        # all host threads (torchrun sets OMP_NUM_THREADS=1 per rank)
+        threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
         steps, wall = time_oracle(st, env, max(1, args.steps),
                                   max(1, min(args.warmup, 2)), threads)
         v = st.spring_count * steps / wall
@@ -345,16 +361,12 @@ def main():
     sec = ms / 1e3
     if dist is not None:
         import torch
-        t = torch.tensor([sec], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t.item())
+        sec = float(reduce_(sec, dist.ReduceOp.MAX, torch.float64))
         dist.barrier()
     total_springs = springs * world
     if dist is not None and args.config != "B":
         import torch
-        t = torch.tensor([springs], device=f"cuda:{local}", dtype=torch.int64)
-        dist.all_reduce(t)
-        total_springs = int(t.item())
+        total_springs = int(reduce_(springs, dist.ReduceOp.SUM, torch.int64))
     value = total_springs * args.steps / sec
     ms_per_step = 1e3 * sec / args.steps
 
@@ -397,10 +409,7 @@ def main():
         assert rep.step_count == k, rep
         if dist is not None:
             import torch
-            t = torch.tensor([wall], device=f"cuda:{local}",
-                             dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
+            wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
         h2d = m * (5 * 24 + 8 + 1 + 1 + 8) + 16 * (m + 1)
         d2h = m * 4 * 24
         e2e = {"value": world * springs * k / wall, "unit": unit,
@@ -415,7 +424,7 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
             import oracle
             oracle.build()
-            thr = oracle.max_threads()
+            thr = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
             st2, env2, _, _, _ = make_workload(args, 0, 1)
             n_s, wall = time_oracle(st2, env2, 3, 1, thr, budget_s=30.0)
             cpu = {"value": st2.spring_count * n_s / wall, "unit": unit,
