@@ -69,6 +69,10 @@ typedef struct sl_stats {
   int32_t device;
   int32_t step_path;   /* fused gather kernel in use: SL_PATH_*             */
   int32_t split_batch; /* gather batch U of the split TMA kernel (0 = n/a) */
+  int64_t fused_groups;   /* body groups of the multi-step fused kernel
+                             (0: the context runs per-step kernels only)  */
+  int64_t fused_launches; /* multi-step fused launches so far             */
+  int64_t fused_aborts;   /* of which re-run through per-step kernels     */
 } sl_stats;
 
 /* sl_stats.step_path */

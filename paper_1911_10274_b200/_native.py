@@ -42,7 +42,9 @@ class SlStats(C.Structure):
                 ("slices", C.c_int64), ("layout_builds", C.c_int64),
                 ("device_bytes", C.c_int64), ("kernel_launches", C.c_int64),
                 ("precision", C.c_int32), ("device", C.c_int32),
-                ("step_path", C.c_int32), ("split_batch", C.c_int32)]
+                ("step_path", C.c_int32), ("split_batch", C.c_int32),
+                ("fused_groups", C.c_int64), ("fused_launches", C.c_int64),
+                ("fused_aborts", C.c_int64)]
 
 STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
               3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma"}

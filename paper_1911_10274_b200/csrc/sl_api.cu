@@ -24,6 +24,7 @@
 #include "sl_device.cuh"
 #include "sl_split.cuh"
 #include "sl_window.cuh"
+#include "sl_fused.cuh"
 
 namespace sl {
 const Launch &launch_fp64();
@@ -109,6 +110,14 @@ struct sl_ctx {
   WinCfg wcfg;
   int win_grid = 0;
   DevBuf win_rec, win_dict, win_actb, win_zero, win_blk, win_fail;
+  // multi-step fused small-body kernel (fp32, sl_fused.cuh)
+  bool fz_enabled = true;  // SL_DISABLE_FUSED=1 keeps per-step kernels
+  bool fz_ok = false;
+  FzCfg fcfg;
+  size_t fz_smem = 0;
+  int64_t fz_launches = 0, fz_aborts = 0;
+  DevBuf fz_gstart, fz_gcount, fz_ent, fz_code, fz_dict, fz_actb, fz_has,
+      fz_zero, fz_gid, fz_fail, fz_times, fz_diff, vel2;
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -647,6 +656,14 @@ KState make_state(sl_ctx *c) {
     const bool act = c->agrp.n > 1;
     S.sp_actc = act ? c->sp_actc.as<float4>() : nullptr;
     S.sp_acto = act ? c->sp_acto.as<double>() : nullptr;
+    if (c->fz_ok) {
+      S.fz_code = c->fz_code.as<uint8_t>();
+      S.fz_gid = c->fz_gid.as<int32_t>();
+      S.fz_gstart = c->fz_gstart.as<int32_t>();
+      S.fz_zero = c->fz_zero.as<uint8_t>();
+      S.fz_rows = c->fcfg.ra + c->fcfg.rb;
+      S.fz_ra = c->fcfg.ra;
+    }
     if (c->win) {
       S.win_blk = c->win_blk.as<unsigned char>();
       S.win_zero = c->win_zero.as<uint8_t>();
@@ -985,6 +1002,142 @@ int build_window_layout(sl_ctx *c) {
   return SL_OK;
 }
 
+// Groups of whole connected components for the multi-step fused kernel
+// (sl_fused.cuh); c->fz_ok stays false when the context is not eligible.
+int build_fused_groups(sl_ctx *c) {
+  c->fz_ok = false;
+  const int64_t m_n = c->m_n, s_n = c->s_n;
+  if (!c->fz_enabled || c->prec != PREC_FP32 || !c->split || c->has_ghost ||
+      m_n == 0 || c->sp_wa + c->sp_wb > FZ_MAXR)
+    return SL_OK;
+  // component boundaries: no alive spring spans (b - 1, b)
+  CK(c->fz_diff.ensure(4 * (m_n + 1)));
+  CK(cudaMemsetAsync(c->fz_diff.p, 0, 4 * (m_n + 1), c->st));
+  if (s_n > 0) {
+    k_fused_cover<<<blocks_for(s_n), 256, 0, c->st>>>(
+        s_n, c->ends.as<int2>(), c->fz_diff.as<int32_t>());
+    CKL();
+  }
+  std::vector<int32_t> diff(m_n + 1);
+  CK(cudaMemcpyAsync(diff.data(), c->fz_diff.p, 4 * (m_n + 1),
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  // pack consecutive components into groups of <= FZ_MAXM masses
+  std::vector<int32_t> gs, gc;
+  int64_t cover = 0, comp0 = 0, g0 = 0;
+  for (int64_t b = 1; b <= m_n; b++) {
+    cover += diff[b];
+    if (b < m_n && cover != 0) continue;  // (b - 1, b) is spanned
+    const int64_t len = b - comp0;        // component [comp0, b)
+    if (len > FZ_MAXM) return SL_OK;      // a body too large for a CTA
+    if (b - g0 > FZ_MAXM) {               // close the group before comp0
+      gs.push_back((int32_t)g0);
+      gc.push_back((int32_t)(comp0 - g0));
+      g0 = comp0;
+    }
+    comp0 = b;
+  }
+  gs.push_back((int32_t)g0);
+  gc.push_back((int32_t)(m_n - g0));
+  const int64_t ng = (int64_t)gs.size();
+  const int ra = (int)c->sp_wa, rb = (int)c->sp_wb;
+  const int rows = std::max(1, ra + rb);
+  CK(c->fz_gstart.ensure(4 * ng));
+  CK(c->fz_gcount.ensure(4 * ng));
+  CK(c->fz_ent.ensure((size_t)2 * ng * rows * FZ_MAXM));
+  CK(c->fz_code.ensure((size_t)ng * rows * FZ_MAXM));
+  CK(c->fz_dict.ensure((size_t)8 * WIN_DMAX * ng));
+  CK(c->fz_actb.ensure((size_t)WIN_ACTB * ng));
+  CK(c->fz_has.ensure(ng));
+  CK(c->fz_zero.ensure(ng));
+  CK(c->fz_gid.ensure(4 * m_n));
+  CK(c->fz_fail.ensure(8));
+  CK(cudaMemcpyAsync(c->fz_gstart.p, gs.data(), 4 * ng,
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->fz_gcount.p, gc.data(), 4 * ng,
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->fz_fail.p, 0, 8, c->st));
+  const int64_t m_pad = c->n_slices * 32;
+  k_fused_build<<<(unsigned)ng, FZ_MAXM, 0, c->st>>>(
+      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
+      c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
+      c->s_grp.as<uint8_t>(), c->vel.as<float4>(), c->sp_a, c->sp_rows,
+      (uint32_t)m_pad, (uint32_t)(c->n_slices << (c->sp_a + 5)),
+      c->fz_gstart.as<int32_t>(), c->fz_gcount.as<int32_t>(), ra, rb,
+      c->fz_ent.as<uint16_t>(), c->fz_code.as<uint8_t>(),
+      c->fz_dict.as<float2>(), c->fz_actb.as<unsigned char>(),
+      c->fz_has.as<uint8_t>(), c->fz_zero.as<uint8_t>(),
+      c->fz_gid.as<int32_t>(), c->fz_fail.as<unsigned long long>());
+  CKL();
+  unsigned long long failed = 0;
+  CK(cudaMemcpyAsync(&failed, c->fz_fail.p, 8, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->launches += 2;
+  if (failed) return SL_OK;
+  FzCfg f{};
+  f.n_groups = ng;
+  f.gstart = c->fz_gstart.as<int32_t>();
+  f.gcount = c->fz_gcount.as<int32_t>();
+  f.ent = c->fz_ent.as<uint16_t>();
+  f.code = c->fz_code.as<uint8_t>();
+  f.dict = c->fz_dict.as<float2>();
+  f.actb = c->fz_actb.as<unsigned char>();
+  f.has_act = c->fz_has.as<uint8_t>();
+  f.ra = ra;
+  f.rb = rb;
+  const size_t smem = 32 * WIN_DMAX + 16 * 2 * (FZ_MAXM + 1) +
+                      8 * 4 * WIN_DMAX + (size_t)4 * rows * FZ_MAXM +
+                      WIN_DMAX;
+  if (launchers(c->prec).fused_setup(smem) != 0) {
+    cudaGetLastError();
+    return SL_OK;
+  }
+  c->fcfg = f;
+  c->fz_smem = smem;
+  c->fz_ok = true;
+  return SL_OK;
+}
+
+// One fused launch of n steps (sl_fused.cuh).  *aborted: the launch hit
+// something only the per-step kernels represent and committed nothing.
+int run_fused(sl_ctx *c, const KState &S, int64_t n, const double *times,
+              double dt, bool *aborted) {
+  *aborted = false;
+  CK(c->fz_times.ensure(8 * n));
+  CK(cudaMemcpyAsync(c->fz_times.p, times, 8 * n, cudaMemcpyHostToDevice,
+                     c->st));
+  CK(c->vel2.ensure(c->vel.bytes));
+  FzCfg f = c->fcfg;
+  f.vel_out = c->vel2.p;
+  f.times = c->fz_times.as<double>();
+  f.n_steps = n;
+  f.cur = c->cur;
+  f.write_acc = 1;
+  launchers(c->prec).fused(S, c->env, f, dt, c->fz_smem, c->st);
+  CKL();
+  c->launches++;
+  c->fz_launches++;
+  CK(cudaMemcpyAsync(c->h_status, c->status.p, 8 * 8, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (c->h_status[5]) {
+    *aborted = true;
+    c->fz_aborts++;
+    CK(cudaMemsetAsync(c->status.p, 0, 8 * 8, c->st));
+    return SL_OK;
+  }
+  std::swap(c->vel, c->vel2);  // committed: the new velocities
+  c->cur ^= 1;                  // final positions in pos[cur ^ 1]
+  if (c->h_status[6]) {
+    k_fused_clear_fext<<<blocks_for(c->m_n), 256, 0, c->st>>>(
+        c->m_n, c->vel2.as<float4>(), c->fext.as<float4>());
+    CKL();
+    c->launches++;
+  }
+  return SL_OK;
+}
+
 // Device build of the split layout (sl_split.cuh).  *used = false when the
 // mesh does not fit its index encoding (the caller falls back to the exact
 // layout).
@@ -1122,6 +1275,7 @@ int build_split_layout(sl_ctx *c, bool *used) {
   c->tma_warps = 0;
   configure_split_tma(c, widths);
   if (int rc = build_window_layout(c)) return rc;
+  if (int rc = build_fused_groups(c)) return rc;
   c->layout_valid = true;
   c->layout_builds++;
   c->launches += 8;
@@ -1220,6 +1374,8 @@ int sl_create(int device, int precision, sl_ctx **out) {
   c->fsz = precision == PREC_FP64 ? 8 : 4;
   if (const char *ev = getenv("SL_DISABLE_TMA")) c->tma_enabled = ev[0] == '0';
   if (const char *ev = getenv("SL_DISABLE_WIN")) c->win_enabled = ev[0] == '0';
+  if (const char *ev = getenv("SL_DISABLE_FUSED"))
+    c->fz_enabled = ev[0] == '0';
   if (const char *ev = getenv("SL_DISABLE_SPLIT"))
     c->split_enabled = ev[0] == '0';
   memset(&c->env, 0, sizeof c->env);
@@ -1270,6 +1426,10 @@ int sl_destroy(sl_ctx *c) {
                     &c->snap_dev, &c->sp_j, &c->sp_kl, &c->sp_s, &c->sp_w,
                     &c->sp_ekl, &c->degB, &c->sp_meta, &c->kdev,
                     &c->ghost, &c->s_grp, &c->sp_actc, &c->sp_acto, &c->win_rec, &c->win_dict, &c->win_actb, &c->win_zero, &c->win_blk,
+                    &c->fz_gstart, &c->fz_gcount, &c->fz_ent, &c->fz_code,
+                    &c->fz_dict, &c->fz_actb, &c->fz_has, &c->fz_fail,
+                    &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
+                    &c->fz_gid,
                     &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1301,6 +1461,9 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
                                                       : SL_PATH_SPLIT)
                  : (c->tma_warps ? SL_PATH_EXACT_TMA : SL_PATH_EXACT);
   o->split_batch = c->split && c->split_warps ? c->scfg.u : 0;
+  o->fused_groups = c->fz_ok ? c->fcfg.n_groups : 0;
+  o->fused_launches = c->fz_launches;
+  o->fused_aborts = c->fz_aborts;
   const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc,
                           &c->fext, &c->load, &c->m_gen, &c->m_alive,
                           &c->ends, &c->kL0, &c->s_alive, &c->s_degen,
@@ -1443,8 +1606,9 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
   // first actuated group on a live split layout: re-layout with act cells
   if (params_only && groups_before <= 1 && c->agrp.n > 1 && c->split)
     c->layout_valid = false;
-  // the window layout's material tables hold (k, L0) by value: rebuild
-  if (params_only && c->win) c->layout_valid = false;
+  // the window / fused layouts' material tables hold (k, L0) by value:
+  // rebuild
+  if (params_only && (c->win || c->fz_ok)) c->layout_valid = false;
   size_t need = align256(8 * n) * 16 + align256(n) * 5 + 2048;
   CK(c->stage.ensure(need));
   size_t off = 0;
@@ -1718,6 +1882,16 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
   const Launch &L = launchers(c->prec);
   KState S = make_state(c);
   if ((rc = upload_state(c, S))) return rc;
+  if (accumulation == SL_ACC_GATHER && c->fz_ok && !c->has_ghost &&
+      n_steps >= 2) {
+    // small bodies: all n steps in one launch, state on chip
+    bool aborted = false;
+    if ((rc = run_fused(c, S, n_steps, sim_times, dt, &aborted))) return rc;
+    if (!aborted) {
+      if (steps_done) *steps_done = n_steps;
+      return SL_OK;  // no spring events / errors on this path (eligibility)
+    }
+  }
   for (int64_t n = 0; n < n_steps; n++) {
     StepP T;
     T.sim_t = sim_times[n];

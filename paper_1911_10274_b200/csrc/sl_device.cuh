@@ -119,6 +119,12 @@ struct KState {
   const uint8_t *win_zero;
   uint32_t win_sb, win_oac, win_obc;
   int win_tt;
+  // multi-step fused groups (sl_fused.cuh; null when not built): material
+  // codes [group][rows][512], group of every mass, group starts / zero codes
+  uint8_t *fz_code;
+  const int32_t *fz_gid, *fz_gstart;
+  const uint8_t *fz_zero;
+  int fz_rows, fz_ra;
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -258,13 +264,17 @@ __device__ __forceinline__ void red_add(double4 *p, double x, double y,
 // Mass pass body (kernels.py:271-376), shared by the fused gather step and
 // the standalone mass kernel.  (fx, fy, fz) enters as the accumulated f_ext.
 // Writes pos_next / vel / acc; returns false on non-finite state.
+// integrate_vals: the new position (xyz, mass in w), velocity (xyz) and
+// acceleration of mass i, nothing stored; integrate(): the same plus the
+// stores and the non-finite check of the per-step kernels.
 template <int P>
-__device__ __forceinline__ void integrate(
-    const KState &S, const EnvP &E, const StepP &T, int64_t i,
+__device__ __forceinline__ void integrate_vals(
+    const KState &S, const EnvP &E, double dt_, int64_t i,
     typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
-    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz,
+    typename Tr<P>::R4 &np4, typename Tr<P>::R4 &nv, typename Tr<P>::R &ax,
+    typename Tr<P>::R &ay, typename Tr<P>::R &az) {
   using R = typename Tr<P>::R;
-  using R4 = typename Tr<P>::R4;
   const R mm = me.w;
   R px = me.x, py = me.y, pz = me.z;
   R vx = v.x, vy = v.y, vz = v.z;
@@ -332,7 +342,6 @@ __device__ __forceinline__ void integrate(
       fz += sc * ddz;
     }
   }
-  R ax, ay, az;
   if constexpr (P == PREC_FP64) {  // parity: three true divisions
     ax = fx / mm;
     ay = fy / mm;
@@ -343,7 +352,7 @@ __device__ __forceinline__ void integrate(
     ay = fy * im;
     az = fz * im;
   }
-  const R dt = (R)T.dt;
+  const R dt = (R)dt_;
   vx += ax * dt;
   vy += ay * dt;
   vz += az * dt;
@@ -379,17 +388,30 @@ __device__ __forceinline__ void integrate(
   px += vx * dt;
   py += vy * dt;
   pz += vz * dt;
-  R4 np4;
   np4.x = px;
   np4.y = py;
   np4.z = pz;
   np4.w = mm;
-  ((R4 *)S.pos[T.cur ^ 1])[i] = np4;
-  R4 nv;
   nv.x = vx;
   nv.y = vy;
   nv.z = vz;
   set_flags(nv.w, fl & ~MF_FEXT);
+}
+
+template <int P>
+__device__ __forceinline__ void integrate(
+    const KState &S, const EnvP &E, const StepP &T, int64_t i,
+    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
+    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  R4 np4, nv;
+  R ax, ay, az;
+  integrate_vals<P>(S, E, T.dt, i, me, v, fl, fx, fy, fz, np4, nv, ax, ay,
+                    az);
+  const R px = np4.x, py = np4.y, pz = np4.z, vx = nv.x, vy = nv.y,
+          vz = nv.z;
+  ((R4 *)S.pos[T.cur ^ 1])[i] = np4;
   ((R4 *)S.vel)[i] = nv;
   if (T.write_acc) {
     R *a = (R *)S.acc + 3 * i;
@@ -1013,6 +1035,20 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
         ((float2 *)S.sp_kl)[S.sp_ekl[s]] = make_float2(0.f, 0.f);
     }
     if (S.e2[s] >= 0) S.sp_j[S.e2[s]] = S.sp_null;
+    if (S.fz_code) {  // fused groups: both entries get the zero code
+      const int64_t per = (int64_t)S.sp_rows * 32;
+      const int64_t es[2] = {S.e1[s], S.e2[s]};
+      for (int q = 0; q < 2; q++) {
+        if (es[q] < 0) continue;
+        const int64_t sl = es[q] / per;
+        const int rem = (int)(es[q] - sl * per);
+        const int64_t i = sl * 32 + (rem & 31);
+        const int row = q == 0 ? rem >> 5 : S.fz_ra + (rem >> 5) - (1 << S.sp_a);
+        const int32_t g = S.fz_gid[i];
+        S.fz_code[((int64_t)g * S.fz_rows + row) * 512 + (i - S.fz_gstart[g])] =
+            S.fz_zero[g];
+      }
+    }
     if (S.win_blk) {  // window layout: both entries get the zero code
       const int a = S.sp_a;
       if (S.e1[s] >= 0) {
@@ -1140,6 +1176,10 @@ struct Launch {
   void (*win)(const KState &, const EnvP &, const StepP &,
               const struct WinCfg &, int grid, cudaStream_t);
   int (*win_setup)(const struct WinCfg &);
+  // multi-step fused small-body kernel (fp32, sl_fused.cuh)
+  void (*fused)(const KState &, const EnvP &, const struct FzCfg &,
+                double dt, size_t smem, cudaStream_t);
+  int (*fused_setup)(size_t smem);
 };
 
 const Launch &launchers(int prec);

@@ -1,0 +1,329 @@
+// sl_fused.cuh -- several steps per launch for small bodies (fp32):
+// north_star "optional fusion of several steps per launch using
+// shared-memory staging for small bodies"; SURVEY.md 7 build step 9.
+//
+// Config D (an RL batch of thousands of 5^3 robots) is a swarm of small
+// disconnected bodies.  Bodies are packed into GROUPS of whole connected
+// components (<= FZ_MAXM masses; the host finds component boundaries from
+// the springs), one CTA per group, one thread per mass.  The group's
+// positions (double-buffered), its incidence entries (16-bit local partner
+// + 8-bit material code, A section then B section per mass, the split
+// layout's order) and its material table live in shared memory for the
+// whole launch; velocities and flags live in registers.  A launch runs all
+// n steps of an sl_step call with one __syncthreads per step and touches
+// HBM only to load the state at the start and store it at the end.
+//
+// Per-step semantics are the window kernel's (same entry arithmetic,
+// win_body; same mass update, integrate_vals; actuation through the
+// per-group table, factor in fp64 once per material per step).  A context
+// is eligible only without special masses (breakable / custom-waveform
+// springs), ghosts or oversized components.  Anything the fast path cannot
+// represent -- a zero-length spring, a non-finite state -- aborts the whole
+// launch: nothing is committed (final positions go to the other ping-pong
+// buffer, velocities to a second buffer, swapped only on success) and the
+// host re-runs the same steps through the per-step kernels, which own the
+// reference's exact event semantics.
+#pragma once
+#include "sl_window.cuh"
+
+namespace sl {
+
+constexpr int FZ_MAXM = 512;  // masses per group = threads per CTA
+constexpr int FZ_MAXR = 32;   // entry rows per mass (A + B)
+
+struct FzCfg {
+  int64_t n_groups;
+  const int32_t *gstart;  // [g] first mass of the group
+  const int32_t *gcount;  // [g] masses
+  const uint16_t *ent;    // [g][ra + rb][FZ_MAXM] local partner (FZ_MAXM:
+                          // the sentinel record)
+  const uint8_t *code;    // [g][ra + rb][FZ_MAXM] material code
+  const float2 *dict;     // [g][WIN_DMAX] (k, k L0)
+  const unsigned char *actb;  // [g][WIN_ACTB] actuation block (window fmt)
+  const uint8_t *has_act;     // [g]
+  int ra, rb;                 // A / B rows per mass
+  void *vel_out;              // final velocities (swapped in on success)
+  const double *times;        // [n_steps] step times (device)
+  int64_t n_steps;
+  int cur;        // position buffer read at step 0; final -> cur ^ 1
+  int write_acc;  // store the last step's accelerations
+};
+
+// Group build: one CTA per group, one thread per mass.  fail[0] |= 1 when
+// the group does not fit (partner outside the group, too many materials,
+// special mass, hash collision).
+static __global__ void __launch_bounds__(FZ_MAXM)
+    k_fused_build(const uint32_t *sp_j, const uint32_t *sp_w,
+                  const float2 *sp_kl, const int32_t *sp_s, const int8_t *mode,
+                  const double4 *act, const uint8_t *grp, const float4 *vel,
+                  int a, int rows, uint32_t sent, uint32_t nul,
+                  const int32_t *gstart, const int32_t *gcount, int ra, int rb,
+                  uint16_t *ent, uint8_t *code, float2 *dict,
+                  unsigned char *actb, uint8_t *has_act, uint8_t *zero,
+                  int32_t *gid, unsigned long long *fail) {
+  __shared__ unsigned long long dkey[WIN_DMAX];
+  __shared__ float2 dkl[WIN_DMAX];
+  __shared__ double4 dact[WIN_DMAX];
+  __shared__ int8_t dmode[WIN_DMAX];
+  __shared__ int ok;
+  const int64_t g = blockIdx.x;
+  const int li = threadIdx.x;
+  const int32_t g0 = gstart[g], gn = gcount[g];
+  const int64_t i = (int64_t)g0 + li;
+  const bool mine = li < gn;
+  if (li < WIN_DMAX) dkey[li] = WIN_EMPTY;
+  if (li == 0) ok = 1;
+  __syncthreads();
+  MatTable tab{dkey, dkl, dact, dmode};
+  const Mat zero_m = mat_zero();
+  const unsigned long long zero_key = mat_hash(zero_m);
+  if (li == 0 && tab.find(zero_key, true, &zero_m) < 0) ok = 0;
+  if (mine && (flags_of(vel[i].w) & MF_SPECIAL)) ok = 0;
+  __syncthreads();
+  const int64_t sl = i >> 5;
+  const int lane = (int)(i & 31);
+  const uint32_t wd = mine ? sp_w[sl] : 0u;
+  const int wa = (int)(wd & 0xFFFF), wb = (int)(wd >> 16);
+  // entry q of this mass: (partner, kl index, spring slot) or none
+  auto entry = [&](int q, uint32_t *kli, uint32_t *s) -> uint32_t {
+    if (!mine) return 0xFFFFFFFFu;
+    if (q < ra) {
+      if (q >= wa) return 0xFFFFFFFFu;
+      const int64_t e = (sl * rows + q) * 32 + lane;
+      const uint32_t w = sp_j[e];
+      if (w == sent) return 0xFFFFFFFFu;
+      *kli = (uint32_t)((sl << (a + 5)) | (q << 5) | lane);
+      *s = (uint32_t)sp_s[e];
+      return w;
+    }
+    const int r = q - ra;
+    if (r >= wb) return 0xFFFFFFFFu;
+    const int64_t e = (sl * rows + (1 << a) + r) * 32 + lane;
+    const uint32_t w = sp_j[e];
+    if (w == nul) return 0xFFFFFFFFu;
+    *kli = w;
+    *s = (uint32_t)sp_s[e];
+    return split_partner(w, a);
+  };
+  for (int q = 0; q < ra + rb; q++) {
+    uint32_t kli = 0, s = 0;
+    const uint32_t j = entry(q, &kli, &s);
+    if (j == 0xFFFFFFFFu) continue;
+    if ((int64_t)j < g0 || (int64_t)j >= (int64_t)g0 + gn) ok = 0;
+    const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
+    if (tab.find(mat_hash(x), true, &x) < 0) ok = 0;
+  }
+  __syncthreads();
+  const int zc = tab.find(zero_key, false, nullptr);
+  if (mine) gid[i] = (int32_t)g;
+  if (li == 0) zero[g] = (uint8_t)(zc < 0 ? 0 : zc);
+  for (int q = 0; q < ra + rb; q++) {
+    uint32_t kli = 0, s = 0;
+    const uint32_t j = entry(q, &kli, &s);
+    uint16_t p = FZ_MAXM;
+    int c = zc;
+    if (j != 0xFFFFFFFFu) {
+      const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
+      c = tab.find(mat_hash(x), false, nullptr);
+      if (!tab.same(c, x)) ok = 0;
+      p = (uint16_t)(j - (uint32_t)g0);
+    }
+    const int64_t x = (g * (ra + rb) + q) * FZ_MAXM + li;
+    ent[x] = p;
+    code[x] = (uint8_t)(c < 0 ? 0 : c);
+  }
+  __syncthreads();
+  if (!ok) {
+    if (li == 0) atomicOr(fail, 1ull);
+    return;
+  }
+  if (li < WIN_DMAX) {  // table + actuation block, the window formats
+    const bool used = dkey[li] != WIN_EMPTY;
+    const float2 kl = used ? dkl[li] : make_float2(0.f, 0.f);
+    dict[g * WIN_DMAX + li] = make_float2(kl.x, kl.x * kl.y);
+    unsigned char *ab = actb + g * WIN_ACTB;
+    ((double4 *)ab)[li] = used ? dact[li] : make_double4(0.0, 0.0, 0.0, 0.0);
+    ((float2 *)(ab + 32 * WIN_DMAX))[li] = kl;
+    ((int8_t *)(ab + 40 * WIN_DMAX))[li] = used ? dmode[li] : (int8_t)0;
+  }
+  if (li == 0) {
+    int any = 0;
+    for (int q = 0; q < WIN_DMAX; q++)
+      if (dkey[q] != WIN_EMPTY && (dmode[q] == 1 || dmode[q] == 2)) any = 1;
+    has_act[g] = (uint8_t)any;
+  }
+}
+
+// The fused multi-step kernel (fp32).  Dynamic shared memory:
+//   act (WIN_DMAX double4) | pos [2][FZ_MAXM + 1] float4 | tables [2] +
+//   static table (3 x WIN_DMAX float2) | raw (k, L0) (WIN_DMAX float2) |
+//   entries (rows x FZ_MAXM u32: partner | code << 16) | modes
+template <int P>
+__global__ void __launch_bounds__(FZ_MAXM, 2)
+    k_fused_small(const KState S, const EnvP E, const FzCfg C, double dt) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int rows = C.ra + C.rb;
+  double4 *sact = (double4 *)smem;
+  R4 *spos = (R4 *)(sact + WIN_DMAX);
+  F2 *stab = (F2 *)(spos + 2 * (FZ_MAXM + 1));  // [3][WIN_DMAX]
+  F2 *skl = stab + 3 * WIN_DMAX;
+  // entries packed as partner | code << 16: one shared load per entry
+  uint32_t *sen = (uint32_t *)(skl + WIN_DMAX);
+  int8_t *smode = (int8_t *)(sen + rows * FZ_MAXM);
+  __shared__ int sbad;
+  const int64_t g = blockIdx.x;
+  const int li = threadIdx.x;
+  const int32_t g0 = C.gstart[g], gn = C.gcount[g];
+  const int64_t i = (int64_t)g0 + li;
+  const bool mine = li < gn;
+  const bool act = C.has_act[g] != 0;
+  // ---- load the group
+  R4 me, v;
+  uint32_t fl = 0;
+  if (mine) {
+    me = ((const R4 *)S.pos[C.cur])[i];
+    v = ((const R4 *)S.vel)[i];
+    fl = flags_of(v.w);
+  } else {
+    me.x = me.y = me.z = (R)SENTINEL_POS;
+    me.w = (R)1;
+    v.x = v.y = v.z = v.w = (R)0;
+  }
+  spos[li] = me;
+  if (li == 0) {
+    R4 far;
+    far.x = far.y = far.z = (R)SENTINEL_POS;
+    far.w = (R)0;
+    spos[FZ_MAXM] = far;
+    spos[2 * FZ_MAXM + 1] = far;
+    sbad = 0;
+  }
+  for (int q = 0; q < rows; q++) {
+    const int64_t x = (g * rows + q) * FZ_MAXM + li;
+    sen[q * FZ_MAXM + li] = (uint32_t)C.ent[x] | ((uint32_t)C.code[x] << 16);
+  }
+  if (li < WIN_DMAX) {
+    stab[2 * WIN_DMAX + li] = C.dict[g * WIN_DMAX + li];
+    if (act) {
+      const unsigned char *ab = C.actb + g * WIN_ACTB;
+      sact[li] = ((const double4 *)ab)[li];
+      skl[li] = ((const float2 *)(ab + 32 * WIN_DMAX))[li];
+      smode[li] = ((const int8_t *)(ab + 40 * WIN_DMAX))[li];
+    }
+  }
+  // f_ext at the first step (loads / spring_pass results), then cleared
+  R f0x = 0, f0y = 0, f0z = 0;
+  const bool had_fext = mine && (fl & MF_FEXT);
+  if (had_fext) {
+    const R4 f = ((const R4 *)S.fext)[i];
+    f0x = f.x;
+    f0y = f.y;
+    f0z = f.z;
+  }
+  const bool live = mine && (fl & MF_ALIVE);
+  R ax = 0, ay = 0, az = 0;
+  // step k's effective table (k, k L0 factor(T_k)) into buffer k & 1
+  // (kernels.py:55-62), by the first WIN_DMAX threads; computed one step
+  // ahead so each step needs one barrier
+  auto eff_table = [&](int64_t k) {
+    if (!act || li >= WIN_DMAX || k >= C.n_steps) return;
+    const double T = __ldg(C.times + k);
+    const double4 A = sact[li];
+    const int m = smode[li];
+    float f = 1.0f;
+    if ((m == 1 || m == 2) && !(m == 2 && !(T >= A.z)))
+      f = (float)(1.0 + A.x * sin(A.y * py_mod(T - A.z, A.w)));
+    F2 e;
+    e.x = skl[li].x;
+    e.y = skl[li].x * (f * skl[li].y);
+    stab[(k & 1) * WIN_DMAX + li] = e;
+  };
+  eff_table(0);
+  __syncthreads();
+  // ---- the steps
+  int64_t k = 0;
+  for (; k < C.n_steps; k++) {
+    const int b = (int)(k & 1);
+    const F2 *tab = act ? stab + b * WIN_DMAX : stab + 2 * WIN_DMAX;
+    const R4 *pin = spos + b * (FZ_MAXM + 1);
+    R4 *pout = spos + (b ^ 1) * (FZ_MAXM + 1);
+    R4 np = me;
+    if (live) {
+      if (fl & MF_FIXED) {  // kernels.py:260-270
+        v.x = v.y = v.z = (R)0;
+        ax = ay = az = (R)0;
+      } else {
+        R gx = 0, gy = 0, gz = 0, bx = 0, by = 0, bz = 0;
+        const uint32_t *e = sen + li;
+#pragma unroll 4
+        for (int q = 0; q < C.ra; q++) {
+          const uint32_t w = e[q * FZ_MAXM];
+          win_body(me, pin[w & 0xFFFFu], tab[w >> 16], gx, gy, gz);
+        }
+#pragma unroll 4
+        for (int q = C.ra; q < rows; q++) {
+          const uint32_t w = e[q * FZ_MAXM];
+          win_body(me, pin[w & 0xFFFFu], tab[w >> 16], bx, by, bz);
+        }
+        const R fx = f0x + (gx + bx), fy = f0y + (gy + by),
+                fz = f0z + (gz + bz);
+        f0x = f0y = f0z = (R)0;
+        R4 nv;
+        integrate_vals<P>(S, E, dt, i, me, v, fl, fx, fy, fz, np, nv, ax, ay,
+                          az);
+        v = nv;
+        const R z0 = np.x * (R)0 + np.y * (R)0 + np.z * (R)0 + v.x * (R)0 +
+                     v.y * (R)0 + v.z * (R)0;
+        if (!(z0 == (R)0)) sbad = 1;  // zero-length spring or blow-up
+      }
+    }
+    pout[li] = np;
+    me = np;
+    eff_table(k + 1);  // the other buffer: nobody reads it this step
+    __syncthreads();
+    if (sbad) break;
+  }
+  if (sbad) {  // nothing committed; the host re-runs the steps
+    if (li == 0) atomicOr(S.status + 5, 1ull);
+    return;
+  }
+  if (!mine) return;
+  ((R4 *)S.pos[C.cur ^ 1])[i] = me;
+  R4 vo = v;
+  set_flags(vo.w, fl & ~MF_FEXT);
+  ((R4 *)C.vel_out)[i] = vo;
+  if (C.write_acc && live) {
+    R *a = (R *)S.acc + 3 * i;
+    a[0] = ax;
+    a[1] = ay;
+    a[2] = az;
+  }
+  if (had_fext) atomicAdd(S.status + 6, 1ull);  // f_ext rows to clear
+}
+
+// f_ext rows of masses whose (pre-launch) flags had MF_FEXT are zeroed after
+// a committed fused launch (kernels.py:372: the accumulator is cleared)
+static __global__ void k_fused_clear_fext(int64_t m_n, const float4 *vel_old,
+                                          float4 *fext) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m_n && (flags_of(vel_old[i].w) & MF_FEXT))
+    fext[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// component boundaries: cover[b] = springs spanning (b - 1, b)
+static __global__ void k_fused_cover(int64_t s_n, const int2 *ends,
+                                     int32_t *diff) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s_n) return;
+  const int2 e = ends[s];
+  if (e.x < 0) return;
+  const int lo = e.x < e.y ? e.x : e.y, hi = e.x < e.y ? e.y : e.x;
+  if (lo == hi) return;
+  atomicAdd(diff + lo + 1, 1);
+  atomicAdd(diff + hi + 1, -1);
+}
+
+}  // namespace sl

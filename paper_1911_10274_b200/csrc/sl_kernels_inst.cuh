@@ -6,6 +6,7 @@
 #include "sl_device.cuh"
 #include "sl_split.cuh"
 #include "sl_window.cuh"
+#include "sl_fused.cuh"
 
 
 namespace sl {
@@ -76,6 +77,20 @@ struct SplitLaunch {
       }
     }
   }
+  // multi-step fused small-body kernel (fp32 only)
+  static void fused(const KState &S, const EnvP &E, const FzCfg &C,
+                    double dt, size_t smem, cudaStream_t st) {
+    if constexpr (P == PREC_FP32)
+      k_fused_small<P><<<(unsigned)C.n_groups, FZ_MAXM, smem, st>>>(S, E, C,
+                                                                   dt);
+  }
+  static int fused_setup(size_t smem) {
+    if constexpr (P == PREC_FP32)
+      return (int)cudaFuncSetAttribute(
+          k_fused_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)smem);
+    return 1;
+  }
   static int win_setup(const WinCfg &C) {
     int rc = 1;
     if constexpr (P == PREC_FP32)
@@ -114,6 +129,9 @@ struct SplitLaunch<PREC_FP64> {
   static void win(const KState &, const EnvP &, const StepP &,
                   const WinCfg &, int, cudaStream_t) {}
   static int win_setup(const WinCfg &) { return 1; }
+  static void fused(const KState &, const EnvP &, const FzCfg &, double,
+                    size_t, cudaStream_t) {}
+  static int fused_setup(size_t) { return 1; }
 };
 }  // namespace sl
 
@@ -173,13 +191,20 @@ struct SplitLaunch<PREC_FP64> {
   int FN##_win_setup(const WinCfg &C) {                                      \
     return SplitLaunch<PREC>::win_setup(C);                                  \
   }                                                                          \
+  void FN##_fused(const KState &S, const EnvP &E, const FzCfg &C, double dt, \
+                  size_t smem, cudaStream_t st) {                            \
+    SplitLaunch<PREC>::fused(S, E, C, dt, smem, st);                         \
+  }                                                                          \
+  int FN##_fused_setup(size_t smem) {                                        \
+    return SplitLaunch<PREC>::fused_setup(smem);                             \
+  }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \
     static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
                              FN##_force, FN##_spring, FN##_mass,             \
                              FN##_split, FN##_split_force, FN##_split_tma,   \
                              FN##_split_setup, FN##_win,                     \
-                             FN##_win_setup};                                \
+                             FN##_win_setup, FN##_fused, FN##_fused_setup};  \
     return L;                                                                \
   }                                                                          \
   }
