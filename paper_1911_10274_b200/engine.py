@@ -160,6 +160,7 @@ class DeviceMirror:
         if springs and s:
             self.ctx.download_springs(store._s_alive[:s].view(np.uint8),
                                       store._s_degen[:s].view(np.uint8))
+            store._deaths_maybe = True
 
     def log_degenerate(self, store: ObjectStore):
         """engine._log_degenerate (engine.py:205-215)."""
@@ -266,6 +267,7 @@ def spring_pass(store: ObjectStore, sim_t: float, cfg: StepConfig) -> None:
     if s:
         mir.ctx.download_springs(store._s_alive[:s].view(np.uint8),
                                  store._s_degen[:s].view(np.uint8))
+        store._deaths_maybe = True
     if mir.counters[2]:
         mir.log_degenerate(store)
 
@@ -357,18 +359,34 @@ def throughput(springs: int, steps: int, wall_seconds: float) -> float:
 def check_stability(store: ObjectStore, dt: float,
                     env: Environment | None = None) -> float:
     """dt*sqrt(k_max/m_min), contacts included; warns above 0.5
-    (engine.py:274-296)."""
-    ms = store.alive_mass_slots()
-    if len(ms) == 0:
+    (engine.py:274-296).  The spring / mass extrema are masked reductions
+    cached on the store's version counters (SimController.start calls this
+    on every start: 12.7 M springs made it ~60 ms of host time)."""
+    store.reconcile_spring_deaths()
+    key = (store.topology_version, store.spring_param_version,
+           store.mass_version, store.spring_slot_count,
+           store.mass_slot_count)
+    cached = getattr(store, "_stability_cache", None)
+    if cached is not None and cached[0] == key:
+        n_alive, k_springs, m_min = cached[1:]
+    else:
+        mn, sn = store.mass_slot_count, store.spring_slot_count
+        alive = store._m_alive[:mn].astype(bool, copy=False)
+        n_alive = int(np.count_nonzero(alive))
+        m_min = float(np.min(store._m_mass[:mn], where=alive,
+                             initial=np.inf)) if n_alive else np.inf
+        s_alive = store._s_alive[:sn].astype(bool, copy=False)
+        k_springs = float(np.max(store._s_k[:sn], where=s_alive,
+                                 initial=0.0)) if sn else 0.0
+        store._stability_cache = (key, n_alive, k_springs, m_min)
+    if n_alive == 0:
         return 0.0
-    ss = store.alive_spring_slots()
-    k_max = float(store._s_k[ss].max()) if len(ss) else 0.0
+    k_max = k_springs
     if env is not None:
         for c in env.contacts:
             k_max = max(k_max, c.stiffness)
     if k_max == 0.0:
         return 0.0
-    m_min = float(store._m_mass[ms].min())
     ratio = dt * math.sqrt(k_max / m_min) if m_min > 0 else math.inf
     if ratio > 0.5:
         log.warning("dt*sqrt(k_max/m_min) = %.3g exceeds 0.5; integration "
