@@ -198,6 +198,18 @@ int sl_download_masses(sl_ctx *ctx, double *pos, double *vel, double *acc,
 /* Spring liveness / zero-length flags back into bool[s_n]; NULL skips. */
 int sl_download_springs(sl_ctx *ctx, uint8_t *alive, uint8_t *degen);
 
+/* ------------------------------------------------------------ diagnostics */
+/* engine.mechanical_energy (engine.py:366-389) from the device state:
+ * out = {kinetic, spring potential (actuated rest length at sim_t),
+ * gravitational potential (origin reference, gravity[3])}; fp64 partial
+ * sums in a fixed order (deterministic). */
+int sl_energy(sl_ctx *ctx, double sim_t, const double *gravity, double *out);
+/* engine.spring_loads (engine.py:392-412): per spring slot [0, s_n) the
+ * length and |k (|d| - f L0)| at sim_t; NaN for dead slots (the caller
+ * compacts over alive slots and forms the stress from its diameters). */
+int sl_spring_loads(sl_ctx *ctx, double sim_t, double *lengths,
+                    double *force_magnitudes);
+
 /* Asynchronous snapshot (north_star "pinned-memory async snapshots"):
  * enqueue a D2H copy of positions + velocities into library-owned pinned
  * buffers on a side stream, ordered after all work issued so far; returns

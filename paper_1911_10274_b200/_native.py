@@ -33,7 +33,7 @@ EXPORTS = (
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
-    "sl_get_stream")
+    "sl_get_stream", "sl_energy", "sl_spring_loads")
 
 
 class SlStats(C.Structure):
@@ -97,6 +97,8 @@ def load_library(path: str = LIB_PATH):
             "sl_mark_ghosts": ([P, I64, P], I),
             "sl_state_pointers": ([P, P, P, P], I),
             "sl_get_stream": ([P, P], I),
+            "sl_energy": ([P, D, P, P], I),
+            "sl_spring_loads": ([P, D, P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -239,6 +241,22 @@ class Context:
         self._check(self.lib.sl_write_spring_params(self.h, len(s), _ptr(s),
                                                     *map(_ptr, a)),
                     "sl_write_spring_params")
+
+    def energy(self, sim_t: float, gravity) -> np.ndarray:
+        """(kinetic, spring potential, gravitational potential)."""
+        g = _c(gravity, np.float64)
+        out = np.zeros(3)
+        self._check(self.lib.sl_energy(self.h, float(sim_t), _ptr(g),
+                                       _ptr(out)), "sl_energy")
+        return out
+
+    def spring_loads(self, sim_t: float, n: int):
+        """(lengths, |F|) per spring slot [0, n); NaN for dead slots."""
+        lengths, fmag = np.empty(n), np.empty(n)
+        self._check(self.lib.sl_spring_loads(self.h, float(sim_t),
+                                             _ptr(lengths), _ptr(fmag)),
+                    "sl_spring_loads")
+        return lengths, fmag
 
     def kill_springs(self, slots):
         s = _c(slots, np.int64)

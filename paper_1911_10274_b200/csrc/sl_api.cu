@@ -118,6 +118,7 @@ struct sl_ctx {
   int64_t fz_launches = 0, fz_aborts = 0;
   DevBuf fz_gstart, fz_gcount, fz_ent, fz_code, fz_dict, fz_actb, fz_has,
       fz_zero, fz_gid, fz_fail, fz_times, fz_diff, vel2;
+  DevBuf diag;  // diagnostics scratch (sl_energy / sl_spring_loads)
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -425,6 +426,79 @@ __global__ void k_validate(KState S, const uint8_t *m_alive,
   S.ends[s] = make_int2(-1, -1);
   S.s_alive[s] = 0;
   if (layout_valid) kill_entries(S, s);
+}
+
+// ------------------------------------------------------- diagnostics
+// engine.mechanical_energy (engine.py:366-389) on the device: per-block
+// partial sums of m |v|^2, m (x . g) and k (|d| - f L0)^2 in fp64 (fixed
+// block tree order), finished on the host in block order -- deterministic.
+constexpr int DIAG_BLOCKS = 592, DIAG_THREADS = 256;
+template <int P>
+__global__ void __launch_bounds__(DIAG_THREADS)
+    k_energy(const KState S, int cur, double gx, double gy, double gz,
+             double sim_t, double *part) {
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  __shared__ double red[3][DIAG_THREADS];
+  double ke = 0.0, gp = 0.0, sp = 0.0;
+  const R4 *pos = (const R4 *)S.pos[cur];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < S.m_n; i += stride) {
+    const R4 v = ((const R4 *)S.vel)[i];
+    if (!(flags_of(v.w) & MF_ALIVE)) continue;
+    const R4 p = pos[i];
+    const double m = (double)p.w;
+    ke += m * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z);
+    gp += m * ((double)p.x * gx + (double)p.y * gy + (double)p.z * gz);
+  }
+  for (int64_t s = t0; s < S.s_n; s += stride) {
+    const int2 e = S.ends[s];
+    if (e.x < 0) continue;
+    const R4 a = pos[e.x], b = pos[e.y];
+    const double dx = (double)b.x - a.x, dy = (double)b.y - a.y,
+                 dz = (double)b.z - a.z;
+    const double len = sqrt(dx * dx + dy * dy + dz * dz);
+    const F2 kl = ((const F2 *)S.kL0)[s];
+    const double f = S.mode[s] ? act_factor(S, s, sim_t) : 1.0;
+    const double x = len - f * (double)kl.y;
+    sp += (double)kl.x * (x * x);
+  }
+  red[0][threadIdx.x] = ke;
+  red[1][threadIdx.x] = gp;
+  red[2][threadIdx.x] = sp;
+  __syncthreads();
+  for (int h = DIAG_THREADS / 2; h; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      for (int q = 0; q < 3; q++) red[q][threadIdx.x] += red[q][threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) part[3 * blockIdx.x + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// engine.spring_loads (engine.py:392-412) minus the host-side stress: per
+// slot the length and |k (|d| - f L0)| (NaN for dead slots)
+template <int P>
+__global__ void k_spring_loads(const KState S, int cur, double sim_t,
+                               double *len_out, double *fmag_out) {
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S.s_n) return;
+  const int2 e = S.ends[s];
+  if (e.x < 0) {
+    len_out[s] = fmag_out[s] = CUDART_NAN;
+    return;
+  }
+  const R4 *pos = (const R4 *)S.pos[cur];
+  const R4 a = pos[e.x], b = pos[e.y];
+  const double dx = (double)b.x - a.x, dy = (double)b.y - a.y,
+               dz = (double)b.z - a.z;
+  const double len = sqrt(dx * dx + dy * dy + dz * dz);
+  const F2 kl = ((const F2 *)S.kL0)[s];
+  const double f = S.mode[s] ? act_factor(S, s, sim_t) : 1.0;
+  len_out[s] = len;
+  fmag_out[s] = fabs((double)kl.x * (len - f * (double)kl.y));
 }
 
 // ------------------------------------------------------- layout build kernels
@@ -1429,7 +1503,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_gstart, &c->fz_gcount, &c->fz_ent, &c->fz_code,
                     &c->fz_dict, &c->fz_actb, &c->fz_has, &c->fz_fail,
                     &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
-                    &c->fz_gid,
+                    &c->fz_gid, &c->diag,
                     &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1986,6 +2060,63 @@ int sl_mass_pass(sl_ctx *c, double dt, int64_t *err_slot) {
   if (err_slot) *err_slot = err;
   if (err) return fail(c, SL_ENUMERIC, "non-finite state on mass slot %lld",
                        (long long)(err - 1));
+  return SL_OK;
+}
+
+int sl_energy(sl_ctx *c, double sim_t, const double *gravity,
+              double *out) {
+  if (!c || !gravity || !out) return fail(c, SL_EINVAL, "sl_energy: NULL");
+  if (!c->masses_set || !c->springs_set)
+    return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
+  CK(cudaSetDevice(c->device));
+  CK(c->diag.ensure(8 * 3 * DIAG_BLOCKS));
+  KState S = make_state(c);
+  auto k = c->prec == PREC_FP64   ? k_energy<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_energy<PREC_FP32>
+                                  : k_energy<PREC_MIXED>;
+  k<<<DIAG_BLOCKS, DIAG_THREADS, 0, c->st>>>(S, c->cur, gravity[0],
+                                             gravity[1], gravity[2], sim_t,
+                                             c->diag.as<double>());
+  CKL();
+  c->launches++;
+  std::vector<double> part(3 * DIAG_BLOCKS);
+  CK(cudaMemcpyAsync(part.data(), c->diag.p, 8 * 3 * DIAG_BLOCKS,
+                     cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  double ke = 0.0, gp = 0.0, sp = 0.0;
+  for (int b = 0; b < DIAG_BLOCKS; b++) {
+    ke += part[3 * b];
+    gp += part[3 * b + 1];
+    sp += part[3 * b + 2];
+  }
+  out[0] = 0.5 * ke;  // kinetic
+  out[1] = 0.5 * sp;  // spring potential
+  out[2] = -gp;       // gravitational potential (origin reference)
+  return SL_OK;
+}
+
+int sl_spring_loads(sl_ctx *c, double sim_t, double *lengths,
+                    double *force_magnitudes) {
+  if (!c || !lengths || !force_magnitudes)
+    return fail(c, SL_EINVAL, "sl_spring_loads: NULL");
+  if (!c->masses_set || !c->springs_set)
+    return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
+  const int64_t n = c->s_n;
+  if (n == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  CK(c->diag.ensure(16 * n));
+  KState S = make_state(c);
+  auto k = c->prec == PREC_FP64   ? k_spring_loads<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_spring_loads<PREC_FP32>
+                                  : k_spring_loads<PREC_MIXED>;
+  double *d = c->diag.as<double>();
+  k<<<blocks_for(n), 256, 0, c->st>>>(S, c->cur, sim_t, d, d + n);
+  CKL();
+  c->launches++;
+  CK(cudaMemcpyAsync(lengths, d, 8 * n, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(force_magnitudes, d + n, 8 * n, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
   return SL_OK;
 }
 

@@ -482,6 +482,44 @@ class SpringLoads:
     stresses: np.ndarray
 
 
+def device_mechanical_energy(store: ObjectStore, env: Environment,
+                             cfg: StepConfig, sim_t: float = 0.0,
+                             push: bool = True) -> EnergyBreakdown:
+    """mechanical_energy from the device copy of the store (sl_energy): the
+    diagnostic cmd_run logs at every pause, without downloading the state.
+    ``push=False`` uses the device state as it stands (the store mirror is
+    current, e.g. right after engine.run_steps)."""
+    mir = mirror_for(store, cfg)
+    if push:
+        mir.push(store, env)
+    if mir.has_custom:
+        mir.push_custom(store, sim_t)
+    ke, spe, gpe = mir.ctx.energy(sim_t, env.gravity.as_array())
+    return EnergyBreakdown(float(ke), float(spe), float(gpe))
+
+
+def device_spring_loads(store: ObjectStore, cfg: StepConfig,
+                        sim_t: float = 0.0, env: Environment | None = None,
+                        push: bool = True) -> SpringLoads:
+    """spring_loads with the per-spring gather / length / |F| on the device
+    (sl_spring_loads); compaction over alive slots and the stress on the
+    host, exactly as spring_loads forms them."""
+    mir = mirror_for(store, cfg)
+    if push:
+        mir.push(store, env)
+    if mir.has_custom:
+        mir.push_custom(store, sim_t)
+    n = store.spring_slot_count
+    lengths, fmag = mir.ctx.spring_loads(sim_t, n)
+    s = store.alive_spring_slots()
+    lengths, fmag = lengths[s], fmag[s]
+    area = 0.25 * np.pi * store._s_diam[s] ** 2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        stress = np.where(area > 0, fmag / np.where(area > 0, area, 1.0),
+                          np.where(fmag > 0, np.inf, 0.0))
+    return SpringLoads(s, lengths, fmag, stress)
+
+
 def spring_loads(store: ObjectStore, sim_t: float = 0.0) -> SpringLoads:
     """Per-spring |F| and stress (engine.py:402-412)."""
     s = store.alive_spring_slots()
