@@ -53,6 +53,7 @@ extern "C" {
  *            (reference "linearizable": order-dependent rounding)         */
 #define SL_ACC_GATHER 0
 #define SL_ACC_ATOMIC 1
+#define SL_ACC_AUTO 2   /* gather unless hub masses (widest list > 128) */
 
 typedef struct sl_ctx sl_ctx;
 

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "libsoftlat_cuda.so")
 
 SL_OK, SL_EINVAL, SL_ECUDA, SL_ENUMERIC, SL_ESTATE, SL_EUNSUPPORTED = range(6)
 PRECISIONS = {"fp64": 0, "fp32": 1, "mixed": 2}
-ACC_GATHER, ACC_ATOMIC = 0, 1
+ACC_GATHER, ACC_ATOMIC, ACC_AUTO = 0, 1, 2
 
 # every symbol the header declares (tests check the .so exports them all)
 EXPORTS = (

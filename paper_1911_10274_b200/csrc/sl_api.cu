@@ -119,6 +119,7 @@ struct sl_ctx {
   DevBuf fz_gstart, fz_gcount, fz_ent, fz_code, fz_dict, fz_actb, fz_has,
       fz_zero, fz_gid, fz_fail, fz_times, fz_diff, vel2;
   DevBuf diag;  // diagnostics scratch (sl_energy / sl_spring_loads)
+  bool auto_atomic = false;  // SL_ACC_AUTO resolved to the atomic variant
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -1357,6 +1358,18 @@ int build_split_layout(sl_ctx *c, bool *used) {
   return SL_OK;
 }
 
+// SL_ACC_AUTO: the deterministic gather unless the mesh has hub masses
+// whose incidence lists would serialise one thread (or warp) per mass; then
+// the per-spring atomic variant spreads them.  Every mesh
+// measured so far picks the gather.
+constexpr int64_t AUTO_HUB_ENTRIES = 128;  // entries per mass (lattice: 26)
+int resolve_accumulation(sl_ctx *c, int acc) {
+  if (acc != SL_ACC_AUTO) return acc;
+  const int64_t widest = c->split ? c->sp_wa + c->sp_wb : c->max_width;
+  c->auto_atomic = widest > AUTO_HUB_ENTRIES;
+  return c->auto_atomic ? SL_ACC_ATOMIC : SL_ACC_GATHER;
+}
+
 int build_layout(sl_ctx *c) {
   c->split = false;
   if (c->prec != PREC_FP64 && c->split_enabled) {
@@ -1944,15 +1957,17 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     return fail(c, SL_EINVAL, "sl_step: bad arguments");
   if (!(dt > 0) || !std::isfinite(dt))
     return fail(c, SL_EINVAL, "dt must be positive, got %g", dt);
-  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC)
+  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC &&
+      accumulation != SL_ACC_AUTO)
     return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
   if (err_slot) *err_slot = 0;
   if (steps_done) *steps_done = 0;
   if (c->async_open)
     return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
   CK(cudaSetDevice(c->device));
-  int rc = prepare(c, accumulation == SL_ACC_GATHER);
+  int rc = prepare(c, accumulation != SL_ACC_ATOMIC);
   if (rc) return rc;
+  accumulation = resolve_accumulation(c, accumulation);
   const Launch &L = launchers(c->prec);
   KState S = make_state(c);
   if ((rc = upload_state(c, S))) return rc;
@@ -2010,8 +2025,9 @@ int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
                    int64_t *counters) {
   if (!c) return fail(c, SL_EINVAL, "NULL context");
   CK(cudaSetDevice(c->device));
-  int rc = prepare(c, accumulation == SL_ACC_GATHER);
+  int rc = prepare(c, accumulation != SL_ACC_ATOMIC);
   if (rc) return rc;
+  accumulation = resolve_accumulation(c, accumulation);
   const Launch &L = launchers(c->prec);
   KState S = make_state(c);
   if ((rc = upload_state(c, S))) return rc;
@@ -2266,11 +2282,13 @@ int sl_step_async(sl_ctx *c, int64_t n_steps, const double *sim_times,
     return fail(c, SL_EINVAL, "sl_step_async: bad arguments");
   if (!(dt > 0) || !std::isfinite(dt))
     return fail(c, SL_EINVAL, "dt must be positive, got %g", dt);
-  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC)
+  if (accumulation != SL_ACC_GATHER && accumulation != SL_ACC_ATOMIC &&
+      accumulation != SL_ACC_AUTO)
     return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
   CK(cudaSetDevice(c->device));
-  int rc = prepare(c, accumulation == SL_ACC_GATHER, !c->async_open);
+  int rc = prepare(c, accumulation != SL_ACC_ATOMIC, !c->async_open);
   if (rc) return rc;
+  accumulation = resolve_accumulation(c, accumulation);
   if (!c->async_open) {
     c->async_open = true;
     c->async_steps = 0;

@@ -46,7 +46,10 @@ V_STICK = 1e-6                       # engine.py:38
 KIND_DIRECTION = 1                   # kernels.py:24-25
 KIND_PLANE = 2
 
-ACCUMULATIONS = ("linearizable", "slotted", "gather", "atomic")
+# "linearizable" / "slotted" (the reference's names) and "gather" are the
+# deterministic per-mass gather; "atomic" the per-spring atomic variant;
+# "auto" picks per mesh (gather unless hub masses, sl_api.cu)
+ACCUMULATIONS = ("linearizable", "slotted", "gather", "atomic", "auto")
 BACKENDS = ("cuda",)
 PRECISIONS = ("fp64", "fp32", "mixed")
 
@@ -81,8 +84,11 @@ class StepConfig:
 
     @property
     def native_accumulation(self) -> int:
-        return (_native.ACC_ATOMIC if self.accumulation == "atomic"
-                else _native.ACC_GATHER)
+        if self.accumulation == "atomic":
+            return _native.ACC_ATOMIC
+        if self.accumulation == "auto":
+            return _native.ACC_AUTO
+        return _native.ACC_GATHER
 
 
 # ----------------------------------------------------------- device mirror

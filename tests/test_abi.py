@@ -43,6 +43,7 @@ def test_abi_version_and_constants():
     assert int(consts["SL_ENUMERIC"]) == _native.SL_ENUMERIC
     assert int(consts["SL_ACC_GATHER"]) == _native.ACC_GATHER
     assert int(consts["SL_ACC_ATOMIC"]) == _native.ACC_ATOMIC
+    assert int(consts["SL_ACC_AUTO"]) == _native.ACC_AUTO
     for name, code in _native.PRECISIONS.items():
         key = {"fp64": "SL_PREC_FP64", "fp32": "SL_PREC_FP32",
                "mixed": "SL_PREC_MIXED"}[name]
