@@ -1003,7 +1003,7 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
 // false when a tile does not fit (the split kernel then runs).
 int build_window_layout(sl_ctx *c) {
   c->win = false;
-  if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP32 ||
+  if (!c->win_enabled || !c->tma_enabled || c->prec == PREC_FP64 ||
       c->n_slices == 0 || c->sp_wa > 64 || c->sp_wb > 64)
     return SL_OK;
   int tt = 16;  // consumer warps per CTA (r1 sweeps: the more the better)
@@ -1011,6 +1011,7 @@ int build_window_layout(sl_ctx *c) {
     const int v = atoi(ev);
     tt = v == 12 || v == 20 || v == 24 ? v : 16;
   }
+  if (c->prec == PREC_MIXED) tt = 16;  // the one mixed instantiation
   const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
   WinCfg w{};
   w.n_tiles = n_tiles;
@@ -1039,7 +1040,7 @@ int build_window_layout(sl_ctx *c) {
       c->s_grp.as<uint8_t>(), c->win_rec.as<TileRec>(),
       c->win_dict.as<float2>(), c->win_actb.as<unsigned char>(),
       c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
-      c->win_fail.as<unsigned long long>());
+      c->prec == PREC_MIXED ? 1 : 0, c->win_fail.as<unsigned long long>());
   CKL();
   unsigned long long res[2] = {0, 0};
   CK(cudaMemcpyAsync(res, c->win_fail.p, 16, cudaMemcpyDeviceToHost, c->st));
@@ -1052,7 +1053,8 @@ int build_window_layout(sl_ctx *c) {
   w.off_dict = sizeof(TileRec);
   w.off_act = w.off_dict + 8 * WIN_DMAX;
   w.off_win = w.off_act + WIN_ACTB;
-  w.off_slice = (w.off_win + 16 * w.cap_rec + 127) / 128 * 128;
+  w.off_slice =
+      (w.off_win + (uint32_t)(4 * c->rsz) * w.cap_rec + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
   const int64_t bar = 8 * 2 * WIN_MAXST + 8 * WIN_MAXST * WIN_DMAX;
   int nst = (int)std::min<int64_t>(

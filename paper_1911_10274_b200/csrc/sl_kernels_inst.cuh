@@ -52,10 +52,10 @@ struct SplitLaunch {
         else tma_u<8, false>(S, E, T, C, A, grid, st);
     }
   }
-  // tiled window kernel (fp32 only)
+  // tiled window kernel (fp32 and mixed)
   static void win(const KState &S, const EnvP &E, const StepP &T,
                   const WinCfg &C, int grid, cudaStream_t st) {
-    if constexpr (P == PREC_FP32) {
+    {
       const size_t sm = win_smem(C);
       win_dispatch(C.tile_slices, [&](auto kern) {
         kern<<<grid, (C.tile_slices + 1) * 32, sm, st>>>(S, E, T, C);
@@ -68,7 +68,9 @@ struct SplitLaunch {
   // call f(kernel) for the instantiation of T
   template <class Fn>
   static void win_dispatch(int tt, Fn f) {
-    if constexpr (P == PREC_FP32) {
+    if constexpr (P == PREC_MIXED) {  // fp64 windows: T = 16 only
+      f(k_win_tma<P, 16>);
+    } else {
       switch (tt) {
         case 12: f(k_win_tma<P, 12>); return;
         case 20: f(k_win_tma<P, 20>); return;
@@ -93,8 +95,7 @@ struct SplitLaunch {
   }
   static int win_setup(const WinCfg &C) {
     int rc = 1;
-    if constexpr (P == PREC_FP32)
-      win_dispatch(C.tile_slices, [&](auto kern) {
+    win_dispatch(C.tile_slices, [&](auto kern) {
         rc = (int)cudaFuncSetAttribute(
             kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
             (int)win_smem(C));

@@ -215,3 +215,23 @@ def test_window_param_edits_match_oracle():
         ref.step(float(times[n]), dt)
     assert rel_maxnorm(pos, ref.c["m_pos"]) < 1e-4
     assert rel_maxnorm(vel, ref.c["m_vel"]) < 1e-3
+
+
+@pytest.mark.parametrize("name", ["cube10_drop", "cube10_contact",
+                                  "lat3_contact_drag", "constraints_contacts",
+                                  "topology_edits"])
+def test_window_mixed_matches_split_kernel(name):
+    """precision="mixed" (fp64 state and force arithmetic, fp32 (k, L0)):
+    the window kernel's fp64 windows and (k, L0) material table give the
+    split kernel's forces to fp64 rounding -- the 1e-9 bar of the mixed
+    mode's split-vs-exact test (test_gpu_split.py)."""
+    g = load_golden(name)
+    n = min(100, int(g["n_steps"]))
+    t, dt = case_times(g)[:n], float(g["dt"])
+    w = _run(g, t, dt, True, precision="mixed")
+    s = _run(g, t, dt, False, precision="mixed")
+    assert w["path"] == PATH_WINDOW_TMA and s["path"] == PATH_SPLIT_TMA
+    assert np.array_equal(w["alive"], s["alive"])
+    assert w["c"].tolist() == s["c"].tolist()
+    assert rel_maxnorm(w["pos"], s["pos"]) < 1e-9
+    assert rel_maxnorm(w["vel"], s["vel"]) < 1e-6
