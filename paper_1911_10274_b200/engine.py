@@ -159,6 +159,7 @@ class DeviceMirror:
     # device -> host
     def pull(self, store: ObjectStore, springs: bool = True,
              acc: bool = True, fext: bool = True):
+        store.materialize_sync()
         m, s = store.mass_slot_count, store.spring_slot_count
         self.ctx.download_masses(store._m_pos[:m], store._m_vel[:m],
                                  store._m_acc[:m] if acc else None,
