@@ -156,6 +156,18 @@ int sl_write_spring_params(sl_ctx *ctx, int64_t n, const int64_t *slots,
                            const double *freq, const double *off,
                            const double *per);
 /* Kill spring slots (delete_spring / reconcile, store.py:440-473). O(n). */
+/* Whole spring records for the given slots (< the current spring count):
+ * spring creations into reused slots at a pause (store.py:356-370).  Only
+ * the touched slots cross the bus; the incidence layout is re-indexed on
+ * the device at the next step. */
+int sl_write_springs(sl_ctx *ctx, int64_t n, const int64_t *slots,
+                     const int64_t *m1, const int64_t *m2,
+                     const int64_t *m1gen, const int64_t *m2gen,
+                     const double *rest, const double *k, const double *diam,
+                     const double *yield, const int8_t *mode,
+                     const double *amp, const double *freq, const double *off,
+                     const double *per, const uint8_t *alive,
+                     const uint8_t *degen);
 int sl_kill_springs(sl_ctx *ctx, int64_t n, const int64_t *slots);
 
 /* -------------------------------------------------------------------- step */

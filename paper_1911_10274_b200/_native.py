@@ -28,7 +28,8 @@ EXPORTS = (
     "sl_abi_version", "sl_device_count", "sl_create", "sl_destroy",
     "sl_last_error", "sl_get_stats", "sl_upload_masses", "sl_upload_springs",
     "sl_set_environment", "sl_set_local_constraints", "sl_set_custom_factors",
-    "sl_write_masses", "sl_write_spring_params", "sl_kill_springs", "sl_step",
+    "sl_write_masses", "sl_write_spring_params", "sl_write_springs",
+    "sl_kill_springs", "sl_step",
     "sl_spring_pass", "sl_mass_pass", "sl_download_masses",
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
@@ -81,6 +82,7 @@ def load_library(path: str = LIB_PATH):
             "sl_write_masses": ([P, I64] + [P] * 10, I),
             "sl_write_spring_params": ([P, I64] + [P] * 10, I),
             "sl_kill_springs": ([P, I64, P], I),
+            "sl_write_springs": ([P, I64, P] + [P] * 15, I),
             "sl_step": ([P, I64, P, D, I, P, P, P], I),
             "sl_spring_pass": ([P, D, I, P], I),
             "sl_mass_pass": ([P, D, P], I),
@@ -257,6 +259,18 @@ class Context:
                                              _ptr(lengths), _ptr(fmag)),
                     "sl_spring_loads")
         return lengths, fmag
+
+    def write_springs(self, slots, m1, m2, m1gen, m2gen, rest, k, diam, yld,
+                      mode, amp, freq, off, per, alive, degen):
+        s = _c(slots, np.int64)
+        a = [_c(m1, np.int64), _c(m2, np.int64), _c(m1gen, np.int64),
+             _c(m2gen, np.int64), _c(rest, np.float64), _c(k, np.float64),
+             _c(diam, np.float64), _c(yld, np.float64), _c(mode, np.int8),
+             _c(amp, np.float64), _c(freq, np.float64), _c(off, np.float64),
+             _c(per, np.float64), _c(alive, np.uint8), _c(degen, np.uint8)]
+        self._check(self.lib.sl_write_springs(self.h, len(s), _ptr(s),
+                                              *map(_ptr, a)),
+                    "sl_write_springs")
 
     def kill_springs(self, slots):
         s = _c(slots, np.int64)

@@ -1664,7 +1664,7 @@ static int upload_springs_impl(sl_ctx *c, int64_t n, const int64_t *slots,
   // the table is full (the spring then takes the exact path).  The mixed
   // mode keeps actuated springs on the exact path: its fp64 sin holds the
   // 1e-9 split-vs-exact bar that the fast path's fp32 sin cannot.
-  if (!params_only) {
+  if (!params_only && !slots) {  // a full upload: groups from scratch
     memset(&c->agrp, 0, sizeof c->agrp);
     c->agrp.n = 1;
     c->agrp.per[0] = 1.0;
@@ -1773,6 +1773,31 @@ int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
   c->springs_set = true;
   c->validate_dirty = true;
   return SL_OK;
+}
+
+int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
+                     const int64_t *m1, const int64_t *m2,
+                     const int64_t *m1gen, const int64_t *m2gen,
+                     const double *rest, const double *k, const double *diam,
+                     const double *yield, const int8_t *mode,
+                     const double *amp, const double *freq, const double *off,
+                     const double *per, const uint8_t *alive,
+                     const uint8_t *degen) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (n < 0 || (n > 0 && (!slots || !m1 || !m2 || !m1gen || !m2gen ||
+                          !rest || !k || !diam || !yield || !mode || !amp ||
+                          !freq || !off || !per || !alive || !degen)))
+    return fail(c, SL_EINVAL, "sl_write_springs: bad arguments");
+  for (int64_t r = 0; r < n; r++)
+    if (slots[r] < 0 || slots[r] >= c->s_n)
+      return fail(c, SL_EINVAL, "spring slot %lld out of range",
+                  (long long)slots[r]);
+  if (n == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  c->layout_valid = false;  // re-indexed on the device at the next step
+  return upload_springs_impl(c, n, slots, m1, m2, m1gen, m2gen, rest, k,
+                             diam, yield, mode, amp, freq, off, per, alive,
+                             degen, false);
 }
 
 int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,

@@ -117,7 +117,9 @@ class DeviceMirror:
                 store._m_fixed[:m], store._m_alive[:m], store._m_gen[:m])
         key = (s, m, store.topology_version, store.spring_param_version,
                id(store._s_m1))
-        if key != self._springs_key:
+        if key != self._springs_key and self._replay_springs(store, key):
+            pass
+        elif key != self._springs_key:
             self.ctx.upload_springs(
                 store._s_m1[:s], store._s_m2[:s], store._s_m1gen[:s],
                 store._s_m2gen[:s], store._s_rest[:s], store._s_k[:s],
@@ -126,6 +128,8 @@ class DeviceMirror:
                 store._s_act_off[:s], store._s_act_per[:s],
                 store._s_alive[:s], store._s_degen[:s])
             self._springs_key = key
+            self._journal_at = (store._s_journal_epoch,
+                                len(store._s_journal))
             self._custom_slots = np.array(
                 sorted(k for k in store._s_custom if k < s), dtype=np.int64)
         ckey = (m, store.constraint_version, id(store._m_pos))
@@ -134,6 +138,45 @@ class DeviceMirror:
             self.ctx.set_local_constraints(lc_off, lc_kind, lc_vec)
             self._constraints_key = ckey
         self.set_env(store, env or Environment())
+
+    def _replay_springs(self, store: ObjectStore, key) -> bool:
+        """O(edits) spring sync: replay the store's spring journal since the
+        last push -- deleted slots become device kills (in place), touched
+        live slots whole-record writes (re-indexed on the device) -- when
+        the spring arrays are the same allocation and the edit set is small.
+        False: the caller uploads everything."""
+        old = self._springs_key
+        if old is None or old[0] != key[0] or old[1] != key[1] or \
+                old[4] != key[4]:
+            return False
+        epoch, at = getattr(self, "_journal_at", (None, 0))
+        if epoch != store._s_journal_epoch or at > len(store._s_journal):
+            return False
+        pending = store._s_journal[at:]
+        if not pending:
+            return False
+        slots = np.unique(np.concatenate(pending))
+        if len(slots) > max(1024, key[0] // 64):
+            return False
+        alive = store._s_alive[slots].astype(bool)
+        dead, live = slots[~alive], slots[alive]
+        if len(dead):
+            self.ctx.kill_springs(dead)
+        if len(live):
+            self.ctx.write_springs(
+                live, store._s_m1[live], store._s_m2[live],
+                store._s_m1gen[live], store._s_m2gen[live],
+                store._s_rest[live], store._s_k[live], store._s_diam[live],
+                store._s_yield[live], store._s_act_mode[live],
+                store._s_act_amp[live], store._s_act_freq[live],
+                store._s_act_off[live], store._s_act_per[live],
+                store._s_alive[live], store._s_degen[live])
+        self._springs_key = key
+        self._journal_at = (store._s_journal_epoch, len(store._s_journal))
+        self._custom_slots = np.array(
+            sorted(k for k in store._s_custom if k < key[0]), dtype=np.int64)
+        self.replays = getattr(self, "replays", 0) + 1
+        return True
 
     def set_env(self, store: ObjectStore, env: Environment):
         planes, balls = flatten_contacts(env)
