@@ -83,6 +83,7 @@ typedef struct sl_stats {
 #define SL_PATH_SPLIT 3       /* split layout, one thread per mass          */
 #define SL_PATH_SPLIT_TMA 4   /* split layout, TMA-pipelined (k_split_tma)  */
 #define SL_PATH_WINDOW_TMA 5  /* split layout, tiled windows (k_win_tma)     */
+#define SL_PATH_EXACT_WINDOW 6 /* exact layout, tiled windows (fp64 k_win_tma) */
 
 /* ---------------------------------------------------------------- lifecycle */
 int sl_abi_version(void);

@@ -48,7 +48,8 @@ class SlStats(C.Structure):
                 ("fused_aborts", C.c_int64)]
 
 STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
-              3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma"}
+              3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma",
+              6: "k_win_tma (exact)"}
 
 
 _lib = None

@@ -1079,6 +1079,68 @@ int build_window_layout(sl_ctx *c) {
   return SL_OK;
 }
 
+// The window layout over the exact layout (fp64 parity mode): T = 12
+// tiles, fp64 windows, exact (k, L0) tables, entries in ascending slot
+// order (k_win64_build).  c->win stays false when a tile does not fit.
+int build_window_exact(sl_ctx *c) {
+  c->win = false;
+  if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP64 ||
+      c->n_slices == 0 || c->max_width == 0 || c->max_width > 64)
+    return SL_OK;
+  const int tt = 12;
+  const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
+  WinCfg w{};
+  w.n_tiles = n_tiles;
+  w.tile_slices = tt;
+  w.cap_a = (int)c->max_width;
+  w.cap_b = 0;
+  auto al16 = [](uint32_t x) { return (x + 15) / 16 * 16; };
+  w.bl.off_acode = al16((uint32_t)w.cap_a * 64);
+  w.bl.off_b16 = w.bl.off_bcode = al16(w.bl.off_acode + (uint32_t)w.cap_a * 32);
+  w.bl.slice_bytes = w.bl.off_bcode;
+  CK(c->win_rec.ensure(sizeof(TileRec) * n_tiles));
+  CK(c->win_dict.ensure(16 * WIN_DMAX * n_tiles));
+  CK(c->win_blk.ensure((size_t)w.bl.slice_bytes * n_tiles * tt));
+  CK(c->win_fail.ensure(16));
+  CK(cudaMemsetAsync(c->win_fail.p, 0, 16, c->st));
+  const int64_t m_pad = c->n_slices * 32;
+  KState S = make_state(c);
+  k_win64_build<<<(unsigned)n_tiles, 256, 0, c->st>>>(
+      S.slice_ptr, c->ent_j.as<uint32_t>(), c->ent_kL0.as<double2>(),
+      c->n_slices, c->m_n, (uint32_t)m_pad, tt, w.bl, w.cap_a,
+      c->win_rec.as<TileRec>(), c->win_dict.as<double2>(),
+      c->win_blk.as<unsigned char>(), c->win_fail.as<unsigned long long>());
+  CKL();
+  unsigned long long res[2] = {0, 0};
+  CK(cudaMemcpyAsync(res, c->win_fail.p, 16, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  c->launches++;
+  if (res[0]) return SL_OK;
+  w.cap_rec = (uint32_t)((res[1] + 7) / 8 * 8);
+  w.off_dict = sizeof(TileRec);
+  w.off_act = w.off_dict + 16 * WIN_DMAX;
+  w.off_win = w.off_act;  // no actuation block in parity mode
+  w.off_slice = (w.off_win + 32 * w.cap_rec + 127) / 128 * 128;
+  w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
+  const int64_t bar = 8 * 2 * WIN_MAXST + 16 * WIN_MAXST * WIN_DMAX;
+  int nst = (int)std::min<int64_t>(
+      WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
+  if (nst < 2) return SL_OK;
+  w.nst = nst;
+  w.off_eff = (uint32_t)nst * w.stage_bytes;
+  w.rec = c->win_rec.as<TileRec>();
+  w.dict = c->win_dict.as<float2>();  // double2 entries (parity mode)
+  w.blk = c->win_blk.as<unsigned char>();
+  if (launchers(c->prec).win_setup(w) != 0) {
+    cudaGetLastError();
+    return SL_OK;
+  }
+  c->wcfg = w;
+  c->win_grid = (int)std::min<int64_t>(n_tiles, c->sm_count);
+  c->win = true;
+  return SL_OK;
+}
+
 // Groups of whole connected components for the multi-step fused kernel
 // (sl_fused.cuh); c->fz_ok stays false when the context is not eligible.
 int build_fused_groups(sl_ctx *c) {
@@ -1380,7 +1442,9 @@ int build_layout(sl_ctx *c) {
     if (rc || used) return rc;
     c->split = false;
   }
-  return build_exact_layout(c);
+  c->win = false;
+  if (int rc = build_exact_layout(c)) return rc;
+  return build_window_exact(c);
 }
 
 int prepare(sl_ctx *c, bool need_layout, bool reset_status = true) {
@@ -1548,6 +1612,7 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
                  : c->split       ? (c->win           ? SL_PATH_WINDOW_TMA
                                      : c->split_warps ? SL_PATH_SPLIT_TMA
                                                       : SL_PATH_SPLIT)
+                 : c->win         ? SL_PATH_EXACT_WINDOW
                  : (c->tma_warps ? SL_PATH_EXACT_TMA : SL_PATH_EXACT);
   o->split_batch = c->split && c->split_warps ? c->scfg.u : 0;
   o->fused_groups = c->fz_ok ? c->fcfg.n_groups : 0;
@@ -1836,6 +1901,8 @@ int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
   k_kill_springs<<<blocks_for(n), 256, 0, c->st>>>(n, ds, S, c->layout_valid);
   CKL();
   c->launches++;
+  // the parity-mode window blocks are not edited in place: re-index
+  if (c->win && !c->split) c->layout_valid = false;
   CK(cudaStreamSynchronize(c->st));
   return SL_OK;
 }
@@ -2023,6 +2090,8 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
           L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
           L.split(S, c->env, T, c->agrp, c->st);
+      } else if (c->win) {
+        L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);
       } else if (c->tma_warps) {
         L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
       } else {
@@ -2286,6 +2355,8 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
           L.split_tma(S, c->env, T, c->scfg, c->agrp, c->split_grid, c->st);
         else
           L.split(S, c->env, T, c->agrp, c->st);
+      } else if (c->win) {
+        L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);
       } else if (c->tma_warps) {
         L.gather_tma(S, c->env, T, c->tma, c->tma_grid, c->st);
       } else {

@@ -10,6 +10,23 @@
 
 
 namespace sl {
+// Opt a kernel into dynamic shared memory: always to the device maximum, so
+// contexts of different layouts on one device (partition shards) never
+// shrink the limit under one another's launch; `need` is only checked.
+template <class K>
+inline int smem_optin(K kern, size_t need) {
+  int dev = 0, most = 0;
+  cudaFuncAttributes fa;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&most, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                             dev) != cudaSuccess ||
+      cudaFuncGetAttributes(&fa, kern) != cudaSuccess)
+    return 1;
+  most -= (int)fa.sharedSizeBytes;  // the kernel's static shared memory
+  if (need > (size_t)most) return 1;
+  return (int)cudaFuncSetAttribute(
+      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+}
 // split-layout launchers; the fp64 parity mode never uses the split layout
 template <int P>
 struct SplitLaunch {
@@ -88,25 +105,19 @@ struct SplitLaunch {
   }
   static int fused_setup(size_t smem) {
     if constexpr (P == PREC_FP32)
-      return (int)cudaFuncSetAttribute(
-          k_fused_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          (int)smem);
+      return smem_optin(k_fused_small<P>, smem);
     return 1;
   }
   static int win_setup(const WinCfg &C) {
     int rc = 1;
     win_dispatch(C.tile_slices, [&](auto kern) {
-        rc = (int)cudaFuncSetAttribute(
-            kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            (int)win_smem(C));
+        rc = smem_optin(kern, win_smem(C));
       });
     return rc;
   }
   template <int U, bool ACT>
   static int setup_u(int smem_bytes) {
-    return (int)cudaFuncSetAttribute(
-        k_split_tma<P, U, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-        smem_bytes);
+    return smem_optin(k_split_tma<P, U, ACT>, (size_t)smem_bytes);
   }
   static int setup(int smem_bytes, int u, int act) {
     if (act) return u == 4 ? setup_u<4, true>(smem_bytes)
@@ -127,9 +138,18 @@ struct SplitLaunch<PREC_FP64> {
   static void tma(const KState &, const EnvP &, const StepP &,
                   const SplitCfg &, const ActP &, int, cudaStream_t) {}
   static int setup(int, int, int) { return 1; }
-  static void win(const KState &, const EnvP &, const StepP &,
-                  const WinCfg &, int, cudaStream_t) {}
-  static int win_setup(const WinCfg &) { return 1; }
+  // the window kernel over the exact layout (parity mode; this unit is
+  // compiled with -fmad=false)
+  static size_t win_smem(const WinCfg &C) {  // eff tables: double2 slots
+    return (size_t)C.off_eff + WIN_MAXST * WIN_DMAX * 16 + 8 * 2 * WIN_MAXST;
+  }
+  static void win(const KState &S, const EnvP &E, const StepP &T,
+                  const WinCfg &C, int grid, cudaStream_t st) {
+    k_win_tma<PREC_FP64, 12><<<grid, 13 * 32, win_smem(C), st>>>(S, E, T, C);
+  }
+  static int win_setup(const WinCfg &C) {
+    return smem_optin(k_win_tma<PREC_FP64, 12>, win_smem(C));
+  }
   static void fused(const KState &, const EnvP &, const FzCfg &, double,
                     size_t, cudaStream_t) {}
   static int fused_setup(size_t) { return 1; }
@@ -149,9 +169,7 @@ struct SplitLaunch<PREC_FP64> {
     k_gather_tma<PREC><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);          \
   }                                                                          \
   int FN##_tma_setup(int smem_bytes) {                                       \
-    return (int)cudaFuncSetAttribute(k_gather_tma<PREC>,                     \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     smem_bytes);                            \
+    return smem_optin(k_gather_tma<PREC>, (size_t)smem_bytes);               \
   }                                                                          \
   void FN##_force(const KState &S, const EnvP &E, const StepP &T,            \
                   cudaStream_t st) {                                         \

@@ -235,3 +235,27 @@ def test_window_mixed_matches_split_kernel(name):
     assert w["c"].tolist() == s["c"].tolist()
     assert rel_maxnorm(w["pos"], s["pos"]) < 1e-9
     assert rel_maxnorm(w["vel"], s["vel"]) < 1e-6
+
+
+def test_window_exact_fp64_bitwise_equals_exact_kernel():
+    """fp64 parity mode on the window layout over the EXACT layout (entries
+    in ascending slot order, exact (k, L0) tables, IEEE sqrt / divide):
+    bit-identical to the exact TMA kernel (SL_DISABLE_WIN=1) and to the
+    oracle, including after kills between launches."""
+    case = _lattice_case(20, 17, 9)
+    dt, n = 1e-4, 50
+    times = np.arange(n, dtype=np.float64) * dt
+    rng = np.random.default_rng(6)
+    kill = np.sort(rng.choice(len(case["s_m1"]), 200, replace=False))
+    w = _run(case, times, dt, True, precision="fp64", kill=kill, kill_at=20)
+    x = _run(case, times, dt, False, precision="fp64", kill=kill, kill_at=20)
+    assert w["path"] == 6 and x["path"] == 2
+    assert w["pos"].tobytes() == x["pos"].tobytes()
+    assert w["vel"].tobytes() == x["vel"].tobytes()
+    ref = orc.OracleSim(case)
+    for k in range(n):
+        if k == 20:
+            ref.c["s_alive"][kill] = 0
+        ref.step(float(times[k]), dt)
+    assert w["pos"].tobytes() == ref.c["m_pos"].tobytes()
+    assert w["vel"].tobytes() == ref.c["m_vel"].tobytes()
