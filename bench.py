@@ -340,7 +340,8 @@ def main():
         return t
 
     mir.ctx.step(times(max(3, args.warmup)), dt, acc, counters)  # warm-up
-    launches0 = mir.ctx.stats()["kernel_launches"]
+    st0 = mir.ctx.stats()
+    launches0, fused0 = st0["kernel_launches"], st0["fused_launches"]
     if dist is not None:
         dist.barrier()
     mir.ctx.sync()
@@ -354,8 +355,10 @@ def main():
     from paper_1911_10274_b200._native import STEP_PATHS
     kernel = (STEP_PATHS.get(stats["step_path"], "?")
               if args.accumulation == "gather" else "k_spring_atomic+k_mass")
-    if stats.get("split_batch"):
+    if stats["step_path"] == 4 and stats.get("split_batch"):
         kernel += f" (U={stats['split_batch']})"
+    if stats.get("fused_launches", 0) > fused0:
+        kernel = "k_fused_small (all steps in one launch)"
     if err:
         raise SystemExit(f"numerical abort at step {done}")
     sec = ms / 1e3
