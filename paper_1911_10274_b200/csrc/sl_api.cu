@@ -53,7 +53,12 @@ struct DevBuf {
     bytes = 0;
     if (want == 0) want = 16;
     cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) bytes = want;
+    if (e == cudaSuccess) {
+      bytes = want;
+      // debug: fill fresh buffers with a pattern (finds uninitialised reads)
+      static const char *poison = getenv("SL_POISON");
+      if (poison) e = cudaMemset(p, (int)strtol(poison, nullptr, 0), want);
+    }
     return e;
   }
   void release() {

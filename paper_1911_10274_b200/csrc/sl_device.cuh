@@ -801,7 +801,7 @@ __device__ __forceinline__ void initial_force(const KState &S, int64_t i,
 // from global memory.  Used for spring_pass (FORCE_ONLY), for tiny bodies
 // and for layouts with very wide slices (hub masses).
 template <int P, bool FORCE_ONLY>
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_gather_step(const KState S, const EnvP E, const StepP T) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
@@ -928,7 +928,7 @@ struct TmaCfg {
 // arrives through four bulk copies on one mbarrier, so the only exposed
 // latency left in the loop is the L2 gather of neighbour positions.
 template <int P>
-__global__ void __launch_bounds__(384)
+static __global__ void __launch_bounds__(384)
     k_gather_tma(const KState S, const EnvP E, const StepP T,
                  const TmaCfg C) {
   using R = typename Tr<P>::R;
@@ -1076,7 +1076,7 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
 // Atomic variant, spring side: one thread per spring slot (kernels.py:36-83
 // with the accumulation of the paper's GPU design).
 template <int P, bool SPECIAL>
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_spring_atomic(const KState S, const StepP T) {
   using R = typename Tr<P>::R;
   using F = typename Tr<P>::M;
@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(256)
 
 // Standalone mass pass (engine.mass_pass; second half of the atomic step).
 template <int P>
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_mass(const KState S, const EnvP E, const StepP T) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;

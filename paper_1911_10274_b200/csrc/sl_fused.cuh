@@ -159,7 +159,7 @@ static __global__ void __launch_bounds__(FZ_MAXM)
 //   static table (3 x WIN_DMAX float2) | raw (k, L0) (WIN_DMAX float2) |
 //   entries (rows x FZ_MAXM u32: partner | code << 16) | modes
 template <int P>
-__global__ void __launch_bounds__(FZ_MAXM, 2)
+static __global__ void __launch_bounds__(FZ_MAXM, 2)
     k_fused_small(const KState S, const EnvP E, const FzCfg C, double dt) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
@@ -167,8 +167,11 @@ __global__ void __launch_bounds__(FZ_MAXM, 2)
   extern __shared__ __align__(16) unsigned char smem[];
   const int rows = C.ra + C.rb;
   double4 *sact = (double4 *)smem;
-  R4 *spos = (R4 *)(sact + WIN_DMAX);
-  F2 *stab = (F2 *)(spos + 2 * (FZ_MAXM + 1));  // [3][WIN_DMAX]
+  // positions as xy pairs + z (the partner's mass is never read): one
+  // 8 B + one 4 B shared load per entry, 3 wavefronts instead of 4
+  float2 *sxy = (float2 *)(sact + WIN_DMAX);       // [2][FZ_MAXM + 1]
+  float *sz = (float *)(sxy + 2 * (FZ_MAXM + 1));  // [2][FZ_MAXM + 1]
+  F2 *stab = (F2 *)(sz + 2 * (FZ_MAXM + 1) + 2 * (FZ_MAXM + 1));  // [3][..]
   F2 *skl = stab + 3 * WIN_DMAX;
   // entries packed as partner | code << 16: one shared load per entry
   uint32_t *sen = (uint32_t *)(skl + WIN_DMAX);
@@ -192,13 +195,14 @@ __global__ void __launch_bounds__(FZ_MAXM, 2)
     me.w = (R)1;
     v.x = v.y = v.z = v.w = (R)0;
   }
-  spos[li] = me;
+  sxy[li] = make_float2(me.x, me.y);
+  sz[li] = me.z;
   if (li == 0) {
     R4 far;
     far.x = far.y = far.z = (R)SENTINEL_POS;
     far.w = (R)0;
-    spos[FZ_MAXM] = far;
-    spos[2 * FZ_MAXM + 1] = far;
+    sxy[FZ_MAXM] = sxy[2 * FZ_MAXM + 1] = make_float2(far.x, far.y);
+    sz[FZ_MAXM] = sz[2 * FZ_MAXM + 1] = far.z;
     sbad = 0;
   }
   for (int q = 0; q < rows; q++) {
@@ -248,8 +252,12 @@ __global__ void __launch_bounds__(FZ_MAXM, 2)
   for (; k < C.n_steps; k++) {
     const int b = (int)(k & 1);
     const F2 *tab = act ? stab + b * WIN_DMAX : stab + 2 * WIN_DMAX;
-    const R4 *pin = spos + b * (FZ_MAXM + 1);
-    R4 *pout = spos + (b ^ 1) * (FZ_MAXM + 1);
+    const float2 *pxy = sxy + b * (FZ_MAXM + 1);
+    const float *pz = sz + b * (FZ_MAXM + 1);
+    auto pin = [&](uint32_t p) {
+      const float2 xy = pxy[p];
+      return make_float4(xy.x, xy.y, pz[p], 0.f);
+    };
     R4 np = me;
     if (live) {
       if (fl & MF_FIXED) {  // kernels.py:260-270
@@ -261,12 +269,12 @@ __global__ void __launch_bounds__(FZ_MAXM, 2)
 #pragma unroll 4
         for (int q = 0; q < C.ra; q++) {
           const uint32_t w = e[q * FZ_MAXM];
-          win_body(me, pin[w & 0xFFFFu], tab[w >> 16], gx, gy, gz);
+          win_body(me, pin(w & 0xFFFFu), tab[w >> 16], gx, gy, gz);
         }
 #pragma unroll 4
         for (int q = C.ra; q < rows; q++) {
           const uint32_t w = e[q * FZ_MAXM];
-          win_body(me, pin[w & 0xFFFFu], tab[w >> 16], bx, by, bz);
+          win_body(me, pin(w & 0xFFFFu), tab[w >> 16], bx, by, bz);
         }
         const R fx = f0x + (gx + bx), fy = f0y + (gy + by),
                 fz = f0z + (gz + bz);
@@ -280,7 +288,8 @@ __global__ void __launch_bounds__(FZ_MAXM, 2)
         if (!(z0 == (R)0)) sbad = 1;  // zero-length spring or blow-up
       }
     }
-    pout[li] = np;
+    sxy[(b ^ 1) * (FZ_MAXM + 1) + li] = make_float2(np.x, np.y);
+    sz[(b ^ 1) * (FZ_MAXM + 1) + li] = np.z;
     me = np;
     eff_table(k + 1);  // the other buffer: nobody reads it this step
     __syncthreads();

@@ -143,6 +143,10 @@ struct SplitLaunch<PREC_FP64> {
   static size_t win_smem(const WinCfg &C) {  // eff tables: double2 slots
     return (size_t)C.off_eff + WIN_MAXST * WIN_DMAX * 16 + 8 * 2 * WIN_MAXST;
   }
+  // Only the -fmad=false unit instantiates the fp64 kernel: a copy
+  // compiled with FMA contraction in another unit could be the one a launch
+  // binds to (tests/test_abi.py checks each cubin's instantiations).
+#ifdef SL_UNIT_FP64
   static void win(const KState &S, const EnvP &E, const StepP &T,
                   const WinCfg &C, int grid, cudaStream_t st) {
     k_win_tma<PREC_FP64, 12><<<grid, 13 * 32, win_smem(C), st>>>(S, E, T, C);
@@ -150,6 +154,11 @@ struct SplitLaunch<PREC_FP64> {
   static int win_setup(const WinCfg &C) {
     return smem_optin(k_win_tma<PREC_FP64, 12>, win_smem(C));
   }
+#else
+  static void win(const KState &, const EnvP &, const StepP &,
+                  const WinCfg &, int, cudaStream_t) {}
+  static int win_setup(const WinCfg &) { return 1; }
+#endif
   static void fused(const KState &, const EnvP &, const FzCfg &, double,
                     size_t, cudaStream_t) {}
   static int fused_setup(size_t) { return 1; }

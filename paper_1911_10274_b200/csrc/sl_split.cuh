@@ -412,7 +412,7 @@ __device__ __forceinline__ void split_forces(
 // Plain variant: one thread per mass, entries read from global memory.
 // Serves spring_pass (FORCE_ONLY) and layouts too wide for the TMA stages.
 template <int P, bool FORCE_ONLY, bool ACT>
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
     k_split_step(const KState S, const EnvP E, const StepP T, const ActP A) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(256)
 // B words, A (k, L0): five bulk async copies on one mbarrier) while the warp
 // computes the current one.
 template <int P, int U, bool ACT>
-__global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
+static __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
     k_split_tma(const KState S, const EnvP E, const StepP T,
                 const SplitCfg C, const ActP A) {
   using R = typename Tr<P>::R;

@@ -73,3 +73,31 @@ def test_bad_arguments_rejected_before_any_device_work():
     assert lib.sl_create(0, 9, C.byref(h)) == _native.SL_EINVAL
     assert lib.sl_step(None, 1, None, 1e-4, 0, None, None, None) == \
         _native.SL_EINVAL
+
+
+def test_fp64_kernels_only_in_the_strict_unit(tmp_path):
+    """Every fp64 (P = 0) kernel instantiation lives in the -fmad=false
+    unit only.  A copy compiled with FMA contraction in another unit (the
+    fp32 unit once instantiated k_win_tma<fp64> through an inline launcher)
+    can be the one a launch binds to once that module is loaded, which
+    broke fp64 bit-exactness after an fp32 context had run."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    subprocess.run([tool, "-xelf", "all", _native.LIB_PATH], cwd=tmp_path,
+                   check=True, capture_output=True)
+    cubins = sorted(p for p in os.listdir(tmp_path) if p.endswith(".cubin"))
+    assert any("sl_kernels_fp64" in p for p in cubins)
+    for p in cubins:
+        out = subprocess.run([tool, "-symbols", str(tmp_path / p)],
+                             check=True, capture_output=True, text=True)
+        fp64 = [ln.split()[-1] for ln in out.stdout.splitlines()
+                if "FUNC" in ln and re.search(r"_ZN2sl\d+k_\w+ILi0E",
+                                              ln.split()[-1])
+                and "$" not in ln.split()[-1]]
+        if "sl_kernels_fp64" in p:
+            assert any("k_win_tma" in s for s in fp64)
+        else:
+            assert fp64 == [], (p, fp64)
