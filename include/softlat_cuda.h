@@ -93,6 +93,12 @@ int sl_create(int device, int precision, sl_ctx **out);
 int sl_destroy(sl_ctx *ctx);
 const char *sl_last_error(const sl_ctx *ctx); /* ctx may be NULL */
 int sl_get_stats(sl_ctx *ctx, sl_stats *out);
+/* Page-locked host memory (cudaHostAlloc, portable) for the store's mass
+ * columns: uploads and downloads from it run at copy-engine speed.  The
+ * reference's arrays are plain numpy (store.py:123-151); the host side moves
+ * the mass columns into such buffers on first push (engine.DeviceMirror). */
+int sl_host_alloc(size_t bytes, void **out);
+int sl_host_free(void *p);
 
 /* ------------------------------------------------------------------ upload */
 /* Whole mass SoA, slots [0, m_n) (store.py:123-132; mass-pass arguments of

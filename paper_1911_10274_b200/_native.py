@@ -34,7 +34,8 @@ EXPORTS = (
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
-    "sl_get_stream", "sl_energy", "sl_spring_loads")
+    "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
+    "sl_host_free")
 
 
 class SlStats(C.Structure):
@@ -102,6 +103,8 @@ def load_library(path: str = LIB_PATH):
             "sl_get_stream": ([P, P], I),
             "sl_energy": ([P, D, P, P], I),
             "sl_spring_loads": ([P, D, P, P], I),
+            "sl_host_alloc": ([C.c_size_t, P], I),
+            "sl_host_free": ([P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -126,6 +129,42 @@ def device_count() -> int:
     n = C.c_int(0)
     rc = lib.sl_device_count(C.byref(n))
     return int(n.value) if rc == SL_OK else 0
+
+
+class _PinnedBlock:
+    """Owner of one sl_host_alloc buffer; freed when the last numpy array
+    viewing it is collected (the arrays keep it alive through .base)."""
+
+    def __init__(self, nbytes: int):
+        lib = load_library()
+        p = C.c_void_p()
+        if lib.sl_host_alloc(max(1, nbytes), C.byref(p)) != SL_OK:
+            raise SoftlatError("sl_host_alloc: " +
+                               (lib.sl_last_error(None) or b"").decode())
+        self._lib, self.ptr, self.nbytes = lib, p.value, nbytes
+        self.__array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "version": 3,
+            "data": (p.value, False)}
+
+    def __del__(self):
+        if self.ptr:
+            self._lib.sl_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (sl_host_alloc)."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+    raw = np.asarray(_PinnedBlock(n))
+    return raw[:n].view(dt).reshape(shape)
+
+
+def is_pinned(a: np.ndarray) -> bool:
+    base = a
+    while isinstance(base, np.ndarray) and base.base is not None:
+        base = base.base
+    return isinstance(base, _PinnedBlock)
 
 
 class Context:

@@ -1514,6 +1514,28 @@ int sl_device_count(int *count) {
   return SL_OK;
 }
 
+int sl_host_alloc(size_t bytes, void **out) {
+  sl_ctx *c = nullptr;
+  if (!out) return fail(c, SL_EINVAL, "out is NULL");
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    *out = nullptr;
+    return fail(c, SL_ECUDA, "cudaHostAlloc(%zu): %s", bytes,
+                cudaGetErrorString(e));
+  }
+  return SL_OK;
+}
+
+int sl_host_free(void *p) {
+  sl_ctx *c = nullptr;
+  if (!p) return SL_OK;
+  cudaError_t e = cudaFreeHost(p);
+  if (e != cudaSuccess)
+    return fail(c, SL_ECUDA, "cudaFreeHost: %s", cudaGetErrorString(e));
+  return SL_OK;
+}
+
 const char *sl_last_error(const sl_ctx *ctx) {
   return ctx ? ctx->err.c_str() : g_err.c_str();
 }

@@ -109,6 +109,9 @@ class DeviceMirror:
     # host -> device
     def push(self, store: ObjectStore, env: Environment | None,
              masses: bool = True):
+        if not _native.is_pinned(store._m_pos):
+            # page-locked mass columns: uploads / pulls at copy-engine speed
+            store.adopt_mass_allocator(_native.pinned_empty)
         m, s = store.mass_slot_count, store.spring_slot_count
         if masses or self.ctx.m_n != m:
             self.ctx.upload_masses(

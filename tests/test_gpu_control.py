@@ -304,3 +304,27 @@ def test_numerical_abort_surfaces_in_report():
     rep = ctl.wait_for_event(timeout=60)
     assert rep.reason == "error" and rep.error is not None
     assert ctl.state == "done"
+
+
+def test_pinned_mass_columns_and_lock_time_reads():
+    """The mirror moves the mass columns into page-locked memory on first
+    push (contents unchanged, growth keeps them pinned); while running,
+    store reads see the lock-time state, after the pause the pulled one."""
+    from paper_1911_10274_b200 import _native
+    ctl, st, body = controller(dt=1e-4)
+    h = body.mass_handles[0]
+    before = st.get_mass(h).pos.as_array()
+    ref_bytes = state_bytes(st)
+    ctl.start(10.0)
+    for _ in range(20):  # lock-time view, never a half-pulled state
+        assert np.array_equal(st.get_mass(h).pos.as_array(), before)
+    ctl.pause()
+    ctl.wait_for_event(timeout=60)
+    assert not np.array_equal(st.get_mass(h).pos.as_array(), before)
+    assert state_bytes(st) != ref_bytes
+    assert _native.is_pinned(st._m_pos) and _native.is_pinned(st._m_gen)
+    grown = st.create_mass(Mass(pos=Vec3(0, 0, 1), m=1.0))
+    for _ in range(7):
+        st.create_mass(Mass(pos=Vec3(0, 0, 1), m=1.0))
+    assert _native.is_pinned(st._m_pos) and st.mass_is_live(grown)
+    ctl.stop()
