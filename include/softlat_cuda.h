@@ -252,6 +252,17 @@ int sl_state_pointers(sl_ctx *ctx, void **pos_read, int64_t *rows,
 /* The context's CUDA stream (cudaStream_t) for ordering foreign work. */
 int sl_get_stream(sl_ctx *ctx, void **stream);
 
+/* ---------------------------------------------------------------- snapshots */
+/* Snapshot CSV of io.py:19-32 (format_snapshot): header "id,x,y,z,vx,vy,vz"
+ * then one row per mass, each double as Python's "{:.17g}" (bit-exact
+ * round trip; "inf"/"-inf"/"nan" for non-finite values).  Host only, no
+ * context.  `out` must hold 18 + n * SL_SNAPSHOT_ROW_MAX bytes; *len gets
+ * the text length (no terminating NUL). */
+#define SL_SNAPSHOT_ROW_MAX 176
+int sl_format_snapshot(int64_t n, const int64_t *ids, const double *pos,
+                       const double *vel, int threads, char *out, size_t cap,
+                       size_t *len);
+
 /* ---------------------------------------------------------- timing / sync */
 /* CUDA events on the context's stream (bench.py measures with these). */
 int sl_timer_start(sl_ctx *ctx);

@@ -8,6 +8,7 @@ the .so travels with the repo snapshot to the GPU box.  Translation units:
   (kernels.py is compiled without fastmath; SURVEY.md 7 hard part 2).
 * csrc/sl_kernels_fp32.cu -- fp32 / mixed kernels (FMA allowed).
 * csrc/sl_api.cu          -- context, layout build (CUB), C ABI.
+* csrc/sl_io.cpp          -- host-side snapshot formatting (threads).
 """
 from __future__ import annotations
 
@@ -32,6 +33,7 @@ UNITS = {
     # denormal-rescaling sequence); IEEE divide/sqrt are not used there
     "sl_kernels_fp32.cu": ["-ftz=true"],
     "sl_api.cu": [],
+    "sl_io.cpp": [],  # host only: snapshot formatting
 }
 
 
@@ -65,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for unit, extra in UNITS.items():
-        obj = os.path.join(OBJ_DIR, unit.replace(".cu", ".o"))
+        obj = os.path.join(OBJ_DIR, os.path.splitext(unit)[0] + ".o")
         cmd = [cc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit),
                "-o", obj]
         if verbose:

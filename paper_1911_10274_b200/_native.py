@@ -35,7 +35,7 @@ EXPORTS = (
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
     "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
-    "sl_host_free")
+    "sl_host_free", "sl_format_snapshot")
 
 
 class SlStats(C.Structure):
@@ -105,6 +105,7 @@ def load_library(path: str = LIB_PATH):
             "sl_spring_loads": ([P, D, P, P], I),
             "sl_host_alloc": ([C.c_size_t, P], I),
             "sl_host_free": ([P], I),
+            "sl_format_snapshot": ([I64, P, P, P, I, P, C.c_size_t, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
