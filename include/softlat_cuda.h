@@ -263,6 +263,24 @@ int sl_format_snapshot(int64_t n, const int64_t *ids, const double *pos,
                        const double *vel, int threads, char *out, size_t cap,
                        size_t *len);
 
+/* ------------------------------------------------------------ host builder */
+/* Lattice generation of builder.py:112-186 (build_lattice + materialize):
+ * n_masses = nx*ny*nz row-major nodes, springs grouped by the 13 cell
+ * offsets; outputs are bit-identical to the numpy builder (rest, k = E A / L,
+ * node mass = half-bar masses in np.add.at order; the caller applies the
+ * minimum-mass rule to bare nodes).  Host only, `threads` workers. */
+int sl_lattice_counts(int64_t nx, int64_t ny, int64_t nz, int64_t *n_masses,
+                      int64_t *n_springs);
+int sl_build_lattice(int64_t nx, int64_t ny, int64_t nz, const double *corner,
+                     double spacing, double elastic_modulus, double density,
+                     double diameter, int threads, double *pos,
+                     double *node_mass, int64_t *a, int64_t *b, double *rest,
+                     double *stiff);
+/* Fill count elements of elem_bytes (<= 64) with *value on `threads`
+ * workers (first touch of fresh store capacity in parallel). */
+int sl_host_fill(void *dst, const void *value, size_t elem_bytes,
+                 int64_t count, int threads);
+
 /* ---------------------------------------------------------- timing / sync */
 /* CUDA events on the context's stream (bench.py measures with these). */
 int sl_timer_start(sl_ctx *ctx);

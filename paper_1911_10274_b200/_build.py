@@ -8,7 +8,8 @@ the .so travels with the repo snapshot to the GPU box.  Translation units:
   (kernels.py is compiled without fastmath; SURVEY.md 7 hard part 2).
 * csrc/sl_kernels_fp32.cu -- fp32 / mixed kernels (FMA allowed).
 * csrc/sl_api.cu          -- context, layout build (CUB), C ABI.
-* csrc/sl_io.cpp          -- host-side snapshot formatting (threads).
+* csrc/sl_host.cpp        -- host-side snapshot formatting, lattice generation,
+  parallel fills (threads; no FMA contraction: bit-exact with numpy).
 """
 from __future__ import annotations
 
@@ -33,7 +34,7 @@ UNITS = {
     # denormal-rescaling sequence); IEEE divide/sqrt are not used there
     "sl_kernels_fp32.cu": ["-ftz=true"],
     "sl_api.cu": [],
-    "sl_io.cpp": [],  # host only: snapshot formatting
+    "sl_host.cpp": ["-Xcompiler", "-ffp-contract=off"],  # host only
 }
 
 

@@ -35,7 +35,8 @@ EXPORTS = (
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
     "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
-    "sl_host_free", "sl_format_snapshot")
+    "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
+    "sl_build_lattice", "sl_host_fill")
 
 
 class SlStats(C.Structure):
@@ -106,6 +107,10 @@ def load_library(path: str = LIB_PATH):
             "sl_host_alloc": ([C.c_size_t, P], I),
             "sl_host_free": ([P], I),
             "sl_format_snapshot": ([I64, P, P, P, I, P, C.c_size_t, P], I),
+            "sl_lattice_counts": ([I64, I64, I64, P, P], I),
+            "sl_build_lattice": ([I64, I64, I64, P, D, D, D, D, I] + [P] * 6,
+                                 I),
+            "sl_host_fill": ([P, P, C.c_size_t, I64, I], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

@@ -163,6 +163,12 @@ def materialize(store: ObjectStore, positions: np.ndarray, a_ids, b_ids,
     node_mass = np.zeros(len(positions))
     np.add.at(node_mass, a_ids, half_bar)
     np.add.at(node_mass, b_ids, half_bar)
+    return _create(store, positions, node_mass, a_ids, b_ids, rests, stiff,
+                   diam, material, fixed, grid_indices)
+
+
+def _create(store, positions, node_mass, a_ids, b_ids, rests, stiff, diam,
+            material, fixed, grid_indices) -> BodyHandle:
     bare = node_mass <= 0.0
     if bare.any():
         log.warning("%d nodes have no bar volume; assigning minimum mass %g kg",
@@ -177,7 +183,60 @@ def materialize(store: ObjectStore, positions: np.ndarray, a_ids, b_ids,
                       grid_indices=grid_indices)
 
 
+def _threads() -> int:
+    import os
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
+def lattice_arrays(spec: LatticeSpec):
+    """(positions, node_mass, a, b, rest, stiff) of ``spec`` from the
+    library's threaded generator (sl_build_lattice), bit-identical to
+    ``_grid_positions`` + ``grid_springs`` + ``materialize``'s numpy."""
+    import ctypes as C
+    from . import _native
+    lib = _native.load_library()
+    nm, ns = C.c_int64(), C.c_int64()
+    if lib.sl_lattice_counts(spec.nx, spec.ny, spec.nz, C.byref(nm),
+                             C.byref(ns)) != _native.SL_OK:
+        raise InvalidValueError("bad lattice counts")
+    nm, ns = nm.value, ns.value
+    pos = np.empty((nm, 3))
+    node_mass = np.empty(nm)
+    a = np.empty(ns, np.int64)
+    b = np.empty(ns, np.int64)
+    rest = np.empty(ns)
+    stiff = np.empty(ns)
+    corner = spec.corner.as_array()
+    m = spec.material
+    p = _native._ptr
+    rc = lib.sl_build_lattice(spec.nx, spec.ny, spec.nz, p(corner),
+                              float(spec.spacing), float(m.elastic_modulus),
+                              float(m.density), float(spec.diameter),
+                              _threads(), p(pos), p(node_mass), p(a), p(b),
+                              p(rest), p(stiff))
+    if rc != _native.SL_OK:
+        raise InvalidValueError(f"sl_build_lattice failed ({rc})")
+    return pos, node_mass, a, b, rest, stiff
+
+
 def build_lattice(spec: LatticeSpec, store: ObjectStore) -> BodyHandle:
+    """builder.py:112-186: generated by the library (threads), same arrays
+    as the numpy path (``build_lattice_numpy``, tests/test_builder.py)."""
+    pos, node_mass, a, b, rest, stiff = lattice_arrays(spec)
+    if not np.all(np.isfinite(pos)):
+        raise InvalidValueError("non-finite mass position")
+    if len(rest) and not np.all(rest > 0):
+        raise InvalidValueError("coincident lattice nodes")
+    idx = np.indices((spec.nx, spec.ny, spec.nz)).reshape(3, -1).T
+    diam = np.broadcast_to(np.asarray(spec.diameter, np.float64), rest.shape)
+    return _create(store, pos, node_mass, a, b, rest, stiff, diam,
+                   spec.material, None, idx)
+
+
+def build_lattice_numpy(spec: LatticeSpec, store: ObjectStore) -> BodyHandle:
     positions, idx = _grid_positions(spec.corner, spec.nx, spec.ny, spec.nz,
                                      spec.spacing)
     a, b = grid_springs(spec.nx, spec.ny, spec.nz)

@@ -3,7 +3,7 @@
 Same formats and names as io.py:1-80.  ``format_snapshot`` /
 ``write_snapshot`` produce byte-identical text (Python's ``{:.17g}`` digits,
 io.py:19-27) through the library's threaded formatter
-(``sl_format_snapshot``, csrc/sl_io.cpp) instead of a per-row Python loop;
+(``sl_format_snapshot``, csrc/sl_host.cpp) instead of a per-row Python loop;
 ``read_snapshot`` parses with numpy's C reader and falls back to the
 reference's line loop for its error messages (io.py:35-49).  Binary
 snapshots (``write_snapshot_npz`` / ``read_snapshot_npz``) are the
