@@ -280,6 +280,8 @@ int sl_build_lattice(int64_t nx, int64_t ny, int64_t nz, const double *corner,
  * workers (first touch of fresh store capacity in parallel). */
 int sl_host_fill(void *dst, const void *value, size_t elem_bytes,
                  int64_t count, int threads);
+/* memcpy on `threads` workers (snapshot copies into fresh arrays). */
+int sl_host_copy(void *dst, const void *src, size_t bytes, int threads);
 
 /* ---------------------------------------------------------- timing / sync */
 /* CUDA events on the context's stream (bench.py measures with these). */

@@ -36,7 +36,7 @@ EXPORTS = (
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
     "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
-    "sl_build_lattice", "sl_host_fill")
+    "sl_build_lattice", "sl_host_fill", "sl_host_copy")
 
 
 class SlStats(C.Structure):
@@ -111,6 +111,7 @@ def load_library(path: str = LIB_PATH):
             "sl_build_lattice": ([I64, I64, I64, P, D, D, D, D, I] + [P] * 6,
                                  I),
             "sl_host_fill": ([P, P, C.c_size_t, I64, I], I),
+            "sl_host_copy": ([P, P, C.c_size_t, I], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -164,6 +165,26 @@ def pinned_empty(shape, dtype) -> np.ndarray:
     n = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
     raw = np.asarray(_PinnedBlock(n))
     return raw[:n].view(dt).reshape(shape)
+
+
+def host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
+def host_copy(a: np.ndarray) -> np.ndarray:
+    """np.array(a) with the copy (and the fresh pages' first touch) spread
+    over the host threads (sl_host_copy); small arrays copy in numpy."""
+    if a.nbytes < (8 << 20) or not a.flags.c_contiguous:
+        return np.array(a)
+    out = np.empty_like(a)
+    rc = load_library().sl_host_copy(_ptr(out), _ptr(a), a.nbytes,
+                                     host_threads())
+    if rc != SL_OK:
+        raise SoftlatError(f"sl_host_copy failed ({rc})")
+    return out
 
 
 def is_pinned(a: np.ndarray) -> bool:

@@ -259,3 +259,17 @@ extern "C" int sl_build_lattice(int64_t nx, int64_t ny, int64_t nz,
   }
   return SL_OK;
 }
+
+// Copy on several threads (fresh destination pages fault in parallel):
+// snapshot copies of the store's mass columns (control.snapshot).
+extern "C" int sl_host_copy(void *dst, const void *src, size_t bytes,
+                            int threads) {
+  if (bytes && (!dst || !src)) return SL_EINVAL;
+  unsigned char *d = (unsigned char *)dst;
+  const unsigned char *s = (const unsigned char *)src;
+  parallel_for((int64_t)bytes, threads, (int64_t)4 << 20,
+               [&](int64_t lo, int64_t hi) {
+                 std::memcpy(d + lo, s + lo, (size_t)(hi - lo));
+               });
+  return SL_OK;
+}
