@@ -20,3 +20,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
 ncu --set full --clock-control none --import-source on -k regex:k_win_tma -s 6 -c 1 \
     -o $out/prof_$tag -f python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $out/ncu_full_$tag.log 2>&1
 tail -1 $out/ncu_full_$tag.log
+for p in fp64 mixed; do
+  ncu --set full --clock-control none --import-source on -k regex:k_win_tma -s 6 -c 1 \
+      -o $out/prof_${p}_$tag -f python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --precision $p > $out/ncu_full_${p}_$tag.log 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:k_fused_small -s 1 -c 1 \
+    -o $out/prof_fused_$tag -f python bench.py --config D --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $out/ncu_full_fused_$tag.log 2>&1
+python bench.py --n 200 --steps 200 --warmup 5 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_n200_$tag.json

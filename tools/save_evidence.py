@@ -52,4 +52,13 @@ if os.path.exists(rep):
               "w") as fh:
         subprocess.run([sys.executable, "tools/ncu_hot.py", "/tmp/_src.csv",
                         "25"], stdout=fh)
+# the other modes' window kernels and the fused small-body kernel
+for name, out_name, ab in (("fp64", "ncu_k_win_tma_fp64", "409600000"),
+                           ("mixed", "ncu_k_win_tma_mixed", "307700000"),
+                           ("fused", "ncu_k_fused_small_fp32", "128400000")):
+    rep = os.path.join(src, f"prof_{name}_{tag}.ncu-rep")
+    if os.path.exists(rep):
+        subprocess.run([sys.executable, "tools/ncu_summary.py", rep,
+                        os.path.join(dst, f"{out_name}_{tag}.txt"), ab],
+                       check=True, stdout=subprocess.DEVNULL)
 print("saved", tag)
