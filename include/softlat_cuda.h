@@ -282,6 +282,10 @@ int sl_host_fill(void *dst, const void *value, size_t elem_bytes,
                  int64_t count, int threads);
 /* memcpy on `threads` workers (snapshot copies into fresh arrays). */
 int sl_host_copy(void *dst, const void *src, size_t bytes, int threads);
+/* min / max of v over mask != 0 (mask may be NULL), NaN-propagating like
+ * numpy; empty selection gives +inf / -inf (check_stability's extrema). */
+int sl_host_masked_extrema(const double *v, const uint8_t *mask, int64_t n,
+                           int threads, double *out_min, double *out_max);
 
 /* ---------------------------------------------------------- timing / sync */
 /* CUDA events on the context's stream (bench.py measures with these). */

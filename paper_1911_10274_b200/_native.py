@@ -36,7 +36,8 @@ EXPORTS = (
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
     "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
-    "sl_build_lattice", "sl_host_fill", "sl_host_copy")
+    "sl_build_lattice", "sl_host_fill", "sl_host_copy",
+    "sl_host_masked_extrema")
 
 
 class SlStats(C.Structure):
@@ -112,6 +113,7 @@ def load_library(path: str = LIB_PATH):
                                  I),
             "sl_host_fill": ([P, P, C.c_size_t, I64, I], I),
             "sl_host_copy": ([P, P, C.c_size_t, I], I),
+            "sl_host_masked_extrema": ([P, P, I64, I, P, P], I),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -185,6 +187,22 @@ def host_copy(a: np.ndarray) -> np.ndarray:
     if rc != SL_OK:
         raise SoftlatError(f"sl_host_copy failed ({rc})")
     return out
+
+
+def masked_extrema(v: np.ndarray, mask: np.ndarray | None):
+    """(min, max) of v where mask (threaded, sl_host_masked_extrema);
+    numpy semantics: NaN propagates, empty gives (inf, -inf)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if mask is not None:
+        mask = np.ascontiguousarray(mask).view(np.uint8)
+        if len(mask) != len(v):
+            raise InvalidValueError("mask length differs")
+    lo, hi = C.c_double(), C.c_double()
+    rc = load_library().sl_host_masked_extrema(
+        _ptr(v), _ptr(mask), len(v), host_threads(), C.byref(lo), C.byref(hi))
+    if rc != SL_OK:
+        raise SoftlatError(f"sl_host_masked_extrema failed ({rc})")
+    return lo.value, hi.value
 
 
 def is_pinned(a: np.ndarray) -> bool:

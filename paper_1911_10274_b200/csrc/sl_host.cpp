@@ -273,3 +273,47 @@ extern "C" int sl_host_copy(void *dst, const void *src, size_t bytes,
                });
   return SL_OK;
 }
+
+// min and max of v[i] over mask[i] != 0 (mask NULL: all), NaN-propagating
+// like numpy's masked np.min / np.max; empty selection: +inf / -inf.
+// check_stability's k_max / m_min over 12.7 M springs (engine.py:274-296).
+extern "C" int sl_host_masked_extrema(const double *v, const uint8_t *mask,
+                                      int64_t n, int threads, double *out_min,
+                                      double *out_max) {
+  if (n < 0 || !out_min || !out_max || (n > 0 && !v)) return SL_EINVAL;
+  int64_t nt = threads < 1 ? 1 : threads;
+  if (nt > n / (1 << 16) + 1) nt = n / (1 << 16) + 1;
+  std::vector<double> mn((size_t)nt), mx((size_t)nt);
+  std::vector<int> nan((size_t)nt);
+  auto chunk = [&](int64_t t) {
+    double a = INFINITY, b = -INFINITY;
+    int bad = 0;
+    for (int64_t i = n * t / nt; i < n * (t + 1) / nt; i++) {
+      if (mask && !mask[i]) continue;
+      const double x = v[i];
+      bad |= x != x;
+      a = x < a ? x : a;
+      b = x > b ? x : b;
+    }
+    mn[(size_t)t] = a;
+    mx[(size_t)t] = b;
+    nan[(size_t)t] = bad;
+  };
+  if (nt == 1) {
+    chunk(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int64_t t = 0; t < nt; t++) pool.emplace_back(chunk, t);
+    for (auto &th : pool) th.join();
+  }
+  double a = INFINITY, b = -INFINITY;
+  int bad = 0;
+  for (int64_t t = 0; t < nt; t++) {
+    a = mn[(size_t)t] < a ? mn[(size_t)t] : a;
+    b = mx[(size_t)t] > b ? mx[(size_t)t] : b;
+    bad |= nan[(size_t)t];
+  }
+  *out_min = bad ? NAN : a;
+  *out_max = bad ? NAN : b;
+  return SL_OK;
+}
