@@ -47,7 +47,9 @@ def parse():
                     help="B: one 100^3 lattice per rank (batched instances);"
                          " D: --robots actuated 5^3 robots sharded over "
                          "the ranks (RL batch)")
-    ap.add_argument("--n", type=int, default=100, help="lattice edge")
+    ap.add_argument("--n", "--edge", dest="n", type=int, default=100,
+                    help="lattice edge (--edge under torchrun, whose parser "
+                         "reads --n as ambiguous)")
     ap.add_argument("--robots", type=int, default=4096)
     ap.add_argument("--precision", default="fp32",
                     choices=["fp32", "mixed", "fp64"])
@@ -81,10 +83,10 @@ def build_robots(count: int, first: int = 0):
     from paper_1911_10274_b200 import (ContactPlane, Environment, Material,
                                        ObjectStore, Vec3)
     from paper_1911_10274_b200.builder import LatticeSpec, build_robot_swarm
-    step = 4 * 0.05 + 2 * 0.05
     st = ObjectStore()
-    build_robot_swarm(LatticeSpec(Vec3(0, first * step, 0), 5, 5, 5, 0.05,
-                                  Material(1e6, 1000.0)), st, count)
+    build_robot_swarm(LatticeSpec(Vec3(0, 0, 0), 5, 5, 5, 0.05,
+                                  Material(1e6, 1000.0)), st, count,
+                      first=first)
     env = Environment(gravity=Vec3(0, 0, -9.81), drag_coeff=0.01,
                       contacts=[ContactPlane(
                           normal=Vec3(0, 0, 1), offset=0.0, stiffness=500.0,
@@ -269,7 +271,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         # nccl on the box (one rank per GPU); gloo lets the rank logic be
         # exercised with several ranks on one device
         dist.init_process_group(backend)

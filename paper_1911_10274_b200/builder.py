@@ -261,13 +261,15 @@ def build_swarm(spec: LatticeSpec, store: ObjectStore, count: int,
 
 
 def build_robot_swarm(spec: LatticeSpec, store: ObjectStore, count: int,
-                      worm: bool = True, gap: float | None = None):
+                      worm: bool = True, gap: float | None = None,
+                      first: int = 0):
     """``count`` lattice robots stacked along +y (cmd_swarm layout,
     cli.py:323-331) created in ONE bulk call, each worm-actuated like
     ``configure_worm`` (actuation.py:72-111) when ``worm``.  Same arrays as
     ``build_swarm`` + per-body ``configure_worm``, built vectorised (config
-    D: thousands of RL robots).  Returns per-body (mass slot range, spring
-    slot range)."""
+    D: thousands of RL robots).  ``first`` places the robots as robots
+    first.. of a larger swarm (a rank's shard).  Returns per-body (mass
+    slot range, spring slot range)."""
     from .actuation import WORM_AMPLITUDE, WORM_FREQUENCY, WORM_PERIOD
     pos1, idx = _grid_positions(spec.corner, spec.nx, spec.ny, spec.nz,
                                 spec.spacing)
@@ -276,7 +278,9 @@ def build_robot_swarm(spec: LatticeSpec, store: ObjectStore, count: int,
     step = extent + 2 * spec.spacing if gap is None else extent + gap
     m1, s1 = len(pos1), len(a1)
     shift = np.zeros((count, 1, 3))
-    shift[:, 0, 1] = np.arange(count) * step
+    # robot i of the global swarm sits at i * step; ``first`` makes a shard
+    # (robots first .. first+count-1) bit-identical to that part of it
+    shift[:, 0, 1] = (first + np.arange(count)) * step
     positions = (pos1[None] + shift).reshape(-1, 3)
     base = (np.arange(count) * m1)[:, None]
     a = (a1[None] + base).reshape(-1)
