@@ -1268,7 +1268,10 @@ int run_fused(sl_ctx *c, const KState &S, int64_t n, const double *times,
   if (c->h_status[5]) {
     *aborted = true;
     c->fz_aborts++;
-    CK(cudaMemsetAsync(c->status.p, 0, 8 * 8, c->st));
+    // keep the counters already in status (prepare's invalid-endpoint
+    // kills, kernels.py:37-45): the per-step re-run adds to them
+    CK(cudaMemsetAsync(c->status.as<unsigned long long>() + 5, 0, 2 * 8,
+                       c->st));
     return SL_OK;
   }
   std::swap(c->vel, c->vel2);  // committed: the new velocities
@@ -2098,8 +2101,12 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     bool aborted = false;
     if ((rc = run_fused(c, S, n_steps, sim_times, dt, &aborted))) return rc;
     if (!aborted) {
+      // no spring events / errors inside the fused launch (eligibility);
+      // the counters are prepare's invalid-endpoint kills of this call
+      if (counters)
+        for (int q = 0; q < 3; q++) counters[q] += (int64_t)c->h_status[q];
       if (steps_done) *steps_done = n_steps;
-      return SL_OK;  // no spring events / errors on this path (eligibility)
+      return SL_OK;
     }
   }
   for (int64_t n = 0; n < n_steps; n++) {
