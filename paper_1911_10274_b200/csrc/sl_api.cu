@@ -1092,7 +1092,7 @@ int build_window_exact(sl_ctx *c) {
   if (!c->win_enabled || !c->tma_enabled || c->prec != PREC_FP64 ||
       c->n_slices == 0 || c->max_width == 0 || c->max_width > 64)
     return SL_OK;
-  const int tt = 12;
+  const int tt = SL_WIN64_T;
   const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
   WinCfg w{};
   w.n_tiles = n_tiles;

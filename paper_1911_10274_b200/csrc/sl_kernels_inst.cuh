@@ -149,10 +149,11 @@ struct SplitLaunch<PREC_FP64> {
 #ifdef SL_UNIT_FP64
   static void win(const KState &S, const EnvP &E, const StepP &T,
                   const WinCfg &C, int grid, cudaStream_t st) {
-    k_win_tma<PREC_FP64, 12><<<grid, 13 * 32, win_smem(C), st>>>(S, E, T, C);
+    k_win_tma<PREC_FP64, SL_WIN64_T>
+        <<<grid, (SL_WIN64_T + 1) * 32, win_smem(C), st>>>(S, E, T, C);
   }
   static int win_setup(const WinCfg &C) {
-    return smem_optin(k_win_tma<PREC_FP64, 12>, win_smem(C));
+    return smem_optin(k_win_tma<PREC_FP64, SL_WIN64_T>, win_smem(C));
   }
 #else
   static void win(const KState &, const EnvP &, const StepP &,
