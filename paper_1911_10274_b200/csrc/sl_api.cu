@@ -122,7 +122,8 @@ struct sl_ctx {
   size_t fz_smem = 0;
   int64_t fz_launches = 0, fz_aborts = 0;
   DevBuf fz_gstart, fz_gcount, fz_ent, fz_code, fz_dict, fz_actb, fz_has,
-      fz_zero, fz_gid, fz_fail, fz_times, fz_diff, vel2;
+      fz_zero, fz_gid, fz_fail, fz_times, fz_diff, vel2, fz_perm, fz_cnt,
+      fz_epos, fz_cnt_a;
   DevBuf diag;  // diagnostics scratch (sl_energy / sl_spring_loads)
   bool auto_atomic = false;  // SL_ACC_AUTO resolved to the atomic variant
   // grouped sine actuation of the split layout's fast path (ActP)
@@ -738,6 +739,7 @@ KState make_state(sl_ctx *c) {
     S.sp_acto = act ? c->sp_acto.as<double>() : nullptr;
     if (c->fz_ok) {
       S.fz_code = c->fz_code.as<uint8_t>();
+      S.fz_epos = c->fz_epos.as<uint16_t>();
       S.fz_gid = c->fz_gid.as<int32_t>();
       S.fz_gstart = c->fz_gstart.as<int32_t>();
       S.fz_zero = c->fz_zero.as<uint8_t>();
@@ -1190,6 +1192,10 @@ int build_fused_groups(sl_ctx *c) {
   CK(c->fz_gcount.ensure(4 * ng));
   CK(c->fz_ent.ensure((size_t)2 * ng * rows * FZ_MAXM));
   CK(c->fz_code.ensure((size_t)ng * rows * FZ_MAXM));
+  CK(c->fz_epos.ensure((size_t)2 * ng * rows * FZ_MAXM));
+  CK(c->fz_perm.ensure((size_t)2 * ng * FZ_MAXM));
+  CK(c->fz_cnt.ensure((size_t)ng * FZ_MAXM));
+  CK(c->fz_cnt_a.ensure((size_t)ng * FZ_MAXM));
   CK(c->fz_dict.ensure((size_t)8 * WIN_DMAX * ng));
   CK(c->fz_actb.ensure((size_t)WIN_ACTB * ng));
   CK(c->fz_has.ensure(ng));
@@ -1209,6 +1215,8 @@ int build_fused_groups(sl_ctx *c) {
       (uint32_t)m_pad, (uint32_t)(c->n_slices << (c->sp_a + 5)),
       c->fz_gstart.as<int32_t>(), c->fz_gcount.as<int32_t>(), ra, rb,
       c->fz_ent.as<uint16_t>(), c->fz_code.as<uint8_t>(),
+      c->fz_perm.as<uint16_t>(), c->fz_cnt.as<uint8_t>(),
+      c->fz_cnt_a.as<uint8_t>(), c->fz_epos.as<uint16_t>(),
       c->fz_dict.as<float2>(), c->fz_actb.as<unsigned char>(),
       c->fz_has.as<uint8_t>(), c->fz_zero.as<uint8_t>(),
       c->fz_gid.as<int32_t>(), c->fz_fail.as<unsigned long long>());
@@ -1225,6 +1233,9 @@ int build_fused_groups(sl_ctx *c) {
   f.gcount = c->fz_gcount.as<int32_t>();
   f.ent = c->fz_ent.as<uint16_t>();
   f.code = c->fz_code.as<uint8_t>();
+  f.perm = c->fz_perm.as<uint16_t>();
+  f.cnt = c->fz_cnt.as<uint8_t>();
+  f.cnt_a = c->fz_cnt_a.as<uint8_t>();
   f.dict = c->fz_dict.as<float2>();
   f.actb = c->fz_actb.as<unsigned char>();
   f.has_act = c->fz_has.as<uint8_t>();
@@ -1612,7 +1623,8 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_gstart, &c->fz_gcount, &c->fz_ent, &c->fz_code,
                     &c->fz_dict, &c->fz_actb, &c->fz_has, &c->fz_fail,
                     &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
-                    &c->fz_gid, &c->diag,
+                    &c->fz_gid, &c->diag, &c->fz_perm, &c->fz_cnt,
+                    &c->fz_epos, &c->fz_cnt_a,
                     &c->win_fail};
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);

@@ -122,6 +122,7 @@ struct KState {
   // multi-step fused groups (sl_fused.cuh; null when not built): material
   // codes [group][rows][512], group of every mass, group starts / zero codes
   uint8_t *fz_code;
+  const uint16_t *fz_epos;  // split row of a mass -> compacted row, thread
   const int32_t *fz_gid, *fz_gstart;
   const uint8_t *fz_zero;
   int fz_rows, fz_ra;
@@ -1045,7 +1046,10 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
         const int64_t i = sl * 32 + (rem & 31);
         const int row = q == 0 ? rem >> 5 : S.fz_ra + (rem >> 5) - (1 << S.sp_a);
         const int32_t g = S.fz_gid[i];
-        S.fz_code[((int64_t)g * S.fz_rows + row) * 512 + (i - S.fz_gstart[g])] =
+        const uint32_t qt =
+            S.fz_epos[((int64_t)g * S.fz_rows + row) * 512 +
+                      (i - S.fz_gstart[g])];
+        S.fz_code[((int64_t)g * S.fz_rows + (qt >> 9)) * 512 + (qt & 511)] =
             S.fz_zero[g];
       }
     }

@@ -35,9 +35,12 @@ struct FzCfg {
   int64_t n_groups;
   const int32_t *gstart;  // [g] first mass of the group
   const int32_t *gcount;  // [g] masses
-  const uint16_t *ent;    // [g][ra + rb][FZ_MAXM] local partner (FZ_MAXM:
-                          // the sentinel record)
+  const uint16_t *ent;    // [g][ra + rb][FZ_MAXM] local partner of the
+                          // q-th entry of thread t (FZ_MAXM: sentinel)
   const uint8_t *code;    // [g][ra + rb][FZ_MAXM] material code
+  const uint16_t *perm;   // [g][FZ_MAXM] thread t -> local mass
+  const uint8_t *cnt;     // [g][FZ_MAXM] entries of thread t
+  const uint8_t *cnt_a;   // [g][FZ_MAXM] of which A-section entries
   const float2 *dict;     // [g][WIN_DMAX] (k, k L0)
   const unsigned char *actb;  // [g][WIN_ACTB] actuation block (window fmt)
   const uint8_t *has_act;     // [g]
@@ -58,9 +61,12 @@ static __global__ void __launch_bounds__(FZ_MAXM)
                   const double4 *act, const uint8_t *grp, const float4 *vel,
                   int a, int rows, uint32_t sent, uint32_t nul,
                   const int32_t *gstart, const int32_t *gcount, int ra, int rb,
-                  uint16_t *ent, uint8_t *code, float2 *dict,
-                  unsigned char *actb, uint8_t *has_act, uint8_t *zero,
-                  int32_t *gid, unsigned long long *fail) {
+                  uint16_t *ent, uint8_t *code, uint16_t *perm, uint8_t *cnt,
+                  uint8_t *cnt_a, uint16_t *epos, float2 *dict,
+                  unsigned char *actb,
+                  uint8_t *has_act, uint8_t *zero, int32_t *gid,
+                  unsigned long long *fail) {
+  __shared__ int16_t scnt[FZ_MAXM];
   __shared__ unsigned long long dkey[WIN_DMAX];
   __shared__ float2 dkl[WIN_DMAX];
   __shared__ double4 dact[WIN_DMAX];
@@ -105,32 +111,53 @@ static __global__ void __launch_bounds__(FZ_MAXM)
     *s = (uint32_t)sp_s[e];
     return split_partner(w, a);
   };
+  int n_mine = 0, n_a = 0;
   for (int q = 0; q < ra + rb; q++) {
     uint32_t kli = 0, s = 0;
     const uint32_t j = entry(q, &kli, &s);
     if (j == 0xFFFFFFFFu) continue;
+    n_mine++;
+    n_a += q < ra;
     if ((int64_t)j < g0 || (int64_t)j >= (int64_t)g0 + gn) ok = 0;
     const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
     if (tab.find(mat_hash(x), true, &x) < 0) ok = 0;
   }
+  // sort key: entry count, then A-section count (both loops warp-uniform)
+  scnt[li] = (int16_t)(mine ? n_mine * 64 + n_a : -1);
   __syncthreads();
+  // thread slot of this mass: masses sorted by entry count, descending
+  // (stable), so a warp's 32 masses have similar counts and its loop runs
+  // to about their own count instead of the group's maximum row count
+  int t = 0;
+  for (int j = 0; j < FZ_MAXM; j++) {
+    const int cj = scnt[j];
+    t += cj > scnt[li] || (cj == scnt[li] && j < li);
+  }
+  perm[g * FZ_MAXM + t] = (uint16_t)li;
+  cnt[g * FZ_MAXM + t] = (uint8_t)(mine ? n_mine : 0);
+  cnt_a[g * FZ_MAXM + t] = (uint8_t)(mine ? n_a : 0);
   const int zc = tab.find(zero_key, false, nullptr);
   if (mine) gid[i] = (int32_t)g;
   if (li == 0) zero[g] = (uint8_t)(zc < 0 ? 0 : zc);
+  int qq = 0;  // compacted row: valid entries in (A rows, B rows) order
   for (int q = 0; q < ra + rb; q++) {
     uint32_t kli = 0, s = 0;
     const uint32_t j = entry(q, &kli, &s);
-    uint16_t p = FZ_MAXM;
-    int c = zc;
-    if (j != 0xFFFFFFFFu) {
-      const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
-      c = tab.find(mat_hash(x), false, nullptr);
-      if (!tab.same(c, x)) ok = 0;
-      p = (uint16_t)(j - (uint32_t)g0);
-    }
-    const int64_t x = (g * (ra + rb) + q) * FZ_MAXM + li;
-    ent[x] = p;
-    code[x] = (uint8_t)(c < 0 ? 0 : c);
+    if (j == 0xFFFFFFFFu) continue;
+    const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
+    const int c = tab.find(mat_hash(x), false, nullptr);
+    if (!tab.same(c, x)) ok = 0;
+    const int64_t o = (g * (ra + rb) + qq) * FZ_MAXM + t;
+    ent[o] = (uint16_t)(j - (uint32_t)g0);
+    code[o] = (uint8_t)(c < 0 ? 0 : c);
+    // split row q of mass li -> (compacted row, thread): device kills
+    epos[(g * (ra + rb) + q) * FZ_MAXM + li] = (uint16_t)(qq * FZ_MAXM + t);
+    qq++;
+  }
+  for (; qq < ra + rb; qq++) {  // padding (never read: the loop stops at cnt)
+    const int64_t o = (g * (ra + rb) + qq) * FZ_MAXM + t;
+    ent[o] = FZ_MAXM;
+    code[o] = (uint8_t)(zc < 0 ? 0 : zc);
   }
   __syncthreads();
   if (!ok) {
@@ -178,10 +205,13 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
   int8_t *smode = (int8_t *)(sen + rows * FZ_MAXM);
   __shared__ int sbad;
   const int64_t g = blockIdx.x;
-  const int li = threadIdx.x;
+  const int t = threadIdx.x;  // thread slot (masses sorted by entry count)
   const int32_t g0 = C.gstart[g], gn = C.gcount[g];
+  const bool mine = t < gn;
+  const int li = mine ? (int)C.perm[g * FZ_MAXM + t] : t;  // local mass
+  const int n_ent = mine ? (int)C.cnt[g * FZ_MAXM + t] : 0;
+  const int n_a = mine ? (int)C.cnt_a[g * FZ_MAXM + t] : 0;
   const int64_t i = (int64_t)g0 + li;
-  const bool mine = li < gn;
   const bool act = C.has_act[g] != 0;
   // ---- load the group
   R4 me, v;
@@ -206,16 +236,16 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
     sbad = 0;
   }
   for (int q = 0; q < rows; q++) {
-    const int64_t x = (g * rows + q) * FZ_MAXM + li;
-    sen[q * FZ_MAXM + li] = (uint32_t)C.ent[x] | ((uint32_t)C.code[x] << 16);
+    const int64_t x = (g * rows + q) * FZ_MAXM + t;
+    sen[q * FZ_MAXM + t] = (uint32_t)C.ent[x] | ((uint32_t)C.code[x] << 16);
   }
-  if (li < WIN_DMAX) {
-    stab[2 * WIN_DMAX + li] = C.dict[g * WIN_DMAX + li];
+  if (t < WIN_DMAX) {
+    stab[2 * WIN_DMAX + t] = C.dict[g * WIN_DMAX + t];
     if (act) {
       const unsigned char *ab = C.actb + g * WIN_ACTB;
-      sact[li] = ((const double4 *)ab)[li];
-      skl[li] = ((const float2 *)(ab + 32 * WIN_DMAX))[li];
-      smode[li] = ((const int8_t *)(ab + 40 * WIN_DMAX))[li];
+      sact[t] = ((const double4 *)ab)[t];
+      skl[t] = ((const float2 *)(ab + 32 * WIN_DMAX))[t];
+      smode[t] = ((const int8_t *)(ab + 40 * WIN_DMAX))[t];
     }
   }
   // f_ext at the first step (loads / spring_pass results), then cleared
@@ -233,17 +263,17 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
   // (kernels.py:55-62), by the first WIN_DMAX threads; computed one step
   // ahead so each step needs one barrier
   auto eff_table = [&](int64_t k) {
-    if (!act || li >= WIN_DMAX || k >= C.n_steps) return;
+    if (!act || t >= WIN_DMAX || k >= C.n_steps) return;
     const double T = __ldg(C.times + k);
-    const double4 A = sact[li];
-    const int m = smode[li];
+    const double4 A = sact[t];
+    const int m = smode[t];
     float f = 1.0f;
     if ((m == 1 || m == 2) && !(m == 2 && !(T >= A.z)))
       f = (float)(1.0 + A.x * sin(A.y * py_mod(T - A.z, A.w)));
     F2 e;
-    e.x = skl[li].x;
-    e.y = skl[li].x * (f * skl[li].y);
-    stab[(k & 1) * WIN_DMAX + li] = e;
+    e.x = skl[t].x;
+    e.y = skl[t].x * (f * skl[t].y);
+    stab[(k & 1) * WIN_DMAX + t] = e;
   };
   eff_table(0);
   __syncthreads();
@@ -265,14 +295,16 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
         ax = ay = az = (R)0;
       } else {
         R gx = 0, gy = 0, gz = 0, bx = 0, by = 0, bz = 0;
-        const uint32_t *e = sen + li;
+        const uint32_t *e = sen + t;
+        // this mass's own entries only (compacted at build), A and B
+        // sections summed separately as the window / split kernels do
 #pragma unroll 4
-        for (int q = 0; q < C.ra; q++) {
+        for (int q = 0; q < n_a; q++) {
           const uint32_t w = e[q * FZ_MAXM];
           win_body(me, pin(w & 0xFFFFu), tab[w >> 16], gx, gy, gz);
         }
 #pragma unroll 4
-        for (int q = C.ra; q < rows; q++) {
+        for (int q = n_a; q < n_ent; q++) {
           const uint32_t w = e[q * FZ_MAXM];
           win_body(me, pin(w & 0xFFFFu), tab[w >> 16], bx, by, bz);
         }
