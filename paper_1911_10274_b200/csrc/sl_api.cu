@@ -1036,8 +1036,8 @@ int build_window_layout(sl_ctx *c) {
   CK(c->win_actb.ensure((size_t)WIN_ACTB * n_tiles));
   CK(c->win_zero.ensure(n_tiles));
   CK(c->win_blk.ensure((size_t)w.bl.slice_bytes * n_tiles * tt));
-  CK(c->win_fail.ensure(16));
-  CK(cudaMemsetAsync(c->win_fail.p, 0, 16, c->st));
+  CK(c->win_fail.ensure(24));
+  CK(cudaMemsetAsync(c->win_fail.p, 0, 24, c->st));
   const int64_t m_pad = c->n_slices * 32;
   k_win_build<<<(unsigned)n_tiles, 256, 0, c->st>>>(
       c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
@@ -1049,17 +1049,19 @@ int build_window_layout(sl_ctx *c) {
       c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
       c->prec == PREC_MIXED ? 1 : 0, c->win_fail.as<unsigned long long>());
   CKL();
-  unsigned long long res[2] = {0, 0};
-  CK(cudaMemcpyAsync(res, c->win_fail.p, 16, cudaMemcpyDeviceToHost, c->st));
+  unsigned long long res[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(res, c->win_fail.p, 24, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   c->launches++;
   if (res[0]) return SL_OK;
-  // stage: record | material table | windows (sized to the widest tile) |
-  // tt slice blocks
+  // stage: record | material table | [actuation block] | windows (sized to
+  // the widest tile) | tt slice blocks.  Without actuated tiles the
+  // actuation block takes no space (config B: 3 stages of 16 slices fit
+  // instead of 2)
   w.cap_rec = (uint32_t)((res[1] + 7) / 8 * 8);
   w.off_dict = sizeof(TileRec);
   w.off_act = w.off_dict + 8 * WIN_DMAX;
-  w.off_win = w.off_act + WIN_ACTB;
+  w.off_win = w.off_act + (res[2] ? WIN_ACTB : 0);
   w.off_slice =
       (w.off_win + (uint32_t)(4 * c->rsz) * w.cap_rec + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
@@ -1072,6 +1074,14 @@ int build_window_layout(sl_ctx *c) {
   w.nst = nst;
   w.off_eff = (uint32_t)nst * w.stage_bytes;
   if (const char *ev = getenv("SL_WIN_DBG")) w.dbg_nocompute = atoi(ev);
+  if (getenv("SL_WIN_INFO"))
+    fprintf(stderr,
+            "[softlat] window layout: %lld tiles of %d slices, cap_rec %u, "
+            "slice %u B, stage %u B (windows %u B), %d stages of %lld B "
+            "opt-in\n",
+            (long long)n_tiles, tt, w.cap_rec, w.bl.slice_bytes,
+            w.stage_bytes, (uint32_t)(4 * c->rsz) * w.cap_rec, nst,
+            (long long)c->smem_optin);
   w.rec = c->win_rec.as<TileRec>();
   w.dict = c->win_dict.as<float2>();
   w.actb = c->win_actb.as<unsigned char>();
