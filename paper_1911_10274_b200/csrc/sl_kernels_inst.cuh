@@ -10,6 +10,28 @@
 
 
 namespace sl {
+// Launch a step kernel with programmatic dependent launch (the kernel
+// waits with griddepcontrol.wait before touching the previous step's
+// output); SL_PDL=0 launches it plainly.
+template <class K, class... A>
+inline void launch_pdl(K kern, int grid, int block, size_t smem,
+                       cudaStream_t st, A... args) {
+  static const bool on = [] {
+    const char *ev = getenv("SL_PDL");
+    return !(ev && ev[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
 // Opt a kernel into dynamic shared memory: always to the device maximum, so
 // contexts of different layouts on one device (partition shards) never
 // shrink the limit under one another's launch; `need` is only checked.
@@ -75,7 +97,7 @@ struct SplitLaunch {
     {
       const size_t sm = win_smem(C);
       win_dispatch(C.tile_slices, [&](auto kern) {
-        kern<<<grid, (C.tile_slices + 1) * 32, sm, st>>>(S, E, T, C);
+        launch_pdl(kern, grid, (C.tile_slices + 1) * 32, sm, st, S, E, T, C);
       });
     }
   }
@@ -151,8 +173,8 @@ struct SplitLaunch<PREC_FP64> {
 #ifdef SL_UNIT_FP64
   static void win(const KState &S, const EnvP &E, const StepP &T,
                   const WinCfg &C, int grid, cudaStream_t st) {
-    k_win_tma<PREC_FP64, SL_WIN64_T>
-        <<<grid, (SL_WIN64_T + 1) * 32, win_smem(C), st>>>(S, E, T, C);
+    launch_pdl(k_win_tma<PREC_FP64, SL_WIN64_T>, grid,
+               (SL_WIN64_T + 1) * 32, win_smem(C), st, S, E, T, C);
   }
   static int win_setup(const WinCfg &C) {
     return smem_optin(k_win_tma<PREC_FP64, SL_WIN64_T>, win_smem(C));
