@@ -801,9 +801,18 @@ __device__ __forceinline__ void initial_force(const KState &S, int64_t i,
 // Fused step, plain variant: one thread per mass, entries read straight
 // from global memory.  Used for spring_pass (FORCE_ONLY), for tiny bodies
 // and for layouts with very wide slices (hub masses).
+// Programmatic dependent launch: let the next step kernel launch now and
+// wait here for the previous one's completion (and memory) before reading
+// anything it wrote.  A no-op for ordinary launches.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 template <int P, bool FORCE_ONLY>
 static __global__ void __launch_bounds__(256)
     k_gather_step(const KState S, const EnvP E, const StepP T) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
@@ -932,6 +941,7 @@ template <int P>
 static __global__ void __launch_bounds__(384)
     k_gather_tma(const KState S, const EnvP E, const StepP T,
                  const TmaCfg C) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
@@ -1082,6 +1092,7 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
 template <int P, bool SPECIAL>
 static __global__ void __launch_bounds__(256)
     k_spring_atomic(const KState S, const StepP T) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using F = typename Tr<P>::M;
   using FS = typename Tr<P>::F;
@@ -1133,6 +1144,7 @@ static __global__ void __launch_bounds__(256)
 template <int P>
 static __global__ void __launch_bounds__(256)
     k_mass(const KState S, const EnvP E, const StepP T) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

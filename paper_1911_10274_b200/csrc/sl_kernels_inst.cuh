@@ -55,7 +55,7 @@ struct SplitLaunch {
   template <bool FO, bool ACT>
   static void step_k(const KState &S, const EnvP &E, const StepP &T,
                      const ActP &A, cudaStream_t st) {
-    k_split_step<P, FO, ACT><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T, A);
+    launch_pdl(k_split_step<P, FO, ACT>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T, A);
   }
   static void step(const KState &S, const EnvP &E, const StepP &T,
                    const ActP &A, cudaStream_t st, bool force_only) {
@@ -73,7 +73,7 @@ struct SplitLaunch {
                     const SplitCfg &C, const ActP &A, int grid,
                     cudaStream_t st) {
     size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);
-    k_split_tma<P, U, ACT><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C, A);
+    launch_pdl(k_split_tma<P, U, ACT>, grid, 32 * C.warps, sm, st, S, E, T, C, A);
   }
   static void tma(const KState &S, const EnvP &E, const StepP &T,
                   const SplitCfg &C, const ActP &A, int grid,
@@ -195,31 +195,31 @@ struct SplitLaunch<PREC_FP64> {
   namespace {                                                                \
   void FN##_gather(const KState &S, const EnvP &E, const StepP &T,           \
                    cudaStream_t st) {                                        \
-    if (S.m_n > 0) k_gather_step<PREC, false><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
+    if (S.m_n > 0) launch_pdl(k_gather_step<PREC, false>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T); \
   }                                                                          \
   void FN##_tma(const KState &S, const EnvP &E, const StepP &T,             \
                const TmaCfg &C, int grid, cudaStream_t st) {                 \
     size_t sm = (size_t)C.warps * (2 * C.stage_bytes + 16);                  \
-    k_gather_tma<PREC><<<grid, 32 * C.warps, sm, st>>>(S, E, T, C);          \
+    launch_pdl(k_gather_tma<PREC>, grid, 32 * C.warps, sm, st, S, E, T, C);  \
   }                                                                          \
   int FN##_tma_setup(int smem_bytes) {                                       \
     return smem_optin(k_gather_tma<PREC>, (size_t)smem_bytes);               \
   }                                                                          \
   void FN##_force(const KState &S, const EnvP &E, const StepP &T,            \
                   cudaStream_t st) {                                         \
-    if (S.m_n > 0) k_gather_step<PREC, true><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
+    if (S.m_n > 0) launch_pdl(k_gather_step<PREC, true>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T); \
   }                                                                          \
   void FN##_spring(const KState &S, const StepP &T, bool special,            \
                    cudaStream_t st) {                                        \
     if (S.s_n <= 0) return;                                                  \
     if (special)                                                             \
-      k_spring_atomic<PREC, true><<<blocks_for(S.s_n), 256, 0, st>>>(S, T);  \
+      launch_pdl(k_spring_atomic<PREC, true>, (int)blocks_for(S.s_n), 256, 0, st, S, T); \
     else                                                                     \
-      k_spring_atomic<PREC, false><<<blocks_for(S.s_n), 256, 0, st>>>(S, T); \
+      launch_pdl(k_spring_atomic<PREC, false>, (int)blocks_for(S.s_n), 256, 0, st, S, T); \
   }                                                                          \
   void FN##_mass(const KState &S, const EnvP &E, const StepP &T,             \
                  cudaStream_t st) {                                          \
-    if (S.m_n > 0) k_mass<PREC><<<blocks_for(S.m_n), 256, 0, st>>>(S, E, T); \
+    if (S.m_n > 0) launch_pdl(k_mass<PREC>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T); \
   }                                                                          \
   void FN##_split(const KState &S, const EnvP &E, const StepP &T,           \
                   const ActP &A, cudaStream_t st) {                          \

@@ -414,6 +414,7 @@ __device__ __forceinline__ void split_forces(
 template <int P, bool FORCE_ONLY, bool ACT>
 static __global__ void __launch_bounds__(256)
     k_split_step(const KState S, const EnvP E, const StepP T, const ActP A) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
@@ -453,6 +454,7 @@ template <int P, int U, bool ACT>
 static __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
     k_split_tma(const KState S, const EnvP E, const StepP T,
                 const SplitCfg C, const ActP A) {
+  pdl_wait();
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
