@@ -17,6 +17,11 @@ python bench.py --steps 100 --warmup 5 --accumulation atomic --no-e2e --no-cpu-b
 SL_DISABLE_WIN=1 python bench.py --steps 300 --warmup 10 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_split_$tag.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
     --log-file $out/launches_$tag.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+# the step kernels only (3 warm-up + 10 timed steps; the setup launches are
+# in launches_TAG)
+ncu --metrics gpu__time_duration.sum --clock-control none \
+    -k regex:"k_win_tma|k_fused|k_split_step|k_split_tma|k_gather|k_spring|k_mass" -c 100 --csv \
+    --log-file $out/launches_timed_$tag.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_win_tma -s 6 -c 1 \
     -o $out/prof_$tag -f python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $out/ncu_full_$tag.log 2>&1
 tail -1 $out/ncu_full_$tag.log
