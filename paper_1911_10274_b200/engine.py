@@ -435,7 +435,12 @@ def check_stability(store: ObjectStore, dt: float,
         m_min = _native.masked_extrema(store._m_mass[:mn], alive)[0] \
             if n_alive else np.inf
         k_springs = 0.0
-        if sn:  # np.max(..., initial=0.0): NaN propagates
+        kc = getattr(store, "_kmax_cache", None)
+        if sn and kc is not None and kc[0] == (store.topology_version,
+                                               store.spring_param_version,
+                                               sn):
+            k_springs = max(kc[1], 0.0) if kc[1] == kc[1] else kc[1]
+        elif sn:  # np.max(..., initial=0.0): NaN propagates
             hi = _native.masked_extrema(store._s_k[:sn],
                                         store._s_alive[:sn])[1]
             k_springs = hi if (hi != hi or hi > 0.0) else 0.0
