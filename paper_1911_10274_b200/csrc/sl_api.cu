@@ -745,6 +745,7 @@ KState make_state(sl_ctx *c) {
       S.fz_zero = c->fz_zero.as<uint8_t>();
       S.fz_rows = c->fcfg.ra + c->fcfg.rb;
       S.fz_ra = c->fcfg.ra;
+      S.fz_maxm = c->fcfg.maxm;
     }
     if (c->win) {
       S.win_blk = c->win_blk.as<unsigned char>();
@@ -1182,15 +1183,28 @@ int build_fused_groups(sl_ctx *c) {
   CK(cudaMemcpyAsync(diff.data(), c->fz_diff.p, 4 * (m_n + 1),
                      cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  // pack consecutive components into groups of <= FZ_MAXM masses
+  // group capacity: 512 masses (two CTAs per SM) unless a component needs
+  // up to 1024 (one 1024-thread CTA per SM)
+  int maxm = FZ_MAXM;
+  {
+    int64_t cov = 0, c0 = 0;
+    for (int64_t b = 1; b <= m_n; b++) {
+      cov += diff[b];
+      if (b < m_n && cov != 0) continue;
+      if (b - c0 > FZ_MAXM_L) return SL_OK;  // a body too large for a CTA
+      if (b - c0 > FZ_MAXM) maxm = FZ_MAXM_L;
+      c0 = b;
+    }
+  }
+  // pack consecutive components into groups of <= maxm masses
   std::vector<int32_t> gs, gc;
   int64_t cover = 0, comp0 = 0, g0 = 0;
   for (int64_t b = 1; b <= m_n; b++) {
     cover += diff[b];
     if (b < m_n && cover != 0) continue;  // (b - 1, b) is spanned
     const int64_t len = b - comp0;        // component [comp0, b)
-    if (len > FZ_MAXM) return SL_OK;      // a body too large for a CTA
-    if (b - g0 > FZ_MAXM) {               // close the group before comp0
+    if (len > maxm) return SL_OK;         // (checked above)
+    if (b - g0 > maxm) {                  // close the group before comp0
       gs.push_back((int32_t)g0);
       gc.push_back((int32_t)(comp0 - g0));
       g0 = comp0;
@@ -1204,12 +1218,12 @@ int build_fused_groups(sl_ctx *c) {
   const int rows = std::max(1, ra + rb);
   CK(c->fz_gstart.ensure(4 * ng));
   CK(c->fz_gcount.ensure(4 * ng));
-  CK(c->fz_ent.ensure((size_t)2 * ng * rows * FZ_MAXM));
-  CK(c->fz_code.ensure((size_t)ng * rows * FZ_MAXM));
-  CK(c->fz_epos.ensure((size_t)2 * ng * rows * FZ_MAXM));
-  CK(c->fz_perm.ensure((size_t)2 * ng * FZ_MAXM));
-  CK(c->fz_cnt.ensure((size_t)ng * FZ_MAXM));
-  CK(c->fz_cnt_a.ensure((size_t)ng * FZ_MAXM));
+  CK(c->fz_ent.ensure((size_t)2 * ng * rows * maxm));
+  CK(c->fz_code.ensure((size_t)ng * rows * maxm));
+  CK(c->fz_epos.ensure((size_t)2 * ng * rows * maxm));
+  CK(c->fz_perm.ensure((size_t)2 * ng * maxm));
+  CK(c->fz_cnt.ensure((size_t)ng * maxm));
+  CK(c->fz_cnt_a.ensure((size_t)ng * maxm));
   CK(c->fz_dict.ensure((size_t)8 * WIN_DMAX * ng));
   CK(c->fz_actb.ensure((size_t)WIN_ACTB * ng));
   CK(c->fz_has.ensure(ng));
@@ -1222,7 +1236,9 @@ int build_fused_groups(sl_ctx *c) {
                      cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->fz_fail.p, 0, 8, c->st));
   const int64_t m_pad = c->n_slices * 32;
-  k_fused_build<<<(unsigned)ng, FZ_MAXM, 0, c->st>>>(
+  auto build = maxm > FZ_MAXM ? k_fused_build<FZ_MAXM_L>
+                              : k_fused_build<FZ_MAXM>;
+  build<<<(unsigned)ng, maxm, 0, c->st>>>(
       c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
       c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
       c->s_grp.as<uint8_t>(), c->vel.as<float4>(), c->sp_a, c->sp_rows,
@@ -1255,10 +1271,11 @@ int build_fused_groups(sl_ctx *c) {
   f.has_act = c->fz_has.as<uint8_t>();
   f.ra = ra;
   f.rb = rb;
-  const size_t smem = 32 * WIN_DMAX + 16 * 2 * (FZ_MAXM + 1) +
-                      8 * 4 * WIN_DMAX + (size_t)4 * rows * FZ_MAXM +
+  const size_t smem = 32 * WIN_DMAX + 16 * 2 * (maxm + 1) +
+                      8 * 4 * WIN_DMAX + (size_t)4 * rows * maxm +
                       WIN_DMAX;
-  if (launchers(c->prec).fused_setup(smem) != 0) {
+  f.maxm = maxm;
+  if (launchers(c->prec).fused_setup(smem, maxm) != 0) {
     cudaGetLastError();
     return SL_OK;
   }

@@ -120,12 +120,12 @@ struct KState {
   uint32_t win_sb, win_oac, win_obc;
   int win_tt;
   // multi-step fused groups (sl_fused.cuh; null when not built): material
-  // codes [group][rows][512], group of every mass, group starts / zero codes
+  // codes [group][rows][maxm], group of every mass, group starts / zero codes
   uint8_t *fz_code;
   const uint16_t *fz_epos;  // split row of a mass -> compacted row, thread
   const int32_t *fz_gid, *fz_gstart;
   const uint8_t *fz_zero;
-  int fz_rows, fz_ra;
+  int fz_rows, fz_ra, fz_maxm;
   // status: [0..2] counters, [3] err_slot (max slot+1), [4] err step+1
   unsigned long long *status;
 };
@@ -1056,10 +1056,11 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
         const int64_t i = sl * 32 + (rem & 31);
         const int row = q == 0 ? rem >> 5 : S.fz_ra + (rem >> 5) - (1 << S.sp_a);
         const int32_t g = S.fz_gid[i];
+        const int mm = S.fz_maxm;
         const uint32_t qt =
-            S.fz_epos[((int64_t)g * S.fz_rows + row) * 512 +
+            S.fz_epos[((int64_t)g * S.fz_rows + row) * mm +
                       (i - S.fz_gstart[g])];
-        S.fz_code[((int64_t)g * S.fz_rows + (qt >> 9)) * 512 + (qt & 511)] =
+        S.fz_code[((int64_t)g * S.fz_rows + qt / mm) * mm + qt % mm] =
             S.fz_zero[g];
       }
     }
@@ -1195,7 +1196,7 @@ struct Launch {
   // multi-step fused small-body kernel (fp32, sl_fused.cuh)
   void (*fused)(const KState &, const EnvP &, const struct FzCfg &,
                 double dt, size_t smem, cudaStream_t);
-  int (*fused_setup)(size_t smem);
+  int (*fused_setup)(size_t smem, int maxm);
 };
 
 const Launch &launchers(int prec);

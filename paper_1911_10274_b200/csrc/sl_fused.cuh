@@ -4,7 +4,8 @@
 //
 // Config D (an RL batch of thousands of 5^3 robots) is a swarm of small
 // disconnected bodies.  Bodies are packed into GROUPS of whole connected
-// components (<= FZ_MAXM masses; the host finds component boundaries from
+// components (<= 512 masses, or <= 1024 with 1024-thread CTAs when a body
+// needs it; the host finds component boundaries from
 // the springs), one CTA per group, one thread per mass.  The group's
 // positions (double-buffered), its incidence entries (16-bit local partner
 // + 8-bit material code, A section then B section per mass, the split
@@ -28,23 +29,26 @@
 
 namespace sl {
 
-constexpr int FZ_MAXM = 512;  // masses per group = threads per CTA
+constexpr int FZ_MAXM = 512;    // masses per group = threads per CTA
+constexpr int FZ_MAXM_L = 1024;  // large groups (bodies of 513..1024 masses,
+                                 // e.g. the 10^3 cube of config A): 1 CTA/SM
 constexpr int FZ_MAXR = 32;   // entry rows per mass (A + B)
 
 struct FzCfg {
   int64_t n_groups;
   const int32_t *gstart;  // [g] first mass of the group
   const int32_t *gcount;  // [g] masses
-  const uint16_t *ent;    // [g][ra + rb][FZ_MAXM] local partner of the
-                          // q-th entry of thread t (FZ_MAXM: sentinel)
-  const uint8_t *code;    // [g][ra + rb][FZ_MAXM] material code
-  const uint16_t *perm;   // [g][FZ_MAXM] thread t -> local mass
-  const uint8_t *cnt;     // [g][FZ_MAXM] entries of thread t
-  const uint8_t *cnt_a;   // [g][FZ_MAXM] of which A-section entries
+  const uint16_t *ent;    // [g][ra + rb][maxm] local partner of the
+                          // q-th entry of thread t (maxm: sentinel)
+  const uint8_t *code;    // [g][ra + rb][maxm] material code
+  const uint16_t *perm;   // [g][maxm] thread t -> local mass
+  const uint8_t *cnt;     // [g][maxm] entries of thread t
+  const uint8_t *cnt_a;   // [g][maxm] of which A-section entries
   const float2 *dict;     // [g][WIN_DMAX] (k, k L0)
   const unsigned char *actb;  // [g][WIN_ACTB] actuation block (window fmt)
   const uint8_t *has_act;     // [g]
   int ra, rb;                 // A / B rows per mass
+  int maxm;                   // group capacity (threads per CTA): 512 / 1024
   void *vel_out;              // final velocities (swapped in on success)
   const double *times;        // [n_steps] step times (device)
   int64_t n_steps;
@@ -55,7 +59,8 @@ struct FzCfg {
 // Group build: one CTA per group, one thread per mass.  fail[0] |= 1 when
 // the group does not fit (partner outside the group, too many materials,
 // special mass, hash collision).
-static __global__ void __launch_bounds__(FZ_MAXM)
+template <int M>
+static __global__ void __launch_bounds__(M)
     k_fused_build(const uint32_t *sp_j, const uint32_t *sp_w,
                   const float2 *sp_kl, const int32_t *sp_s, const int8_t *mode,
                   const double4 *act, const uint8_t *grp, const float4 *vel,
@@ -66,7 +71,7 @@ static __global__ void __launch_bounds__(FZ_MAXM)
                   unsigned char *actb,
                   uint8_t *has_act, uint8_t *zero, int32_t *gid,
                   unsigned long long *fail) {
-  __shared__ int16_t scnt[FZ_MAXM];
+  __shared__ int16_t scnt[M];
   __shared__ unsigned long long dkey[WIN_DMAX];
   __shared__ float2 dkl[WIN_DMAX];
   __shared__ double4 dact[WIN_DMAX];
@@ -129,13 +134,13 @@ static __global__ void __launch_bounds__(FZ_MAXM)
   // (stable), so a warp's 32 masses have similar counts and its loop runs
   // to about their own count instead of the group's maximum row count
   int t = 0;
-  for (int j = 0; j < FZ_MAXM; j++) {
+  for (int j = 0; j < M; j++) {
     const int cj = scnt[j];
     t += cj > scnt[li] || (cj == scnt[li] && j < li);
   }
-  perm[g * FZ_MAXM + t] = (uint16_t)li;
-  cnt[g * FZ_MAXM + t] = (uint8_t)(mine ? n_mine : 0);
-  cnt_a[g * FZ_MAXM + t] = (uint8_t)(mine ? n_a : 0);
+  perm[g * M + t] = (uint16_t)li;
+  cnt[g * M + t] = (uint8_t)(mine ? n_mine : 0);
+  cnt_a[g * M + t] = (uint8_t)(mine ? n_a : 0);
   const int zc = tab.find(zero_key, false, nullptr);
   if (mine) gid[i] = (int32_t)g;
   if (li == 0) zero[g] = (uint8_t)(zc < 0 ? 0 : zc);
@@ -147,16 +152,16 @@ static __global__ void __launch_bounds__(FZ_MAXM)
     const Mat x = mat_of_spring(sp_kl, mode, act, grp, kli, s);
     const int c = tab.find(mat_hash(x), false, nullptr);
     if (!tab.same(c, x)) ok = 0;
-    const int64_t o = (g * (ra + rb) + qq) * FZ_MAXM + t;
+    const int64_t o = (g * (ra + rb) + qq) * M + t;
     ent[o] = (uint16_t)(j - (uint32_t)g0);
     code[o] = (uint8_t)(c < 0 ? 0 : c);
     // split row q of mass li -> (compacted row, thread): device kills
-    epos[(g * (ra + rb) + q) * FZ_MAXM + li] = (uint16_t)(qq * FZ_MAXM + t);
+    epos[(g * (ra + rb) + q) * M + li] = (uint16_t)(qq * M + t);
     qq++;
   }
   for (; qq < ra + rb; qq++) {  // padding (never read: the loop stops at cnt)
-    const int64_t o = (g * (ra + rb) + qq) * FZ_MAXM + t;
-    ent[o] = FZ_MAXM;
+    const int64_t o = (g * (ra + rb) + qq) * M + t;
+    ent[o] = M;
     code[o] = (uint8_t)(zc < 0 ? 0 : zc);
   }
   __syncthreads();
@@ -182,11 +187,11 @@ static __global__ void __launch_bounds__(FZ_MAXM)
 }
 
 // The fused multi-step kernel (fp32).  Dynamic shared memory:
-//   act (WIN_DMAX double4) | pos [2][FZ_MAXM + 1] float4 | tables [2] +
+//   act (WIN_DMAX double4) | pos [2][M + 1] xy + z | tables [2] +
 //   static table (3 x WIN_DMAX float2) | raw (k, L0) (WIN_DMAX float2) |
-//   entries (rows x FZ_MAXM u32: partner | code << 16) | modes
-template <int P>
-static __global__ void __launch_bounds__(FZ_MAXM, 2)
+//   entries (rows x M u32: partner | code << 16) | modes
+template <int P, int M>
+static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
     k_fused_small(const KState S, const EnvP E, const FzCfg C, double dt) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
@@ -196,21 +201,21 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
   double4 *sact = (double4 *)smem;
   // positions as xy pairs + z (the partner's mass is never read): one
   // 8 B + one 4 B shared load per entry, 3 wavefronts instead of 4
-  float2 *sxy = (float2 *)(sact + WIN_DMAX);       // [2][FZ_MAXM + 1]
-  float *sz = (float *)(sxy + 2 * (FZ_MAXM + 1));  // [2][FZ_MAXM + 1]
-  F2 *stab = (F2 *)(sz + 2 * (FZ_MAXM + 1) + 2 * (FZ_MAXM + 1));  // [3][..]
+  float2 *sxy = (float2 *)(sact + WIN_DMAX);       // [2][M + 1]
+  float *sz = (float *)(sxy + 2 * (M + 1));  // [2][M + 1]
+  F2 *stab = (F2 *)(sz + 2 * (M + 1) + 2 * (M + 1));  // [3][..]
   F2 *skl = stab + 3 * WIN_DMAX;
   // entries packed as partner | code << 16: one shared load per entry
   uint32_t *sen = (uint32_t *)(skl + WIN_DMAX);
-  int8_t *smode = (int8_t *)(sen + rows * FZ_MAXM);
+  int8_t *smode = (int8_t *)(sen + rows * M);
   __shared__ int sbad;
   const int64_t g = blockIdx.x;
   const int t = threadIdx.x;  // thread slot (masses sorted by entry count)
   const int32_t g0 = C.gstart[g], gn = C.gcount[g];
   const bool mine = t < gn;
-  const int li = mine ? (int)C.perm[g * FZ_MAXM + t] : t;  // local mass
-  const int n_ent = mine ? (int)C.cnt[g * FZ_MAXM + t] : 0;
-  const int n_a = mine ? (int)C.cnt_a[g * FZ_MAXM + t] : 0;
+  const int li = mine ? (int)C.perm[g * M + t] : t;  // local mass
+  const int n_ent = mine ? (int)C.cnt[g * M + t] : 0;
+  const int n_a = mine ? (int)C.cnt_a[g * M + t] : 0;
   const int64_t i = (int64_t)g0 + li;
   const bool act = C.has_act[g] != 0;
   // ---- load the group
@@ -231,13 +236,13 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
     R4 far;
     far.x = far.y = far.z = (R)SENTINEL_POS;
     far.w = (R)0;
-    sxy[FZ_MAXM] = sxy[2 * FZ_MAXM + 1] = make_float2(far.x, far.y);
-    sz[FZ_MAXM] = sz[2 * FZ_MAXM + 1] = far.z;
+    sxy[M] = sxy[2 * M + 1] = make_float2(far.x, far.y);
+    sz[M] = sz[2 * M + 1] = far.z;
     sbad = 0;
   }
   for (int q = 0; q < rows; q++) {
-    const int64_t x = (g * rows + q) * FZ_MAXM + t;
-    sen[q * FZ_MAXM + t] = (uint32_t)C.ent[x] | ((uint32_t)C.code[x] << 16);
+    const int64_t x = (g * rows + q) * M + t;
+    sen[q * M + t] = (uint32_t)C.ent[x] | ((uint32_t)C.code[x] << 16);
   }
   if (t < WIN_DMAX) {
     stab[2 * WIN_DMAX + t] = C.dict[g * WIN_DMAX + t];
@@ -282,8 +287,8 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
   for (; k < C.n_steps; k++) {
     const int b = (int)(k & 1);
     const F2 *tab = act ? stab + b * WIN_DMAX : stab + 2 * WIN_DMAX;
-    const float2 *pxy = sxy + b * (FZ_MAXM + 1);
-    const float *pz = sz + b * (FZ_MAXM + 1);
+    const float2 *pxy = sxy + b * (M + 1);
+    const float *pz = sz + b * (M + 1);
     auto pin = [&](uint32_t p) {
       const float2 xy = pxy[p];
       return make_float4(xy.x, xy.y, pz[p], 0.f);
@@ -300,12 +305,12 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
         // sections summed separately as the window / split kernels do
 #pragma unroll 4
         for (int q = 0; q < n_a; q++) {
-          const uint32_t w = e[q * FZ_MAXM];
+          const uint32_t w = e[q * M];
           win_body(me, pin(w & 0xFFFFu), tab[w >> 16], gx, gy, gz);
         }
 #pragma unroll 4
         for (int q = n_a; q < n_ent; q++) {
-          const uint32_t w = e[q * FZ_MAXM];
+          const uint32_t w = e[q * M];
           win_body(me, pin(w & 0xFFFFu), tab[w >> 16], bx, by, bz);
         }
         const R fx = f0x + (gx + bx), fy = f0y + (gy + by),
@@ -320,8 +325,8 @@ static __global__ void __launch_bounds__(FZ_MAXM, 2)
         if (!(z0 == (R)0)) sbad = 1;  // zero-length spring or blow-up
       }
     }
-    sxy[(b ^ 1) * (FZ_MAXM + 1) + li] = make_float2(np.x, np.y);
-    sz[(b ^ 1) * (FZ_MAXM + 1) + li] = np.z;
+    sxy[(b ^ 1) * (M + 1) + li] = make_float2(np.x, np.y);
+    sz[(b ^ 1) * (M + 1) + li] = np.z;
     me = np;
     eff_table(k + 1);  // the other buffer: nobody reads it this step
     __syncthreads();

@@ -120,16 +120,23 @@ struct SplitLaunch {
       }
     }
   }
-  // multi-step fused small-body kernel (fp32 only)
+  // multi-step fused small-body kernel (fp32 only); C.maxm = 512 (two
+  // CTAs per SM) or 1024 (bodies of up to 1024 masses, one CTA per SM)
   static void fused(const KState &S, const EnvP &E, const FzCfg &C,
                     double dt, size_t smem, cudaStream_t st) {
-    if constexpr (P == PREC_FP32)
-      k_fused_small<P><<<(unsigned)C.n_groups, FZ_MAXM, smem, st>>>(S, E, C,
-                                                                   dt);
+    if constexpr (P == PREC_FP32) {
+      if (C.maxm > FZ_MAXM)
+        k_fused_small<P, FZ_MAXM_L>
+            <<<(unsigned)C.n_groups, FZ_MAXM_L, smem, st>>>(S, E, C, dt);
+      else
+        k_fused_small<P, FZ_MAXM>
+            <<<(unsigned)C.n_groups, FZ_MAXM, smem, st>>>(S, E, C, dt);
+    }
   }
-  static int fused_setup(size_t smem) {
+  static int fused_setup(size_t smem, int maxm) {
     if constexpr (P == PREC_FP32)
-      return smem_optin(k_fused_small<P>, smem);
+      return maxm > FZ_MAXM ? smem_optin(k_fused_small<P, FZ_MAXM_L>, smem)
+                            : smem_optin(k_fused_small<P, FZ_MAXM>, smem);
     return 1;
   }
   static int win_setup(const WinCfg &C) {
@@ -186,7 +193,7 @@ struct SplitLaunch<PREC_FP64> {
 #endif
   static void fused(const KState &, const EnvP &, const FzCfg &, double,
                     size_t, cudaStream_t) {}
-  static int fused_setup(size_t) { return 1; }
+  static int fused_setup(size_t, int) { return 1; }
 };
 }  // namespace sl
 
@@ -248,8 +255,8 @@ struct SplitLaunch<PREC_FP64> {
                   size_t smem, cudaStream_t st) {                            \
     SplitLaunch<PREC>::fused(S, E, C, dt, smem, st);                         \
   }                                                                          \
-  int FN##_fused_setup(size_t smem) {                                        \
-    return SplitLaunch<PREC>::fused_setup(smem);                             \
+  int FN##_fused_setup(size_t smem, int maxm) {                              \
+    return SplitLaunch<PREC>::fused_setup(smem, maxm);                       \
   }                                                                          \
   }                                                                          \
   const Launch &FN() {                                                       \

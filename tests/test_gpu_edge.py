@@ -44,7 +44,9 @@ def _ragged(big=False):
     y = 0.0
     shapes = [(3, 3, 3), (4, 5, 2), (40, 1, 1), (2, 2, 2)]
     if big:
-        shapes.insert(1, (10, 9, 8))  # 720 masses: one component > 512
+        # 1100 masses: one component > 1024 (the fused kernel's largest
+        # group), so the per-step window kernel runs
+        shapes.insert(1, (11, 10, 10))
     for nx, ny, nz in shapes:
         body = build_lattice(LatticeSpec(Vec3(0, y, 0.01), nx, ny, nz, 0.05,
                                          Material(1e5, 1000.0)), st)
@@ -101,7 +103,7 @@ def test_single_spring(precision):
 def test_ragged_swarm(big):
     case = _case(_ragged(big), _env())
     pos, vel, ref, st = _run(case, "fp32")
-    # small components only: the fused multi-step kernel; with a 720-mass
+    # small components only: the fused multi-step kernel; with a 1100-mass
     # body: per-step window kernel
     assert (st["fused_launches"] > 0) == (not big)
     assert rel_maxnorm(pos, ref["m_pos"]) < 1e-4

@@ -119,3 +119,22 @@ def test_fused_abort_reruns_per_step():
     assert np.array_equal(f["degen"], p["degen"])
     assert f["c"].tolist() == p["c"].tolist()
     assert f["degen"][0] == 1
+
+
+@pytest.mark.parametrize("dims", [(10, 10, 10), (9, 11, 8), (12, 9, 9)])
+def test_fused_large_body_1024_threads(dims):
+    """A single body of 513..1024 masses (the config-A 10^3 cube) runs in
+    the 1024-thread variant: one CTA holds the whole body for all steps."""
+    case = _lattice_case(*dims)
+    dt, n = 1e-4, 80
+    times = np.arange(n, dtype=np.float64) * dt
+    f = _run(case, times, dt, True, chunks=(30,))
+    p = _run(case, times, dt, False, chunks=(30,))
+    assert f["st"]["fused_groups"] == 1 and f["st"]["fused_launches"] == 2
+    assert f["st"]["fused_aborts"] == 0
+    assert rel_maxnorm(f["pos"], p["pos"]) < 1e-6
+    assert rel_maxnorm(f["vel"], p["vel"]) < 1e-5
+    assert np.array_equal(f["alive"], p["alive"])
+    ref = _oracle(case, times, dt)
+    assert rel_maxnorm(f["pos"], ref["m_pos"]) < 1e-4
+    assert rel_maxnorm(f["vel"], ref["m_vel"]) < 5e-4
