@@ -43,10 +43,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="B", choices=["B", "D"],
+    ap.add_argument("--config", default="B", choices=["A", "B", "D"],
                     help="B: one 100^3 lattice per rank (batched instances);"
                          " D: --robots actuated 5^3 robots sharded over "
-                         "the ranks (RL batch)")
+                         "the ranks (RL batch); A: the reference's bouncing "
+                         "10^3 cube (scenarios/bouncing_cube.ini) per rank")
     ap.add_argument("--n", "--edge", dest="n", type=int, default=100,
                     help="lattice edge (--edge under torchrun, whose parser "
                          "reads --n as ambiguous)")
@@ -69,6 +70,22 @@ def build_workload(n: int):
     body = build_lattice(LatticeSpec(Vec3(0, 0, 0), n, n, n, 0.05,
                                      Material(1e5, 1000.0)), st)
     st._m_pos[body.mass_handles.slots] *= 1.01
+    env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
+        normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
+        static_friction=1.0, kinetic_friction=0.8)])
+    return st, env
+
+
+def build_cube():
+    """Config A (scenarios/bouncing_cube.ini): a 10^3
+    lattice, corner (0, 0, 0.3), spacing 0.1, E = 1e6, rho = 1000, d = 1 mm,
+    falling onto a ground plane k = 2000, mu_s = 1, mu_k = 0.8."""
+    from paper_1911_10274_b200 import (ContactPlane, Environment, Material,
+                                       ObjectStore, Vec3)
+    from paper_1911_10274_b200.builder import LatticeSpec, build_lattice
+    st = ObjectStore()
+    build_lattice(LatticeSpec(Vec3(0, 0, 0.3), 10, 10, 10, 0.1,
+                              Material(1e6, 1000.0), 1e-3), st)
     env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
         normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
         static_friction=1.0, kinetic_friction=0.8)])
@@ -105,6 +122,11 @@ def make_workload(args, rank: int, world: int):
                 f"friction ground plane, sharded over {world} rank(s), "
                 f"{args.precision}, {args.accumulation}")
         return st, env, desc, ("strong" if world > 1 else "weak"), 1
+    if args.config == "A":
+        st, env = build_cube()
+        desc = (f"A: 10^3 bouncing cube (scenarios/bouncing_cube.ini) per "
+                f"rank, {args.precision}, {args.accumulation}")
+        return st, env, desc, "weak", 0
     st, env = build_workload(args.n)
     desc = (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
             f"x1.01 stretch, {args.precision}, {args.accumulation}")
@@ -370,7 +392,7 @@ def main():
         sec = float(reduce_(sec, dist.ReduceOp.MAX, torch.float64))
         dist.barrier()
     total_springs = springs * world
-    if dist is not None and args.config != "B":
+    if dist is not None and args.config == "D":
         import torch
         total_springs = int(reduce_(springs, dist.ReduceOp.SUM, torch.int64))
     value = total_springs * args.steps / sec
@@ -383,7 +405,8 @@ def main():
     achieved = algo / (sec / args.steps) / 1e9
     key = (f"{args.n}^3/{args.precision}/{args.accumulation}"
            if args.config == "B" else
-           f"D{args.robots}/{args.precision}/{args.accumulation}")
+           f"{args.config}{args.robots if args.config == 'D' else ''}/"
+           f"{args.precision}/{args.accumulation}")
     traffic = committed_traffic(key)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -452,14 +475,16 @@ def main():
                 "config": {"workload": workload, "masses": masses,
                            "springs": springs,
                            "total_springs": total_springs,
-                           "per_gpu_instances": (1 if args.config == "B"
-                                                 else "robot shard"),
+                           "per_gpu_instances": (
+                               "robot shard" if args.config == "D" else 1),
                            "precision": args.precision,
                            "accumulation": args.accumulation,
                            "l2": ("working set > 126 MB L2 every step "
                                   "(no flush needed)" if args.config == "B"
-                                  else "working set may fit L2 (config D "
-                                       "shards); no flush"),
+                                  and args.n >= 100 else
+                                  "working set fits L2 (small bodies / "
+                                  "shards); no flush: an L2-resident "
+                                  "simulation is the workload"),
                            "parallelism": f"batched instances x{world}"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk,

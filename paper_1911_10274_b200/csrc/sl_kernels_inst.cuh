@@ -178,12 +178,19 @@ struct SplitLaunch<PREC_FP64> {
   // compiled with FMA contraction in another unit could be the one a launch
   // binds to (tests/test_abi.py checks each cubin's instantiations).
 #ifdef SL_UNIT_FP64
+  // T = SL_WIN64_T (12); 4-slice tiles for small meshes (more CTAs)
   static void win(const KState &S, const EnvP &E, const StepP &T,
                   const WinCfg &C, int grid, cudaStream_t st) {
-    launch_pdl(k_win_tma<PREC_FP64, SL_WIN64_T>, grid,
-               (SL_WIN64_T + 1) * 32, win_smem(C), st, S, E, T, C);
+    if (C.tile_slices == 4)
+      launch_pdl(k_win_tma<PREC_FP64, 4>, grid, 5 * 32, win_smem(C), st, S,
+                 E, T, C);
+    else
+      launch_pdl(k_win_tma<PREC_FP64, SL_WIN64_T>, grid,
+                 (SL_WIN64_T + 1) * 32, win_smem(C), st, S, E, T, C);
   }
   static int win_setup(const WinCfg &C) {
+    if (C.tile_slices == 4)
+      return smem_optin(k_win_tma<PREC_FP64, 4>, win_smem(C));
     return smem_optin(k_win_tma<PREC_FP64, SL_WIN64_T>, win_smem(C));
   }
 #else
