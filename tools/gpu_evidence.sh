@@ -11,6 +11,8 @@ python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 | tee $out/smo
 python bench.py 2>&1 | tail -1 | tee $out/bench_$tag.json
 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1 | tee $out/bench_ref_$tag.json
 python bench.py --config D --steps 300 --warmup 10 2>&1 | tail -1 | tee $out/bench_D_$tag.json
+python bench.py --config A --steps 2000 --warmup 10 2>&1 | tail -1 | tee $out/bench_A_$tag.json
+python bench.py --config A --precision fp64 --steps 2000 --warmup 10 --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_A_fp64_$tag.json
 python bench.py --steps 300 --warmup 10 --precision mixed --no-e2e --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_mixed_$tag.json
 python bench.py --steps 100 --warmup 5 --precision fp64 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_fp64_$tag.json
 python bench.py --steps 100 --warmup 5 --accumulation atomic --no-e2e --no-cpu-baseline 2>&1 | tail -1 | tee $out/bench_atomic_$tag.json
