@@ -85,8 +85,11 @@ def test_fused_robots_match_per_step_and_oracle(worm):
     assert rel_maxnorm(f["vel"], ref["m_vel"]) < 2e-3
 
 
-def test_fused_kills_between_launches():
-    case = _lattice_case(0, 0, 0, robots=6)
+@pytest.mark.parametrize("big", [False, True])
+def test_fused_kills_between_launches(big):
+    # robots: 512-thread groups; big: the 10^3 cube in one 1024-thread group
+    case = _lattice_case(10, 10, 10) if big else \
+        _lattice_case(0, 0, 0, robots=6)
     dt, n = 1e-4, 90
     times = np.arange(n, dtype=np.float64) * dt
     rng = np.random.default_rng(3)
