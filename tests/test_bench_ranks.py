@@ -54,3 +54,14 @@ def test_reference_arm_two_gloo_ranks_one_line():
     assert d["impl"] == "reference" and d["n_gpus"] == 2
     assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_config_a_is_the_reference_bouncing_cube():
+    """bench --config A builds scenarios/bouncing_cube.ini's cube: 10^3
+    masses, 10,476 springs, corner at z = 0.3."""
+    st, env, desc, scaling, extra = bench.make_workload(_args(config="A"),
+                                                        0, 1)
+    assert st.mass_count == 1000 and st.spring_count == 10476
+    assert float(st._m_pos[:1000, 2].min()) == 0.3 and extra == 0
+    assert desc.startswith("A: 10^3 bouncing cube") and scaling == "weak"
+    assert len(env.contacts) == 1
