@@ -179,7 +179,7 @@ def host_threads() -> int:
 def host_copy(a: np.ndarray) -> np.ndarray:
     """np.array(a) with the copy (and the fresh pages' first touch) spread
     over the host threads (sl_host_copy); small arrays copy in numpy."""
-    if a.nbytes < (8 << 20) or not a.flags.c_contiguous:
+    if a.nbytes < (1 << 20) or not a.flags.c_contiguous:
         return np.array(a)
     out = np.empty_like(a)
     rc = load_library().sl_host_copy(_ptr(out), _ptr(a), a.nbytes,
