@@ -205,6 +205,29 @@ def masked_extrema(v: np.ndarray, mask: np.ndarray | None):
     return lo.value, hi.value
 
 
+def host_copy_into(dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[...] = src (same shape / dtype, contiguous) on the host threads."""
+    src = np.ascontiguousarray(src)
+    if dst.shape != src.shape or dst.dtype != src.dtype:
+        raise InvalidValueError("host_copy_into: shape / dtype mismatch")
+    if src.nbytes < (1 << 20):
+        dst[...] = src
+        return
+    rc = load_library().sl_host_copy(_ptr(dst), _ptr(src), src.nbytes,
+                                     host_threads())
+    if rc != SL_OK:
+        raise SoftlatError(f"sl_host_copy failed ({rc})")
+
+
+def host_touch(a: np.ndarray) -> None:
+    """First-touch every page of a fresh array (zero fill, host threads)."""
+    zero = np.zeros(1, np.uint8)
+    rc = load_library().sl_host_fill(_ptr(a), _ptr(zero), 1, a.nbytes,
+                                     host_threads())
+    if rc != SL_OK:
+        raise SoftlatError(f"sl_host_fill failed ({rc})")
+
+
 def is_pinned(a: np.ndarray) -> bool:
     base = a
     while isinstance(base, np.ndarray) and base.base is not None:
