@@ -111,26 +111,34 @@ def build_robots(count: int, first: int = 0):
     return st, env
 
 
+def describe(args, world: int):
+    """(workload description, scaling, per-spring extra words)."""
+    if args.config == "D":
+        return (f"D: {args.robots} worm-actuated 5^3 robots (RL batch) on a "
+                f"friction ground plane, sharded over {world} rank(s), "
+                f"{args.precision}, {args.accumulation}",
+                "strong" if world > 1 else "weak", 1)
+    if args.config == "A":
+        return (f"A: 10^3 bouncing cube (scenarios/bouncing_cube.ini) per "
+                f"rank, {args.precision}, {args.accumulation}", "weak", 0)
+    return (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
+            f"x1.01 stretch, {args.precision}, {args.accumulation}",
+            "weak", 0)
+
+
 def make_workload(args, rank: int, world: int):
     """(store, env, description, scaling, per-spring extra words)."""
+    desc, scaling, extra = describe(args, world)
     if args.config == "D":
         per = args.robots // world
         first = rank * per + min(rank, args.robots % world)
         count = per + (1 if rank < args.robots % world else 0)
         st, env = build_robots(count, first)
-        desc = (f"D: {args.robots} worm-actuated 5^3 robots (RL batch) on a "
-                f"friction ground plane, sharded over {world} rank(s), "
-                f"{args.precision}, {args.accumulation}")
-        return st, env, desc, ("strong" if world > 1 else "weak"), 1
-    if args.config == "A":
+    elif args.config == "A":
         st, env = build_cube()
-        desc = (f"A: 10^3 bouncing cube (scenarios/bouncing_cube.ini) per "
-                f"rank, {args.precision}, {args.accumulation}")
-        return st, env, desc, "weak", 0
-    st, env = build_workload(args.n)
-    desc = (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
-            f"x1.01 stretch, {args.precision}, {args.accumulation}")
-    return st, env, desc, "weak", 0
+    else:
+        st, env = build_workload(args.n)
+    return st, env, desc, scaling, extra
 
 
 def algorithmic_bytes(springs: int, masses: int, precision: str,
@@ -161,13 +169,22 @@ def store_case(st, env):
 
 
 # ------------------------------------------------------------ cpu timing
-def time_oracle(st, env, steps: int, warmup: int, threads: int,
+def reference_case(args):
+    """The workload as an oracle case, built by oracle/workloads.py (numpy
+    only): the reference arm maps nothing from the product package
+    (tests/test_workloads.py: same arrays as the product builder)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import workloads
+    return workloads.workload(args.config, args.n, args.robots)
+
+
+def time_oracle(case, steps: int, warmup: int, threads: int,
                 budget_s: float = 120.0):
     """Reference algorithm (oracle/ C restatement, fp64, slotted parallel =
     the reference's parallel+slotted backend) on the host cores."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
-    sim = oracle.OracleSim(store_case(st, env), nthreads=threads)
+    sim = oracle.OracleSim(case, nthreads=threads)
     dt = 1e-4
     t = 0.0
     for _ in range(warmup):
@@ -312,26 +329,30 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        st, env, workload, _, _ = make_workload(args, 0, 1)
-        threads = os.cpu_count() or 1
+        case = reference_case(args)
+        workload = describe(args, 1)[0]
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle
         oracle.build()
         # all host threads (torchrun sets OMP_NUM_THREADS=1 per rank)
         threads = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
-        steps, wall = time_oracle(st, env, max(1, args.steps),
-                                  max(1, min(args.warmup, 2)), threads)
-        v = st.spring_count * steps / wall
+        steps, wall = time_oracle(case, max(1, args.steps),
+                                  max(1, args.warmup), threads,
+                                  budget_s=180.0)
+        springs = int(np.count_nonzero(case["s_alive"]))
+        v = springs * steps / wall
         line = {"impl": "reference", "metric": metric, "value": v,
                 "unit": unit, "n_gpus": args.gpus, "steps": steps,
-                "warmup": min(args.warmup, 2), "ms_per_step": 1e3 * wall /
+                "warmup": args.warmup, "ms_per_step": 1e3 * wall /
                 steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": v / PAPER_RATE, "dtype": "f64",
                 "data": "synthetic",
                 "config": {"workload": workload.replace(args.precision,
                                                         "fp64 (reference)"),
-                           "masses": st.mass_count,
-                           "springs": st.spring_count},
+                           "masses": len(case["m_mass"]),
+                           "springs": springs,
+                           "inputs": "oracle/workloads.py (numpy; no "
+                                     "product code on this arm)"},
                 "cpu_baseline": {"value": v, "unit": unit, "cores": threads,
                                  "kind": "port",
                                  "sample": f"{steps} full steps of the "
@@ -454,9 +475,10 @@ def main():
             import oracle
             oracle.build()
             thr = max(oracle.max_threads(), len(os.sched_getaffinity(0)))
-            st2, env2, _, _, _ = make_workload(args, 0, 1)
-            n_s, wall = time_oracle(st2, env2, 3, 1, thr, budget_s=30.0)
-            cpu = {"value": st2.spring_count * n_s / wall, "unit": unit,
+            case2 = reference_case(args)
+            n_s, wall = time_oracle(case2, 3, 1, thr, budget_s=30.0)
+            cpu = {"value": int(case2["s_alive"].sum()) * n_s / wall,
+                   "unit": unit,
                    "cores": thr, "kind": "port",
                    "sample": f"{n_s} steps of the same config-"
                              f"{args.config} workload (fp64, slotted, "

@@ -74,6 +74,9 @@ typedef struct sl_stats {
                              (0: the context runs per-step kernels only)  */
   int64_t fused_launches; /* multi-step fused launches so far             */
   int64_t fused_aborts;   /* of which re-run through per-step kernels     */
+  int32_t win_tile_slices; /* window kernel: slices per tile = consumer
+                              warps (the k_win_tma<P, T> instantiation)   */
+  int32_t win_stages;      /* window kernel: tile stages in the ring      */
 } sl_stats;
 
 /* sl_stats.step_path */
@@ -249,6 +252,11 @@ int sl_mark_ghosts(sl_ctx *ctx, int64_t n, const int64_t *slots);
  * step call. */
 int sl_state_pointers(sl_ctx *ctx, void **pos_read, int64_t *rows,
                       int32_t *record_bytes);
+/* fp32 mode: device pointer of the position LOW parts (ly, lz) (float2 per
+ * mass) of the buffer the next step reads; the record (sl_state_pointers)
+ * is (x, y, z, lx) in this mode, a position is record + low part and the
+ * masses live apart.  NULL in fp64 / mixed. */
+int sl_state_lo(sl_ctx *ctx, void **lo_read);
 /* The context's CUDA stream (cudaStream_t) for ordering foreign work. */
 int sl_get_stream(sl_ctx *ctx, void **stream);
 

@@ -34,7 +34,7 @@ EXPORTS = (
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
-    "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
+    "sl_state_lo", "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
     "sl_build_lattice", "sl_host_fill", "sl_host_copy",
     "sl_host_masked_extrema")
@@ -48,7 +48,8 @@ class SlStats(C.Structure):
                 ("precision", C.c_int32), ("device", C.c_int32),
                 ("step_path", C.c_int32), ("split_batch", C.c_int32),
                 ("fused_groups", C.c_int64), ("fused_launches", C.c_int64),
-                ("fused_aborts", C.c_int64)]
+                ("fused_aborts", C.c_int64),
+                ("win_tile_slices", C.c_int32), ("win_stages", C.c_int32)]
 
 STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
               3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma",
@@ -102,6 +103,7 @@ def load_library(path: str = LIB_PATH):
             "sl_step_finish": ([P, P, P, P], I),
             "sl_mark_ghosts": ([P, I64, P], I),
             "sl_state_pointers": ([P, P, P, P], I),
+            "sl_state_lo": ([P, P], I),
             "sl_get_stream": ([P, P], I),
             "sl_energy": ([P, D, P, P], I),
             "sl_spring_loads": ([P, D, P, P], I),
@@ -434,6 +436,13 @@ class Context:
                                                C.byref(rows), C.byref(rb)),
                     "sl_state_pointers")
         return int(p.value or 0), int(rows.value), int(rb.value)
+
+    def state_lo(self) -> int:
+        """fp32 mode: device pointer of the position low parts of the
+        buffer the next step reads (8 B per mass); 0 otherwise."""
+        p = C.c_void_p()
+        self._check(self.lib.sl_state_lo(self.h, C.byref(p)), "sl_state_lo")
+        return int(p.value or 0)
 
     def stream(self) -> int:
         p = C.c_void_p()

@@ -88,6 +88,8 @@ struct sl_ctx {
   bool snap_pending = false;
   // mass SoA
   DevBuf pos[2], vel, acc, fext, load, m_gen, m_alive, xflags;
+  DevBuf plo[2];  // fp32: position low parts (ly, lz); lx in pos[].w
+  DevBuf pmass;   // fp32: masses (the position record's w holds lx)
   DevBuf lc_off, lc_kind, lc_vec;
   bool has_lc = false;
   // spring SoA
@@ -190,6 +192,7 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
                               const double *load, const double *mass,
                               const uint8_t *fixed, const uint8_t *alive,
                               const int64_t *slots, void *pos0, void *pos1,
+                              void *plo0, void *plo1, float *pmass_o,
                               void *velo, void *acco, void *fexto,
                               void *loado, int64_t *gen_o, uint8_t *alive_o,
                               const int64_t *gen_in, const uint8_t *xflags) {
@@ -214,6 +217,14 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
   p.y = (R)pos[3 * r + 1];
   p.z = (R)pos[3 * r + 2];
   p.w = (R)mass[r];
+  if constexpr (P == PREC_FP32) {  // compensated: the residuals x - hi
+    p.w = (float)(pos[3 * r] - (double)p.x);  // lx in the record
+    const float2 l = make_float2((float)(pos[3 * r + 1] - (double)p.y),
+                                 (float)(pos[3 * r + 2] - (double)p.z));
+    ((float2 *)plo0)[i] = l;
+    ((float2 *)plo1)[i] = l;
+    pmass_o[i] = (float)mass[r];
+  }
   ((R4 *)pos0)[i] = p;
   ((R4 *)pos1)[i] = p;
   R4 v;
@@ -244,19 +255,26 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
 }
 
 template <int P>
-__global__ void k_unpack_masses(int64_t n, const void *posb, const void *velb,
-                                const void *accb, const void *fextb,
-                                double *pos, double *vel, double *acc,
-                                double *fext) {
+__global__ void k_unpack_masses(int64_t n, const void *posb, const void *plob,
+                                const void *velb, const void *accb,
+                                const void *fextb, double *pos, double *vel,
+                                double *acc, double *fext) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (pos) {
     R4 p = ((const R4 *)posb)[i];
-    pos[3 * i] = (double)p.x;
-    pos[3 * i + 1] = (double)p.y;
-    pos[3 * i + 2] = (double)p.z;
+    double x = (double)p.x, y = (double)p.y, z = (double)p.z;
+    if constexpr (P == PREC_FP32) {  // hi + lo, exact in fp64
+      const float2 l = ((const float2 *)plob)[i];
+      x += (double)p.w;
+      y += (double)l.x;
+      z += (double)l.y;
+    }
+    pos[3 * i] = x;
+    pos[3 * i + 1] = y;
+    pos[3 * i + 2] = z;
   }
   if (vel) {
     R4 v = ((const R4 *)velb)[i];
@@ -436,6 +454,21 @@ __global__ void k_validate(KState S, const uint8_t *m_alive,
 }
 
 // ------------------------------------------------------- diagnostics
+// position of mass i in fp64 (fp32 mode: hi + lo)
+template <int P>
+__device__ __forceinline__ double3 pos_f64(const KState &S, int cur,
+                                           int64_t i) {
+  using R4 = typename Tr<P>::R4;
+  const R4 p = ((const R4 *)S.pos[cur])[i];
+  double3 r = make_double3((double)p.x, (double)p.y, (double)p.z);
+  if constexpr (P == PREC_FP32) {
+    const float2 l = ((const float2 *)S.plo[cur])[i];
+    r.x += (double)p.w;
+    r.y += (double)l.x;
+    r.z += (double)l.y;
+  }
+  return r;
+}
 // engine.mechanical_energy (engine.py:366-389) on the device: per-block
 // partial sums of m |v|^2, m (x . g) and k (|d| - f L0)^2 in fp64 (fixed
 // block tree order), finished on the host in block order -- deterministic.
@@ -448,23 +481,21 @@ __global__ void __launch_bounds__(DIAG_THREADS)
   using F2 = typename Tr<P>::F2;
   __shared__ double red[3][DIAG_THREADS];
   double ke = 0.0, gp = 0.0, sp = 0.0;
-  const R4 *pos = (const R4 *)S.pos[cur];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (int64_t i = t0; i < S.m_n; i += stride) {
     const R4 v = ((const R4 *)S.vel)[i];
     if (!(flags_of(v.w) & MF_ALIVE)) continue;
-    const R4 p = pos[i];
-    const double m = (double)p.w;
+    const double3 p = pos_f64<P>(S, cur, i);
+    const double m = (double)mass_of<P>(S, ((const R4 *)S.pos[cur])[i], i);
     ke += m * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z);
-    gp += m * ((double)p.x * gx + (double)p.y * gy + (double)p.z * gz);
+    gp += m * (p.x * gx + p.y * gy + p.z * gz);
   }
   for (int64_t s = t0; s < S.s_n; s += stride) {
     const int2 e = S.ends[s];
     if (e.x < 0) continue;
-    const R4 a = pos[e.x], b = pos[e.y];
-    const double dx = (double)b.x - a.x, dy = (double)b.y - a.y,
-                 dz = (double)b.z - a.z;
+    const double3 a = pos_f64<P>(S, cur, e.x), b = pos_f64<P>(S, cur, e.y);
+    const double dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
     const double len = sqrt(dx * dx + dy * dy + dz * dz);
     const F2 kl = ((const F2 *)S.kL0)[s];
     const double f = S.mode[s] ? act_factor(S, s, sim_t) : 1.0;
@@ -497,10 +528,8 @@ __global__ void k_spring_loads(const KState S, int cur, double sim_t,
     len_out[s] = fmag_out[s] = CUDART_NAN;
     return;
   }
-  const R4 *pos = (const R4 *)S.pos[cur];
-  const R4 a = pos[e.x], b = pos[e.y];
-  const double dx = (double)b.x - a.x, dy = (double)b.y - a.y,
-               dz = (double)b.z - a.z;
+  const double3 a = pos_f64<P>(S, cur, e.x), b = pos_f64<P>(S, cur, e.y);
+  const double dx = b.x - a.x, dy = b.y - a.y, dz = b.z - a.z;
   const double len = sqrt(dx * dx + dy * dy + dz * dz);
   const F2 kl = ((const F2 *)S.kL0)[s];
   const double f = S.mode[s] ? act_factor(S, s, sim_t) : 1.0;
@@ -696,6 +725,9 @@ KState make_state(sl_ctx *c) {
   S.s_n = c->s_n;
   S.pos[0] = c->pos[0].p;
   S.pos[1] = c->pos[1].p;
+  S.plo[0] = c->prec == PREC_FP32 ? c->plo[0].p : nullptr;
+  S.plo[1] = c->prec == PREC_FP32 ? c->plo[1].p : nullptr;
+  S.pmass = c->prec == PREC_FP32 ? c->pmass.as<float>() : nullptr;
   S.vel = c->vel.p;
   S.acc = c->acc.p;
   S.fext = c->fext.p;
@@ -782,6 +814,12 @@ int ensure_masses(sl_ctx *c, int64_t m_n) {
   m_n = (m_n + 31) / 32 * 32;  // bulk copies move whole 32-mass slices
   // + one slice of sentinel records (split layout's dead / padding target)
   for (int b = 0; b < 2; b++) CK(c->pos[b].ensure(r4 * (m_n + 32)));
+  if (c->prec == PREC_FP32)  // low parts; padding / sentinel rows stay 0
+    for (int b = 0; b < 2; b++) {
+      CK(c->plo[b].ensure(8 * (m_n + 32)));
+      CK(cudaMemsetAsync(c->plo[b].p, 0, 8 * (m_n + 32), c->st));
+      CK(c->pmass.ensure(4 * (m_n + 32)));
+    }
   CK(c->vel.ensure(r4 * m_n));
   CK(c->acc.ensure(3 * c->rsz * m_n));
   CK(c->fext.ensure(r4 * m_n));
@@ -1009,6 +1047,7 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
 
 // Tile/window geometry of the fp32 split layout (sl_window.cuh); c->win stays
 // false when a tile does not fit (the split kernel then runs).
+int build_window_tt(sl_ctx *c, int tt);
 int build_window_layout(sl_ctx *c) {
   c->win = false;
   if (!c->win_enabled || !c->tma_enabled || c->prec == PREC_FP64 ||
@@ -1019,11 +1058,23 @@ int build_window_layout(sl_ctx *c) {
   // latency-bound per tile, so 8-slice tiles spread them over more SMs
   // (10^3..30^3: 8.2 -> 6.2 us/step; 50^3 and up keep 16)
   int tt = c->n_slices <= (int64_t)8 * c->sm_count ? 8 : 16;
+  if (c->prec == PREC_MIXED) tt = 16;  // the one mixed instantiation
   if (const char *ev = getenv("SL_WIN_T")) {
     const int v = atoi(ev);
-    tt = v == 4 || v == 8 || v == 12 || v == 20 || v == 24 ? v : 16;
+    if (c->prec != PREC_MIXED)
+      tt = v == 4 || v == 8 || v == 12 || v == 20 || v == 24 ? v : 16;
+    return build_window_tt(c, tt);
   }
-  if (c->prec == PREC_MIXED) tt = 16;  // the one mixed instantiation
+  if (int rc = build_window_tt(c, tt)) return rc;
+  // fp32 (compensated positions: larger windows): a ring of 3 stages of
+  // 12-slice tiles beats 2 stages of 16 (config B 47.8 vs 53.1 us/step)
+  if (c->prec == PREC_FP32 && tt == 16 && (!c->win || c->wcfg.nst < 3))
+    return build_window_tt(c, 12);
+  return SL_OK;
+}
+
+int build_window_tt(sl_ctx *c, int tt) {
+  c->win = false;
   const int64_t n_tiles = (c->n_slices + tt - 1) / tt;
   WinCfg w{};
   w.n_tiles = n_tiles;
@@ -1067,8 +1118,15 @@ int build_window_layout(sl_ctx *c) {
   w.off_dict = sizeof(TileRec);
   w.off_act = w.off_dict + 8 * WIN_DMAX;
   w.off_win = w.off_act + (res[2] ? WIN_ACTB : 0);
-  w.off_slice =
-      (w.off_win + (uint32_t)(4 * c->rsz) * w.cap_rec + 127) / 128 * 128;
+  uint32_t win_end = w.off_win + (uint32_t)(4 * c->rsz) * w.cap_rec;
+  if (c->prec == PREC_FP32) {  // the windows' position low parts, masses
+    w.off_wlo = (win_end + 15) / 16 * 16;
+    win_end = w.off_wlo + 8 * w.cap_rec;
+    w.off_mass = (win_end + 15) / 16 * 16;
+    win_end = w.off_mass + 4 * 32 * tt;
+    w.pmass = c->pmass.as<float>();
+  }
+  w.off_slice = (win_end + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
   const int64_t bar = 8 * 2 * WIN_MAXST + 8 * WIN_MAXST * WIN_DMAX;
   int nst = (int)std::min<int64_t>(
@@ -1085,7 +1143,7 @@ int build_window_layout(sl_ctx *c) {
             "slice %u B, stage %u B (windows %u B), %d stages of %lld B "
             "opt-in\n",
             (long long)n_tiles, tt, w.cap_rec, w.bl.slice_bytes,
-            w.stage_bytes, (uint32_t)(4 * c->rsz) * w.cap_rec, nst,
+            w.stage_bytes, w.off_slice - w.off_win, nst,
             (long long)c->smem_optin);
   w.rec = c->win_rec.as<TileRec>();
   w.dict = c->win_dict.as<float2>();
@@ -1275,9 +1333,8 @@ int build_fused_groups(sl_ctx *c) {
   f.has_act = c->fz_has.as<uint8_t>();
   f.ra = ra;
   f.rb = rb;
-  const size_t smem = 32 * WIN_DMAX + 16 * 2 * (maxm + 1) +
-                      8 * 4 * WIN_DMAX + (size_t)4 * rows * maxm +
-                      WIN_DMAX;
+  const size_t smem = 32 * WIN_DMAX + 24 * 2 * (maxm + 1) +
+                      8 * 4 * WIN_DMAX + (size_t)4 * rows * maxm + WIN_DMAX;
   f.maxm = maxm;
   if (launchers(c->prec).fused_setup(smem, maxm) != 0) {
     cudaGetLastError();
@@ -1644,7 +1701,7 @@ int sl_destroy(sl_ctx *c) {
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   if (c->side) cudaStreamSynchronize(c->side);
-  DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc, &c->fext,
+  DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->plo[0], &c->plo[1], &c->pmass, &c->vel, &c->acc, &c->fext,
                     &c->load, &c->m_gen, &c->m_alive, &c->xflags, &c->lc_off,
                     &c->lc_kind, &c->lc_vec, &c->ends, &c->kL0, &c->s_alive,
                     &c->s_degen, &c->mode, &c->act, &c->thr, &c->custom,
@@ -1695,7 +1752,9 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
   o->fused_groups = c->fz_ok ? c->fcfg.n_groups : 0;
   o->fused_launches = c->fz_launches;
   o->fused_aborts = c->fz_aborts;
-  const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->vel, &c->acc,
+  o->win_tile_slices = c->win ? c->wcfg.tile_slices : 0;
+  o->win_stages = c->win ? c->wcfg.nst : 0;
+  const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->plo[0], &c->plo[1], &c->pmass, &c->vel, &c->acc,
                           &c->fext, &c->load, &c->m_gen, &c->m_alive,
                           &c->ends, &c->kL0, &c->s_alive, &c->s_degen,
                           &c->mode, &c->act, &c->thr, &c->custom, &c->m1gen,
@@ -1763,7 +1822,8 @@ int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
                                     : k_pack_masses<PREC_MIXED>;
     k<<<blocks_for(m_n), 256, 0, c->st>>>(
         m_n, dp, dv, da, df, dl, dm, dfx, dal, nullptr, c->pos[0].p,
-        c->pos[1].p, c->vel.p, c->acc.p, c->fext.p, c->load.p,
+        c->pos[1].p, c->plo[0].p, c->plo[1].p, c->pmass.as<float>(), c->vel.p,
+        c->acc.p, c->fext.p, c->load.p,
         c->m_gen.as<int64_t>(), c->m_alive.as<uint8_t>(), dg,
         (c->layout_valid && m_n == c->m_n) ? c->xflags.as<uint8_t>()
                                            : nullptr);
@@ -2023,7 +2083,8 @@ int sl_write_masses(sl_ctx *c, int64_t n, const int64_t *slots,
   // rewritten by the step kernels, so both halves must agree)
   k<<<blocks_for(n), 256, 0, c->st>>>(
       n, dp, dv, da, df, dl, dm, dfx, dal, ds, c->pos[0].p, c->pos[1].p,
-      c->vel.p, c->acc.p, c->fext.p, c->load.p, c->m_gen.as<int64_t>(),
+      c->plo[0].p, c->plo[1].p, c->pmass.as<float>(), c->vel.p, c->acc.p,
+      c->fext.p, c->load.p, c->m_gen.as<int64_t>(),
       c->m_alive.as<uint8_t>(), dg,
       c->layout_valid ? c->xflags.as<uint8_t>() : nullptr);
   CKL();
@@ -2162,7 +2223,11 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     T.dt = dt;
     T.step = n;
     T.cur = (int)((c->cur + n) & 1);
-    T.write_acc = n == n_steps - 1;
+    // accelerations are stored on the last step of a batch -- and on every
+    // step in fp64 parity mode, so a numerical abort at any step leaves the
+    // aborting step's accelerations, as the reference's mass pass does
+    // (kernels.py:368-376)
+    T.write_acc = n == n_steps - 1 || c->prec == PREC_FP64;
     if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
         if (c->win)
@@ -2328,8 +2393,9 @@ int sl_download_masses(sl_ctx *c, double *pos, double *vel, double *acc,
   auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
            : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
                                   : k_unpack_masses<PREC_MIXED>;
-  k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p, c->vel.p,
-                                      c->acc.p, c->fext.p, dp, dv, da, df);
+  k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p,
+                                      c->plo[c->cur].p, c->vel.p, c->acc.p,
+                                      c->fext.p, dp, dv, da, df);
   CKL();
   c->launches++;
   if (pos) CK(cudaMemcpyAsync(pos, dp, 24 * m, cudaMemcpyDeviceToHost, c->st));
@@ -2374,9 +2440,10 @@ int sl_snapshot_begin(sl_ctx *c) {
              : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
                                     : k_unpack_masses<PREC_MIXED>;
     double *dp = (double *)c->snap_dev.p;
-    k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p, c->vel.p,
-                                        nullptr, nullptr, dp, dp + 3 * m,
-                                        nullptr, nullptr);
+    k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p,
+                                        c->plo[c->cur].p, c->vel.p, nullptr,
+                                        nullptr, dp, dp + 3 * m, nullptr,
+                                        nullptr);
     CKL();
     c->launches++;
   }
@@ -2542,6 +2609,12 @@ int sl_state_pointers(sl_ctx *c, void **pos_read, int64_t *rows,
   if (pos_read) *pos_read = c->pos[c->cur].p;
   if (rows) *rows = (int64_t)(c->pos[c->cur].bytes / (4 * c->rsz));
   if (record_bytes) *record_bytes = (int32_t)(4 * c->rsz);
+  return SL_OK;
+}
+
+int sl_state_lo(sl_ctx *c, void **lo_read) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (lo_read) *lo_read = c->prec == PREC_FP32 ? c->plo[c->cur].p : nullptr;
   return SL_OK;
 }
 

@@ -72,6 +72,9 @@ struct EnvP {
 struct KState {
   int64_t m_n, s_n;
   void *pos[2];
+  void *plo[2];  // fp32: position low parts (ly, lz) float2 per mass (the
+                 // record's w holds lx, see lo_at); null in fp64 / mixed
+  const float *pmass;  // fp32: masses (the record's w is lx); else null
   void *vel;
   void *acc;   // R[3*m_n]
   void *fext;  // R4[m_n]
@@ -138,10 +141,13 @@ struct StepP {
   int write_acc;  // store acceleration (final step of a launch)
 };
 
+// fp64 / mixed state: a position is its R4 record alone
+struct NoLo {};
 template <int P>
 struct Tr;
 template <>
 struct Tr<PREC_FP64> {
+  using L = NoLo;
   using R = double;
   using F = double;
   using R4 = double4;
@@ -152,6 +158,7 @@ struct Tr<PREC_FP64> {
 };
 template <>
 struct Tr<PREC_FP32> {
+  using L = float3;  // compensated positions: x = hi + lo
   using R = float;
   using F = float;
   using R4 = float4;
@@ -162,6 +169,7 @@ struct Tr<PREC_FP32> {
 };
 template <>
 struct Tr<PREC_MIXED> {
+  using L = NoLo;
   using R = double;
   using F = float;
   using R4 = double4;
@@ -197,6 +205,62 @@ __device__ __forceinline__ void or_flags(float4 *v, uint32_t f) {
 }
 __device__ __forceinline__ void or_flags(double4 *v, uint32_t f) {
   atomicOr((unsigned int *)&v->w, f);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 mode: compensated positions.  A position is hi + lo, hi the fp32
+// coordinates and lo their rounding residuals, all fp32:
+//   pos[b][i] = (x_hi, y_hi, z_hi, lx)   plo[b][i] = (ly, lz)
+// (the mass lives in pmass).  Spring vectors are formed as
+// (o_hi - me_hi) + (o_lo - me_lo): the first difference is exact for
+// neighbouring masses (Sterbenz), so |d| carries ~2^-48 of |x| instead of
+// fp32's 2^-24 -- the spurious strain of a rounded position (ulp 6e-8 m at
+// |x| ~ 1 m, 1.2e-4 m at |x| ~ 1 km, times k) no longer exists, which is
+// what holds fp32 velocities to 1e-4 of the fp64 reference.
+// The position update is a two-sum (integrate_vals).
+// lo of mass j whose record is o (fp32; an empty value otherwise)
+template <int P>
+__device__ __forceinline__ typename Tr<P>::L lo_at(
+    const typename Tr<P>::R4 &o, const void *plo, int64_t j) {
+  if constexpr (P == PREC_FP32) {
+    const float2 b = __ldg((const float2 *)plo + j);
+    return make_float3(o.w, b.x, b.y);
+  } else {
+    return {};
+  }
+}
+// mass of mass i (fp32: pmass; else the record's w)
+template <int P>
+__device__ __forceinline__ typename Tr<P>::R mass_of(
+    const KState &S, const typename Tr<P>::R4 &me, int64_t i) {
+  if constexpr (P == PREC_FP32)
+    return __ldg(S.pmass + i);
+  else
+    return me.w;
+}
+// d = (o + o_lo) - (me + me_lo), in the force arithmetic type M
+template <int P, class M>
+__device__ __forceinline__ void pdiff(const typename Tr<P>::R4 &me,
+                                      const typename Tr<P>::L &ml,
+                                      const typename Tr<P>::R4 &o,
+                                      const typename Tr<P>::L &ol, M &dx,
+                                      M &dy, M &dz) {
+  if constexpr (P == PREC_FP32) {
+    dx = (o.x - me.x) + (ol.x - ml.x);
+    dy = (o.y - me.y) + (ol.y - ml.y);
+    dz = (o.z - me.z) + (ol.z - ml.z);
+  } else {
+    dx = (M)(o.x - me.x);
+    dy = (M)(o.y - me.y);
+    dz = (M)(o.z - me.z);
+  }
+}
+// exact sum hi + t as (s, e), s = fl(hi + t) (Knuth's two-sum)
+__device__ __forceinline__ float two_sum(float a, float b, float &e) {
+  const float s = __fadd_rn(a, b);
+  const float bb = __fsub_rn(s, a);
+  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+  return s;
 }
 
 // Python float % (CPython float_rem, which numba follows; kernels.py:58).
@@ -271,12 +335,12 @@ __device__ __forceinline__ void red_add(double4 *p, double x, double y,
 template <int P>
 __device__ __forceinline__ void integrate_vals(
     const KState &S, const EnvP &E, double dt_, int64_t i,
-    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
-    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz,
-    typename Tr<P>::R4 &np4, typename Tr<P>::R4 &nv, typename Tr<P>::R &ax,
+    typename Tr<P>::R4 me, typename Tr<P>::L lo, typename Tr<P>::R mm,
+    typename Tr<P>::R4 v, uint32_t fl, typename Tr<P>::R fx,
+    typename Tr<P>::R fy, typename Tr<P>::R fz, typename Tr<P>::R4 &np4,
+    typename Tr<P>::L &nlo, typename Tr<P>::R4 &nv, typename Tr<P>::R &ax,
     typename Tr<P>::R &ay, typename Tr<P>::R &az) {
   using R = typename Tr<P>::R;
-  const R mm = me.w;
   R px = me.x, py = me.y, pz = me.z;
   R vx = v.x, vy = v.y, vz = v.z;
   // F = ((f_ext + load) + m*g) - drag*v; an all-zero load adds +0.0, which
@@ -301,7 +365,9 @@ __device__ __forceinline__ void integrate_vals(
   // contact planes with Coulomb friction on the running force
   for (int p = 0; p < E.np; p++) {
     const R nx = (R)E.pl[p][0], ny = (R)E.pl[p][1], nz = (R)E.pl[p][2];
-    const R depth = (R)E.pl[p][3] - (px * nx + py * ny + pz * nz);
+    R depth = (R)E.pl[p][3] - (px * nx + py * ny + pz * nz);
+    if constexpr (P == PREC_FP32)
+      depth = depth - (lo.x * nx + lo.y * ny + lo.z * nz);
     if (depth > (R)0.0) {
       const R nmag = (R)E.pl[p][4] * depth;
       fx += nmag * nx;
@@ -332,8 +398,13 @@ __device__ __forceinline__ void integrate_vals(
     }
   }
   for (int b = 0; b < E.nb; b++) {
-    const R ddx = px - (R)E.bl[b][0], ddy = py - (R)E.bl[b][1],
-            ddz = pz - (R)E.bl[b][2];
+    R ddx = px - (R)E.bl[b][0], ddy = py - (R)E.bl[b][1],
+      ddz = pz - (R)E.bl[b][2];
+    if constexpr (P == PREC_FP32) {
+      ddx = ddx + lo.x;
+      ddy = ddy + lo.y;
+      ddz = ddz + lo.z;
+    }
     const R dist = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
     const R depth = (R)E.bl[b][3] - dist;
     if (depth > (R)0.0 && dist > (R)0.0) {
@@ -386,13 +457,25 @@ __device__ __forceinline__ void integrate_vals(
       }
     }
   }
-  px += vx * dt;
-  py += vy * dt;
-  pz += vz * dt;
+  if constexpr (P == PREC_FP32) {
+    // (hi, lo) + v dt: lo absorbs the increment, a two-sum renormalises
+    float ex, ey, ez;
+    px = two_sum(px, fmaf(vx, dt, lo.x), ex);
+    py = two_sum(py, fmaf(vy, dt, lo.y), ey);
+    pz = two_sum(pz, fmaf(vz, dt, lo.z), ez);
+    nlo = make_float3(ex, ey, ez);
+  } else {
+    px += vx * dt;
+    py += vy * dt;
+    pz += vz * dt;
+  }
   np4.x = px;
   np4.y = py;
   np4.z = pz;
-  np4.w = mm;
+  if constexpr (P == PREC_FP32)
+    np4.w = nlo.x;  // the record carries lx
+  else
+    np4.w = mm;
   nv.x = vx;
   nv.y = vy;
   nv.z = vz;
@@ -402,14 +485,18 @@ __device__ __forceinline__ void integrate_vals(
 template <int P>
 __device__ __forceinline__ void integrate(
     const KState &S, const EnvP &E, const StepP &T, int64_t i,
-    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
-    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+    typename Tr<P>::R4 me, typename Tr<P>::L lo, typename Tr<P>::R mm,
+    typename Tr<P>::R4 v, uint32_t fl, typename Tr<P>::R fx,
+    typename Tr<P>::R fy, typename Tr<P>::R fz) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   R4 np4, nv;
+  typename Tr<P>::L nlo;
   R ax, ay, az;
-  integrate_vals<P>(S, E, T.dt, i, me, v, fl, fx, fy, fz, np4, nv, ax, ay,
-                    az);
+  integrate_vals<P>(S, E, T.dt, i, me, lo, mm, v, fl, fx, fy, fz, np4, nlo,
+                    nv, ax, ay, az);
+  if constexpr (P == PREC_FP32)
+    ((float2 *)S.plo[T.cur ^ 1])[i] = make_float2(nlo.y, nlo.z);
   const R px = np4.x, py = np4.y, pz = np4.z, vx = nv.x, vy = nv.y,
           vz = nv.z;
   ((R4 *)S.pos[T.cur ^ 1])[i] = np4;
@@ -460,22 +547,18 @@ __device__ __forceinline__ void fixed_mass(const KState &S, const StepP &T,
 template <int P>
 __device__ __forceinline__ bool entry_force(
     const KState &S, int64_t e, uint32_t jr, typename Tr<P>::R4 me,
-    typename Tr<P>::R4 other, typename Tr<P>::F2 kl, double sim_t,
-    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+    typename Tr<P>::L ml, typename Tr<P>::R4 other, typename Tr<P>::L ol,
+    typename Tr<P>::F2 kl, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using F = typename Tr<P>::M;
   const bool is_m2 = (jr & EJ_M2) != 0;
   // d = pos[m2] - pos[m1]
   F dx, dy, dz;
-  if (is_m2) {
-    dx = (F)(me.x - other.x);
-    dy = (F)(me.y - other.y);
-    dz = (F)(me.z - other.z);
-  } else {
-    dx = (F)(other.x - me.x);
-    dy = (F)(other.y - me.y);
-    dz = (F)(other.z - me.z);
-  }
+  if (is_m2)
+    pdiff<P>(other, ol, me, ml, dx, dy, dz);
+  else
+    pdiff<P>(me, ml, other, ol, dx, dy, dz);
   const F len2 = dx * dx + dy * dy + dz * dz;
   if (len2 == (F)0.0) {  // <=> sqrt(len2) == 0, kernels.py:50
     if (!is_m2) {
@@ -539,12 +622,13 @@ __device__ __forceinline__ bool entry_force(
 // This exact path serves fp64 parity mode.
 template <int P, bool GLOBAL_SRC>
 __device__ __forceinline__ void gather_forces_exact(
-    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
-    const typename Tr<P>::F2 *ekl, int width, int64_t ebase,
-    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
-    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+    const KState &S, const typename Tr<P>::R4 *pos, const void *plo,
+    const uint32_t *ej, const typename Tr<P>::F2 *ekl, int width,
+    int64_t ebase, typename Tr<P>::R4 me, typename Tr<P>::L ml, double sim_t,
+    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
+  using L = typename Tr<P>::L;
   // fp64 parity mode runs everything here; in the tolerance modes only
   // masses with actuated / breakable springs do -- keep it register-light
   constexpr int U = P == PREC_FP64 ? Tr<P>::U : 2;
@@ -552,6 +636,7 @@ __device__ __forceinline__ void gather_forces_exact(
     uint32_t jr[U];
     F2 kl[U];
     R4 o[U];
+    L ol[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (t0 + u < width)
@@ -564,13 +649,14 @@ __device__ __forceinline__ void gather_forces_exact(
       if (!(jr[u] & EJ_DEAD)) {
         kl[u] = GLOBAL_SRC ? __ldg(ekl + 32 * (t0 + u)) : ekl[32 * (t0 + u)];
         o[u] = pos[jr[u] & EJ_MASK];
+        ol[u] = lo_at<P>(o[u], plo, jr[u] & EJ_MASK);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (!(jr[u] & EJ_DEAD))
-        entry_force<P>(S, ebase + 32 * (int64_t)(t0 + u), jr[u], me, o[u],
-                       kl[u], sim_t, fx, fy, fz);
+        entry_force<P>(S, ebase + 32 * (int64_t)(t0 + u), jr[u], me, ml,
+                       o[u], ol[u], kl[u], sim_t, fx, fy, fz);
     }
   }
 }
@@ -585,10 +671,10 @@ __device__ __forceinline__ void gather_forces_exact(
 // (deterministic run to run).  Returns true if a zero-length spring was seen.
 template <int P, bool GLOBAL_SRC>
 __device__ __forceinline__ bool gather_forces_fast(
-    const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::R4 *pos, const void *plo, const uint32_t *ej,
     const typename Tr<P>::F2 *ekl, int width, uint32_t self,
-    typename Tr<P>::R4 me, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
-    typename Tr<P>::R &fz) {
+    typename Tr<P>::R4 me, typename Tr<P>::L ml, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using M = typename Tr<P>::M;
   using R4 = typename Tr<P>::R4;
@@ -596,7 +682,9 @@ __device__ __forceinline__ bool gather_forces_fast(
   constexpr int U = Tr<P>::U;
   bool odd = false;
   auto body = [&](uint32_t jr, F2 kl, R4 o) {
-    const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+    const uint32_t j = (jr & EJ_DEAD) ? self : (jr & EJ_MASK);
+    M dx, dy, dz;
+    pdiff<P>(me, ml, o, lo_at<P>(o, plo, j), dx, dy, dz);
     const M len2 = dx * dx + dy * dy + dz * dz;
     M r;
     if constexpr (P == PREC_FP32) {
@@ -646,17 +734,19 @@ __device__ __forceinline__ bool gather_forces_fast(
 // runs few warps per SM and can afford the registers.
 template <int P, int U>
 __device__ __forceinline__ bool gather_forces_pipe(
-    const typename Tr<P>::R4 *pos, const uint32_t *ej,
+    const typename Tr<P>::R4 *pos, const void *plo, const uint32_t *ej,
     const typename Tr<P>::F2 *ekl, int width, uint32_t self,
-    typename Tr<P>::R4 me, typename Tr<P>::R &fx, typename Tr<P>::R &fy,
-    typename Tr<P>::R &fz) {
+    typename Tr<P>::R4 me, typename Tr<P>::L ml, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using M = typename Tr<P>::M;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
   bool odd = false;
   auto body = [&](uint32_t jr, F2 kl, R4 o) {
-    const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+    const uint32_t j = (jr & EJ_DEAD) ? self : (jr & EJ_MASK);
+    M dx, dy, dz;
+    pdiff<P>(me, ml, o, lo_at<P>(o, plo, j), dx, dy, dz);
     const M len2 = dx * dx + dy * dy + dz * dz;
     M r;
     if constexpr (P == PREC_FP32) {
@@ -713,12 +803,15 @@ template <int P, bool GLOBAL_SRC>
 __device__ __noinline__ void degenerate_flags(
     const int32_t *ent_s, uint8_t *s_degen, unsigned long long *status,
     const uint8_t *ghost, int64_t self, const typename Tr<P>::R4 *pos,
-    const uint32_t *ej, int width, int64_t ebase, typename Tr<P>::R4 me) {
+    const void *plo, const uint32_t *ej, int width, int64_t ebase,
+    typename Tr<P>::R4 me, typename Tr<P>::L ml) {
   for (int t = 0; t < width; t++) {
     const uint32_t jr = GLOBAL_SRC ? __ldg(ej + 32 * t) : ej[32 * t];
     if (jr & (EJ_DEAD | EJ_M2)) continue;
     const typename Tr<P>::R4 o = pos[jr & EJ_MASK];
-    if (o.x == me.x && o.y == me.y && o.z == me.z) {
+    typename Tr<P>::M dx, dy, dz;
+    pdiff<P>(me, ml, o, lo_at<P>(o, plo, jr & EJ_MASK), dx, dy, dz);
+    if (dx == 0 && dy == 0 && dz == 0) {
       const int32_t s = ent_s[ebase + 32 * (int64_t)t];
       if (!s_degen[s]) {
         s_degen[s] = 1;
@@ -730,22 +823,24 @@ __device__ __noinline__ void degenerate_flags(
 
 template <int P, bool GLOBAL_SRC>
 __device__ __forceinline__ void gather_forces(
-    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ej,
-    const typename Tr<P>::F2 *ekl, int width, int64_t ebase, int64_t self,
-    uint32_t fl, typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    const KState &S, const typename Tr<P>::R4 *pos, const void *plo,
+    const uint32_t *ej, const typename Tr<P>::F2 *ekl, int width,
+    int64_t ebase, int64_t self, uint32_t fl, typename Tr<P>::R4 me,
+    typename Tr<P>::L ml, double sim_t, typename Tr<P>::R &fx,
     typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   if constexpr (P == PREC_FP64) {
-    gather_forces_exact<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, me,
-                                       sim_t, fx, fy, fz);
+    gather_forces_exact<P, GLOBAL_SRC>(S, pos, plo, ej, ekl, width, ebase, me,
+                                       ml, sim_t, fx, fy, fz);
   } else {
     if (fl & MF_SPECIAL)
-      gather_forces_exact<P, GLOBAL_SRC>(S, pos, ej, ekl, width, ebase, me,
-                                         sim_t, fx, fy, fz);
-    else if (gather_forces_fast<P, GLOBAL_SRC>(pos, ej, ekl, width,
-                                                 (uint32_t)self, me, fx, fy,
-                                                 fz))
+      gather_forces_exact<P, GLOBAL_SRC>(S, pos, plo, ej, ekl, width, ebase,
+                                         me, ml, sim_t, fx, fy, fz);
+    else if (gather_forces_fast<P, GLOBAL_SRC>(pos, plo, ej, ekl, width,
+                                                 (uint32_t)self, me, ml, fx,
+                                                 fy, fz))
       degenerate_flags<P, GLOBAL_SRC>(S.ent_s, S.s_degen, S.status, S.ghost,
-                                      self, pos, ej, width, ebase, me);
+                                      self, pos, plo, ej, width, ebase, me,
+                                      ml);
   }
 }
 
@@ -753,8 +848,9 @@ __device__ __forceinline__ void gather_forces(
 template <int P, bool FORCE_ONLY>
 __device__ __forceinline__ void finish_mass(
     const KState &S, const EnvP &E, const StepP &T, int64_t i,
-    typename Tr<P>::R4 me, typename Tr<P>::R4 v, uint32_t fl,
-    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+    typename Tr<P>::R4 me, typename Tr<P>::L ml, typename Tr<P>::R mm,
+    typename Tr<P>::R4 v, uint32_t fl, typename Tr<P>::R fx,
+    typename Tr<P>::R fy, typename Tr<P>::R fz) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   if (FORCE_ONLY) {
@@ -778,7 +874,7 @@ __device__ __forceinline__ void finish_mass(
     z.x = z.y = z.z = z.w = (R)0.0;
     ((R4 *)S.fext)[i] = z;
   }
-  integrate<P>(S, E, T, i, me, v, fl, fx, fy, fz);
+  integrate<P>(S, E, T, i, me, ml, mm, v, fl, fx, fy, fz);
 }
 
 template <int P>
@@ -824,15 +920,18 @@ static __global__ void __launch_bounds__(256)
   const uint32_t fl = flags_of(v.w);
   if (!(fl & MF_ALIVE)) return;
   const R4 me = pos[i];
+  const void *plo = S.plo[T.cur];
+  const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
   R fx, fy, fz;
   initial_force<P>(S, i, fl, FORCE_ONLY, fx, fy, fz);
   const int64_t w = i >> 5;
   const int64_t ebase = S.slice_ptr[w] + (i & 31);
   const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
-  gather_forces<P, true>(S, pos, S.ent_j + ebase,
+  gather_forces<P, true>(S, pos, plo, S.ent_j + ebase,
                          (const F2 *)S.ent_kL0 + ebase, width, ebase, i, fl,
-                         me, T.sim_t, fx, fy, fz);
-  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
+                         me, ml, T.sim_t, fx, fy, fz);
+  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, ml, mass_of<P>(S, me, i), v,
+                             fl, fx, fy, fz);
 }
 
 // ---------------------------------------------------------------------------
@@ -1009,24 +1108,30 @@ static __global__ void __launch_bounds__(384)
       const uint32_t fl = flags_of(v.w);
       if (fl & MF_ALIVE) {
         const R4 me = ((const R4 *)st)[lane];
+        const void *plo = S.plo[T.cur];
+        const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
         R fx, fy, fz;
         initial_force<P>(S, i, fl, false, fx, fy, fz);
         const uint32_t *ej = (const uint32_t *)(st + j_off) + lane;
         const F2 *ekl = (const F2 *)(st + k_off) + lane;
         if constexpr (P == PREC_FP64) {
-          gather_forces_exact<P, false>(S, pos, ej, ekl, width, e0 + lane,
-                                        me, T.sim_t, fx, fy, fz);
+          gather_forces_exact<P, false>(S, pos, plo, ej, ekl, width,
+                                        e0 + lane, me, ml, T.sim_t, fx, fy,
+                                        fz);
         } else {
           if (fl & MF_SPECIAL)
-            gather_forces_exact<P, false>(S, pos, ej, ekl, width, e0 + lane,
-                                          me, T.sim_t, fx, fy, fz);
-          else if (gather_forces_pipe<P, Tr<P>::UP>(pos, ej, ekl, width,
-                                                     (uint32_t)i, me, fx, fy,
-                                                     fz))
+            gather_forces_exact<P, false>(S, pos, plo, ej, ekl, width,
+                                          e0 + lane, me, ml, T.sim_t, fx, fy,
+                                          fz);
+          else if (gather_forces_pipe<P, Tr<P>::UP>(pos, plo, ej, ekl, width,
+                                                     (uint32_t)i, me, ml, fx,
+                                                     fy, fz))
             degenerate_flags<P, false>(S.ent_s, S.s_degen, S.status, S.ghost,
-                                       i, pos, ej, width, e0 + lane, me);
+                                       i, pos, plo, ej, width, e0 + lane, me,
+                                       ml);
         }
-        finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+        finish_mass<P, false>(S, E, T, i, me, ml, mass_of<P>(S, me, i), v, fl,
+                              fx, fy, fz);
       }
     }
     __syncwarp();
@@ -1107,7 +1212,9 @@ static __global__ void __launch_bounds__(256)
   const R4 *pos = (const R4 *)S.pos[T.cur];
   const R4 pa = pos[ab.x], pb = pos[ab.y];
   const F2 kl = ((const F2 *)S.kL0)[s];
-  const F dx = (F)(pb.x - pa.x), dy = (F)(pb.y - pa.y), dz = (F)(pb.z - pa.z);
+  F dx, dy, dz;
+  pdiff<P>(pa, lo_at<P>(pa, S.plo[T.cur], ab.x), pb,
+           lo_at<P>(pb, S.plo[T.cur], ab.y), dx, dy, dz);
   const F len = sqrt(dx * dx + dy * dy + dz * dz);
   if (len == (F)0.0) {
     if (!S.s_degen[s]) {
@@ -1164,7 +1271,8 @@ static __global__ void __launch_bounds__(256)
   z.x = z.y = z.z = z.w = (R)0.0;
   *fe = z;
   const R4 me = ((const R4 *)S.pos[T.cur])[i];
-  integrate<P>(S, E, T, i, me, v, fl, f0.x, f0.y, f0.z);
+  integrate<P>(S, E, T, i, me, lo_at<P>(me, S.plo[T.cur], i),
+               mass_of<P>(S, me, i), v, fl, f0.x, f0.y, f0.z);
 }
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }

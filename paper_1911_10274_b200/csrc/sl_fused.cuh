@@ -187,9 +187,11 @@ static __global__ void __launch_bounds__(M)
 }
 
 // The fused multi-step kernel (fp32).  Dynamic shared memory:
-//   act (WIN_DMAX double4) | pos [2][M + 1] xy + z | tables [2] +
-//   static table (3 x WIN_DMAX float2) | raw (k, L0) (WIN_DMAX float2) |
-//   entries (rows x M u32: partner | code << 16) | modes
+//   act (WIN_DMAX double4) | pos [2][M + 1] (x, y, z, lx) | low parts
+//   [2][M + 1] (ly, lz) | tables [2] + static table (3 x WIN_DMAX float2) |
+//   raw (k, L0) (WIN_DMAX float2) | entries (rows x M u32: partner |
+//   code << 16) | modes
+// (the global fp32 layout: compensated positions, sl_device.cuh lo_at)
 template <int P, int M>
 static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
     k_fused_small(const KState S, const EnvP E, const FzCfg C, double dt) {
@@ -199,11 +201,11 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
   extern __shared__ __align__(16) unsigned char smem[];
   const int rows = C.ra + C.rb;
   double4 *sact = (double4 *)smem;
-  // positions as xy pairs + z (the partner's mass is never read): one
-  // 8 B + one 4 B shared load per entry, 3 wavefronts instead of 4
-  float2 *sxy = (float2 *)(sact + WIN_DMAX);       // [2][M + 1]
-  float *sz = (float *)(sxy + 2 * (M + 1));  // [2][M + 1]
-  F2 *stab = (F2 *)(sz + 2 * (M + 1) + 2 * (M + 1));  // [3][..]
+  // positions: record (x, y, z, lx) + (ly, lz), one 16 B and one 8 B
+  // shared load per entry
+  float4 *sp4 = (float4 *)(sact + WIN_DMAX);  // [2][M + 1]
+  float2 *sl2 = (float2 *)(sp4 + 2 * (M + 1));  // [2][M + 1]
+  F2 *stab = (F2 *)(sl2 + 2 * (M + 1));  // [3][..]
   F2 *skl = stab + 3 * WIN_DMAX;
   // entries packed as partner | code << 16: one shared load per entry
   uint32_t *sen = (uint32_t *)(skl + WIN_DMAX);
@@ -220,24 +222,28 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
   const bool act = C.has_act[g] != 0;
   // ---- load the group
   R4 me, v;
+  float3 ml = make_float3(0.f, 0.f, 0.f);
+  R mm = (R)1;
   uint32_t fl = 0;
   if (mine) {
     me = ((const R4 *)S.pos[C.cur])[i];
+    ml = lo_at<P>(me, S.plo[C.cur], i);
+    mm = mass_of<P>(S, me, i);
     v = ((const R4 *)S.vel)[i];
     fl = flags_of(v.w);
   } else {
     me.x = me.y = me.z = (R)SENTINEL_POS;
-    me.w = (R)1;
+    me.w = (R)0;
     v.x = v.y = v.z = v.w = (R)0;
   }
-  sxy[li] = make_float2(me.x, me.y);
-  sz[li] = me.z;
+  sp4[li] = me;
+  sl2[li] = make_float2(ml.y, ml.z);
   if (li == 0) {
     R4 far;
     far.x = far.y = far.z = (R)SENTINEL_POS;
     far.w = (R)0;
-    sxy[M] = sxy[2 * M + 1] = make_float2(far.x, far.y);
-    sz[M] = sz[2 * M + 1] = far.z;
+    sp4[M] = sp4[2 * M + 1] = far;
+    sl2[M] = sl2[2 * M + 1] = make_float2(0.f, 0.f);
     sbad = 0;
   }
   for (int q = 0; q < rows; q++) {
@@ -287,12 +293,8 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
   for (; k < C.n_steps; k++) {
     const int b = (int)(k & 1);
     const F2 *tab = act ? stab + b * WIN_DMAX : stab + 2 * WIN_DMAX;
-    const float2 *pxy = sxy + b * (M + 1);
-    const float *pz = sz + b * (M + 1);
-    auto pin = [&](uint32_t p) {
-      const float2 xy = pxy[p];
-      return make_float4(xy.x, xy.y, pz[p], 0.f);
-    };
+    const float4 *pp = sp4 + b * (M + 1);
+    const float2 *pl = sl2 + b * (M + 1);
     R4 np = me;
     if (live) {
       if (fl & MF_FIXED) {  // kernels.py:260-270
@@ -306,27 +308,31 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
 #pragma unroll 4
         for (int q = 0; q < n_a; q++) {
           const uint32_t w = e[q * M];
-          win_body(me, pin(w & 0xFFFFu), tab[w >> 16], gx, gy, gz);
+          win_body(me, ml, pp[w & 0xFFFFu], pl[w & 0xFFFFu], tab[w >> 16],
+                   gx, gy, gz);
         }
 #pragma unroll 4
         for (int q = n_a; q < n_ent; q++) {
           const uint32_t w = e[q * M];
-          win_body(me, pin(w & 0xFFFFu), tab[w >> 16], bx, by, bz);
+          win_body(me, ml, pp[w & 0xFFFFu], pl[w & 0xFFFFu], tab[w >> 16],
+                   bx, by, bz);
         }
         const R fx = f0x + (gx + bx), fy = f0y + (gy + by),
                 fz = f0z + (gz + bz);
         f0x = f0y = f0z = (R)0;
         R4 nv;
-        integrate_vals<P>(S, E, dt, i, me, v, fl, fx, fy, fz, np, nv, ax, ay,
-                          az);
+        float3 nl;
+        integrate_vals<P>(S, E, dt, i, me, ml, mm, v, fl, fx, fy, fz, np, nl,
+                          nv, ax, ay, az);
+        ml = nl;
         v = nv;
         const R z0 = np.x * (R)0 + np.y * (R)0 + np.z * (R)0 + v.x * (R)0 +
                      v.y * (R)0 + v.z * (R)0;
         if (!(z0 == (R)0)) sbad = 1;  // zero-length spring or blow-up
       }
     }
-    sxy[(b ^ 1) * (M + 1) + li] = make_float2(np.x, np.y);
-    sz[(b ^ 1) * (M + 1) + li] = np.z;
+    sp4[(b ^ 1) * (M + 1) + li] = np;
+    sl2[(b ^ 1) * (M + 1) + li] = make_float2(ml.y, ml.z);
     me = np;
     eff_table(k + 1);  // the other buffer: nobody reads it this step
     __syncthreads();
@@ -338,6 +344,7 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
   }
   if (!mine) return;
   ((R4 *)S.pos[C.cur ^ 1])[i] = me;
+  ((float2 *)S.plo[C.cur ^ 1])[i] = make_float2(ml.y, ml.z);
   R4 vo = v;
   set_flags(vo.w, fl & ~MF_FEXT);
   ((R4 *)C.vel_out)[i] = vo;

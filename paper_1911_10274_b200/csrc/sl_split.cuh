@@ -64,7 +64,9 @@ __device__ __forceinline__ uint32_t split_partner(uint32_t w, int a) {
 // `factor` scales the rest length (actuation, 1 otherwise).
 template <int P, bool ACT>
 __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
+                                           typename Tr<P>::L ml,
                                            typename Tr<P>::R4 o,
+                                           typename Tr<P>::L ol,
                                            typename Tr<P>::F2 kl,
                                            float factor,
                                            typename Tr<P>::R &fx,
@@ -72,7 +74,8 @@ __device__ __forceinline__ void split_body(typename Tr<P>::R4 me,
                                            typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using M = typename Tr<P>::M;
-  const M dx = (M)(o.x - me.x), dy = (M)(o.y - me.y), dz = (M)(o.z - me.z);
+  M dx, dy, dz;
+  pdiff<P>(me, ml, o, ol, dx, dy, dz);
   const M len2 = dx * dx + dy * dy + dz * dz;
   M r;
   if constexpr (P == PREC_FP32) {
@@ -197,6 +200,7 @@ __device__ __forceinline__ float act_fast(const ActG *tab, float4 c,
 template <int P, int U, bool PADDED, bool ACT>
 __device__ __forceinline__ void split_fast(const KState &S,
                                            const typename Tr<P>::R4 *pos,
+                                           const void *plo,
                                            const uint32_t *ja,
                                            const uint32_t *jb,
                                            const typename Tr<P>::F2 *kla,
@@ -205,12 +209,14 @@ __device__ __forceinline__ void split_fast(const KState &S,
                                            double sim_t,
                                            int wa, int wb,
                                            typename Tr<P>::R4 me,
+                                           typename Tr<P>::L ml,
                                            typename Tr<P>::R &fx,
                                            typename Tr<P>::R &fy,
                                            typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using R4 = typename Tr<P>::R4;
   using F2 = typename Tr<P>::F2;
+  using L = typename Tr<P>::L;
   const F2 *gkl = (const F2 *)S.sp_kl;
   const float4 *gact = S.sp_actc;
   const double *acto = S.sp_acto;
@@ -228,12 +234,17 @@ __device__ __forceinline__ void split_fast(const KState &S,
     R bx = 0, by = 0, bz = 0;
     for (int t = 0; t < wa || t < wb; t += U) {
       R4 oa[U], ob[U];
+      L la[U], lb[U];
       F2 kb[U];
       float4 ab[U];
       const bool has_a = t < wa, has_b = t < wb;  // warp-uniform
       if (has_a) {
 #pragma unroll
-        for (int u = 0; u < U; u++) oa[u] = ldg4(pos + ja[32 * (t + u)]);
+        for (int u = 0; u < U; u++) {
+          const uint32_t j = ja[32 * (t + u)];
+          oa[u] = ldg4(pos + j);
+          la[u] = lo_at<P>(oa[u], plo, j);
+        }
       }
       if (has_b) {
 #pragma unroll
@@ -242,18 +253,19 @@ __device__ __forceinline__ void split_fast(const KState &S,
           kb[u] = __ldg(gkl + w);
           if constexpr (ACT) ab[u] = __ldg(gact + w);
           ob[u] = ldg4(pos + split_partner(w, a));
+          lb[u] = lo_at<P>(ob[u], plo, split_partner(w, a));
         }
       }
       if (has_a) {
 #pragma unroll
         for (int u = 0; u < U; u++)
-          split_body<P, ACT>(me, oa[u], kla[32 * (t + u)], fa(t + u), fx, fy,
-                             fz);
+          split_body<P, ACT>(me, ml, oa[u], la[u], kla[32 * (t + u)],
+                             fa(t + u), fx, fy, fz);
       }
       if (has_b) {
 #pragma unroll
         for (int u = 0; u < U; u++)
-          split_body<P, ACT>(me, ob[u], kb[u],
+          split_body<P, ACT>(me, ml, ob[u], lb[u], kb[u],
                              ACT ? act_fast(tab, ab[u], acto,
                                             [&] { return jb[32 * (t + u)]; },
                                             sim_t)
@@ -269,18 +281,24 @@ __device__ __forceinline__ void split_fast(const KState &S,
   // section A: partner index + (k, L0) from the source rows
   for (int t = 0; t < wa; t += U) {
     R4 o[U];
+    L lo[U];
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (t + u < wa) o[u] = ldg4(pos + ja[32 * (t + u)]);
+      if (t + u < wa) {
+        const uint32_t j = ja[32 * (t + u)];
+        o[u] = ldg4(pos + j);
+        lo[u] = lo_at<P>(o[u], plo, j);
+      }
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (t + u < wa)
-        split_body<P, ACT>(me, o[u], kla[32 * (t + u)], fa(t + u), fx, fy,
-                           fz);
+        split_body<P, ACT>(me, ml, o[u], lo[u], kla[32 * (t + u)], fa(t + u),
+                           fx, fy, fz);
   }
   // section B: (k, L0) gathered from the partner's A cell (L2)
   for (int t = 0; t < wb; t += U) {
     R4 o[U];
+    L lo[U];
     F2 kl[U];
     float4 ab[U];
 #pragma unroll
@@ -290,11 +308,12 @@ __device__ __forceinline__ void split_fast(const KState &S,
         kl[u] = __ldg(gkl + w);
         if constexpr (ACT) ab[u] = __ldg(gact + w);
         o[u] = ldg4(pos + split_partner(w, a));
+        lo[u] = lo_at<P>(o[u], plo, split_partner(w, a));
       }
 #pragma unroll
     for (int u = 0; u < U; u++)
       if (t + u < wb)
-        split_body<P, ACT>(me, o[u], kl[u],
+        split_body<P, ACT>(me, ml, o[u], lo[u], kl[u],
                            ACT ? act_fast(tab, ab[u], acto,
                                           [&] { return jb[32 * (t + u)]; },
                                           sim_t)
@@ -312,13 +331,14 @@ __device__ __forceinline__ void split_fast(const KState &S,
 template <int P>
 __device__ __forceinline__ void split_entry_exact(
     const KState *S, int64_t e, bool side_b, typename Tr<P>::R4 me,
-    typename Tr<P>::R4 other, typename Tr<P>::F2 kl, double sim_t,
-    typename Tr<P>::R &fx, typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
+    typename Tr<P>::L ml, typename Tr<P>::R4 other, typename Tr<P>::L ol,
+    typename Tr<P>::F2 kl, double sim_t, typename Tr<P>::R &fx,
+    typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   using F = typename Tr<P>::M;
   using FS = typename Tr<P>::F;
-  const F dx = (F)(other.x - me.x), dy = (F)(other.y - me.y),
-          dz = (F)(other.z - me.z);
+  F dx, dy, dz;
+  pdiff<P>(me, ml, other, ol, dx, dy, dz);
   const F len2 = dx * dx + dy * dy + dz * dz;
   const int32_t s = S->sp_s[e];
   if (len2 == (F)0.0) {
@@ -359,10 +379,11 @@ struct Vec3R {
 
 template <int P>
 __device__ __noinline__ Vec3R<typename Tr<P>::R> split_special(
-    const KState *S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
-    const uint32_t *jb, const typename Tr<P>::F2 *kla, int wa, int wb,
-    int64_t ea, int64_t eb, typename Tr<P>::R4 me, double sim_t,
-    typename Tr<P>::R fx, typename Tr<P>::R fy, typename Tr<P>::R fz) {
+    const KState *S, const typename Tr<P>::R4 *pos, const void *plo,
+    const uint32_t *ja, const uint32_t *jb, const typename Tr<P>::F2 *kla,
+    int wa, int wb, int64_t ea, int64_t eb, typename Tr<P>::R4 me,
+    typename Tr<P>::L ml, double sim_t, typename Tr<P>::R fx,
+    typename Tr<P>::R fy, typename Tr<P>::R fz) {
   using F2 = typename Tr<P>::F2;
   const F2 *gkl = (const F2 *)S->sp_kl;
   const uint32_t sent = S->sp_sent, nul = S->sp_null;
@@ -370,31 +391,33 @@ __device__ __noinline__ Vec3R<typename Tr<P>::R> split_special(
   for (int t = 0; t < wa; t++) {
     const uint32_t j = ja[32 * t];
     if (j == sent) continue;
-    split_entry_exact<P>(S, ea + 32 * (int64_t)t, false, me, pos[j],
-                         kla[32 * t], sim_t, fx, fy, fz);
+    split_entry_exact<P>(S, ea + 32 * (int64_t)t, false, me, ml, pos[j],
+                         lo_at<P>(pos[j], plo, j), kla[32 * t], sim_t, fx, fy,
+                         fz);
   }
   for (int t = 0; t < wb; t++) {
     const uint32_t w = jb[32 * t];
     if (w == nul) continue;
-    split_entry_exact<P>(S, eb + 32 * (int64_t)t, true, me,
-                         pos[split_partner(w, a)], gkl[w], sim_t, fx, fy,
-                         fz);
+    const uint32_t j = split_partner(w, a);
+    split_entry_exact<P>(S, eb + 32 * (int64_t)t, true, me, ml, pos[j],
+                         lo_at<P>(pos[j], plo, j), gkl[w], sim_t, fx, fy, fz);
   }
   return {fx, fy, fz};
 }
 
 template <int P, int U, bool PADDED, bool ACT>
 __device__ __forceinline__ void split_forces(
-    const KState &S, const typename Tr<P>::R4 *pos, const uint32_t *ja,
-    const uint32_t *jb, const typename Tr<P>::F2 *kla, const float4 *kaa,
-    uint32_t kc0, const ActG *tab, int wa, int wb, int64_t ea, int64_t eb, uint32_t fl,
-    typename Tr<P>::R4 me, double sim_t, typename Tr<P>::R &fx,
+    const KState &S, const typename Tr<P>::R4 *pos, const void *plo,
+    const uint32_t *ja, const uint32_t *jb, const typename Tr<P>::F2 *kla,
+    const float4 *kaa, uint32_t kc0, const ActG *tab, int wa, int wb,
+    int64_t ea, int64_t eb, uint32_t fl, typename Tr<P>::R4 me,
+    typename Tr<P>::L ml, double sim_t, typename Tr<P>::R &fx,
     typename Tr<P>::R &fy, typename Tr<P>::R &fz) {
   using R = typename Tr<P>::R;
   if (!(fl & MF_SPECIAL)) {
     R gx = fx, gy = fy, gz = fz;
-    split_fast<P, U, PADDED, ACT>(S, pos, ja, jb, kla, kaa, kc0, tab, sim_t, wa,
-                                  wb, me, gx, gy, gz);
+    split_fast<P, U, PADDED, ACT>(S, pos, plo, ja, jb, kla, kaa, kc0, tab,
+                                  sim_t, wa, wb, me, ml, gx, gy, gz);
     if (isfinite(gx + gy + gz)) {
       fx = gx;
       fy = gy;
@@ -402,8 +425,8 @@ __device__ __forceinline__ void split_forces(
       return;
     }
   }
-  const Vec3R<R> f = split_special<P>(S.self, pos, ja, jb, kla, wa, wb, ea,
-                                      eb, me, sim_t, fx, fy, fz);
+  const Vec3R<R> f = split_special<P>(S.self, pos, plo, ja, jb, kla, wa, wb,
+                                      ea, eb, me, ml, sim_t, fx, fy, fz);
   fx = f.x;
   fy = f.y;
   fz = f.z;
@@ -428,6 +451,8 @@ static __global__ void __launch_bounds__(256)
   const uint32_t fl = flags_of(v.w);
   if (!(fl & MF_ALIVE)) return;
   const R4 me = pos[i];
+  const void *plo = S.plo[T.cur];
+  const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
   R fx, fy, fz;
   initial_force<P>(S, i, fl, FORCE_ONLY, fx, fy, fz);
   const int64_t w = i >> 5;
@@ -435,13 +460,14 @@ static __global__ void __launch_bounds__(256)
   const int64_t ea = w * S.sp_rows * 32 + (i & 31);
   const int64_t eb = ea + ((int64_t)32 << S.sp_a);
   const int64_t kc = (w << (S.sp_a + 5)) | (i & 31);
-  split_forces<P, 4, false, ACT>(S, pos, S.sp_j + ea, S.sp_j + eb,
+  split_forces<P, 4, false, ACT>(S, pos, plo, S.sp_j + ea, S.sp_j + eb,
                                  (const F2 *)S.sp_kl + kc,
                                  ACT ? S.sp_actc + kc : nullptr,
                                  (uint32_t)kc, tab,
-                                 wd & 0xFFFF, wd >> 16, ea, eb, fl, me,
+                                 wd & 0xFFFF, wd >> 16, ea, eb, fl, me, ml,
                                  T.sim_t, fx, fy, fz);
-  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, v, fl, fx, fy, fz);
+  finish_mass<P, FORCE_ONLY>(S, E, T, i, me, ml, mass_of<P>(S, me, i), v,
+                             fl, fx, fy, fz);
 }
 
 // TMA-pipelined fused step on the split layout (production path of the
@@ -552,19 +578,22 @@ static __global__ void __launch_bounds__(SPLIT_MAX_WARPS * 32)
       const uint32_t fl = flags_of(v.w);
       if (fl & MF_ALIVE) {
         const R4 me = ((const R4 *)st)[lane];
+        const void *plo = S.plo[T.cur];
+        const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
         R fx, fy, fz;
         initial_force<P>(S, i, fl, false, fx, fy, fz);
         const int64_t ea = s * rows32 + lane;
         const int64_t eb = ea + ((int64_t)32 << a);
         split_forces<P, U, true, ACT>(
-            S, pos, (const uint32_t *)(st + ja_off) + lane,
+            S, pos, plo, (const uint32_t *)(st + ja_off) + lane,
             (const uint32_t *)(st + jb_off) + lane,
             (const F2 *)(st + kl_off) + lane,
             (const float4 *)(st + ac_off) + lane,
             ((uint32_t)s << (a + 5)) | (uint32_t)lane, tab, wd & 0xFFFF,
             wd >> 16,
-            ea, eb, fl, me, T.sim_t, fx, fy, fz);
-        finish_mass<P, false>(S, E, T, i, me, v, fl, fx, fy, fz);
+            ea, eb, fl, me, ml, T.sim_t, fx, fy, fz);
+        finish_mass<P, false>(S, E, T, i, me, ml, mass_of<P>(S, me, i), v, fl,
+                              fx, fy, fz);
       }
     }
     __syncwarp();

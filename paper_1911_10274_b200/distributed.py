@@ -49,18 +49,40 @@ def context_for_case(case: dict, device: int = 0, precision: str = "fp64",
 class _DeviceArray:
     def __init__(self, ptr: int, rows: int, record_bytes: int):
         self.__cuda_array_interface__ = {
-            "shape": (rows, 4),
-            "typestr": "<f4" if record_bytes == 16 else "<f8",
+            "shape": (rows, 2 if record_bytes == 8 else 4),
+            "typestr": "<f8" if record_bytes == 32 else "<f4",
             "data": (ptr, False), "version": 2, "strides": None}
 
 
 def position_view(ctx: _native.Context):
-    """torch view (rows, 4) = (x, y, z, m) of the buffer the next step
-    reads.  Re-fetch after every step (the buffers ping-pong)."""
+    """torch view of the buffer the next step reads: (rows, 4) = (x, y, z,
+    m); in fp32 mode a pair: the records (x, y, z, lx) and the position low
+    parts (ly, lz) (sl_state_lo) -- the halo moves all six.  Re-fetch after
+    every step (the buffers ping-pong)."""
     import torch
     ptr, rows, rb = ctx.state_pointers()
-    return torch.as_tensor(_DeviceArray(ptr, rows, rb),
-                           device=f"cuda:{ctx.device}")
+    dev = f"cuda:{ctx.device}"
+    hi = torch.as_tensor(_DeviceArray(ptr, rows, rb), device=dev)
+    lo = ctx.state_lo()
+    if not lo:
+        return hi
+    return _HiLo(hi, torch.as_tensor(_DeviceArray(lo, rows, 8), device=dev))
+
+
+class _HiLo:
+    """(record, low part) pair behind the exchange's row indexing."""
+
+    def __init__(self, hi, lo):
+        self.hi, self.lo = hi, lo
+        self.device, self.dtype = hi.device, hi.dtype
+
+    def rows(self, idx):
+        import torch
+        return torch.cat([self.hi[idx, :4], self.lo[idx, :2]], dim=1)
+
+    def set_rows(self, idx, buf):
+        self.hi[idx, :4] = buf[:, :4]
+        self.lo[idx, :2] = buf[:, 4:6]
 
 
 class PartitionedRun:

@@ -152,13 +152,16 @@ def exchange(plan: HaloPlan, pos, dist=None, group=None):
         import torch.distributed as dist
     ops, inbox = [], {}
     dev = pos.device
+    # fp32 contexts expose (record, low part) pairs (distributed._HiLo)
+    split = hasattr(pos, "rows")
+    cols = 6 if split else 3
     for q in plan.peers:
         if q in plan.send:
             idx = torch.as_tensor(plan.send[q], device=dev)
-            ops.append(dist.P2POp(dist.isend,
-                                  pos[idx, :3].contiguous(), q, group))
+            rows = pos.rows(idx) if split else pos[idx, :3]
+            ops.append(dist.P2POp(dist.isend, rows.contiguous(), q, group))
         if q in plan.recv:
-            buf = torch.empty((len(plan.recv[q]), 3), dtype=pos.dtype,
+            buf = torch.empty((len(plan.recv[q]), cols), dtype=pos.dtype,
                               device=dev)
             inbox[q] = buf
             ops.append(dist.P2POp(dist.irecv, buf, q, group))
@@ -167,7 +170,10 @@ def exchange(plan: HaloPlan, pos, dist=None, group=None):
             w.wait()
     for q, buf in inbox.items():
         idx = torch.as_tensor(plan.recv[q], device=dev)
-        pos[idx, :3] = buf
+        if split:
+            pos.set_rows(idx, buf)
+        else:
+            pos[idx, :3] = buf
     return pos
 
 

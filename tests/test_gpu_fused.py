@@ -65,7 +65,7 @@ def _oracle(case, times, dt, kill=None, kill_at=None):
 @pytest.mark.parametrize("worm", [False, True])
 def test_fused_robots_match_per_step_and_oracle(worm):
     case = _lattice_case(0, 0, 0, robots=11, worm=worm)
-    dt, n = 1e-4, 120
+    dt, n = 1e-4, 100
     times = np.arange(n, dtype=np.float64) * dt
     f = _run(case, times, dt, True, chunks=(50,))
     p = _run(case, times, dt, False, chunks=(50,))
@@ -79,10 +79,9 @@ def test_fused_robots_match_per_step_and_oracle(worm):
     assert np.array_equal(f["alive"], p["alive"])
     ref = _oracle(case, times, dt)
     assert rel_maxnorm(f["pos"], ref["m_pos"]) < 1e-4
-    # fp32 STATE on stiff robots (E = 1e6, m ~ 1 g): the per-step kernels
-    # carry the same velocity error vs the fp64 reference (test_gpu_parity
-    # FP32_STATE_VEL_BOUND); precision="mixed" is the 1e-4 mode
-    assert rel_maxnorm(f["vel"], ref["m_vel"]) < 2e-3
+    # north_star fp32 contract over the 100-step horizon (compensated
+    # positions)
+    assert rel_maxnorm(f["vel"], ref["m_vel"]) < 1e-4
 
 
 @pytest.mark.parametrize("big", [False, True])
@@ -140,4 +139,4 @@ def test_fused_large_body_1024_threads(dims):
     assert np.array_equal(f["alive"], p["alive"])
     ref = _oracle(case, times, dt)
     assert rel_maxnorm(f["pos"], ref["m_pos"]) < 1e-4
-    assert rel_maxnorm(f["vel"], ref["m_vel"]) < 5e-4
+    assert rel_maxnorm(f["vel"], ref["m_vel"]) < 1e-4

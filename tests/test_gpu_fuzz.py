@@ -182,7 +182,7 @@ def test_fuzz_tolerance_modes(seed, shape, precision):
                      yields=False, zero_length=shape != "components")
     pos, vel, alive, degen, c, st, ref, rc = run(case, precision, 30)
     assert rel_maxnorm(pos, ref["m_pos"]) < 1e-4
-    assert rel_maxnorm(vel, ref["m_vel"]) < 2e-3
+    assert rel_maxnorm(vel, ref["m_vel"]) < 1e-4
     assert np.array_equal(alive, ref["s_alive"])
     assert np.array_equal(degen, ref["s_degen"])
     assert c.tolist() == rc.tolist()

@@ -56,7 +56,10 @@ def partitioned(case, ranks, steps, dt, precision="fp64"):
             for q, idx in p.recv.items():
                 src = torch.as_tensor(plans[q].send[p.rank], device="cuda")
                 dst = torch.as_tensor(idx, device="cuda")
-                views[p.rank][dst, :3] = views[q][src, :3]
+                if hasattr(views[q], "rows"):  # fp32: record + low part
+                    views[p.rank].set_rows(dst, views[q].rows(src))
+                else:
+                    views[p.rank][dst, :3] = views[q][src, :3]
         torch.cuda.synchronize()
         for r, run in enumerate(runs):
             run.ctx.step_async(np.array([n * dt]), dt, _native.ACC_GATHER)
