@@ -58,6 +58,8 @@ def parse():
                     choices=["gather", "atomic"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true",
+                    help="skip the fp64 parity-mode sub-measurement")
     return ap.parse_args()
 
 
@@ -145,10 +147,15 @@ def algorithmic_bytes(springs: int, masses: int, precision: str,
                       extra_words: int = 0) -> int:
     """B = S*Bs + M*Bm.  Bs = int32 i,j + k, L0 words (+ an
     actuation phase word for actuated springs); Bm = pos r+w, vel r+w, m r
-    (words of the state precision)."""
+    (words of the state precision).  The fp32 mode's positions are
+    compensated (hi + lo): 6 position words r+w, so
+    Bm = (12 + 6 + 1) x 4 = 76 B."""
     w_s = 8 if precision == "fp64" else 4
-    w_m = 4 if precision == "fp32" else 8
-    return springs * (8 + (2 + extra_words) * w_s) + masses * 13 * w_m
+    if precision == "fp32":
+        bm = 19 * 4
+    else:
+        bm = 13 * 8
+    return springs * (8 + (2 + extra_words) * w_s) + masses * bm
 
 
 def store_case(st, env):
@@ -394,7 +401,11 @@ def main():
     clocks = ClockSampler(local)
     mir.ctx.timer_start()
     done, err = mir.ctx.step(times(args.steps), dt, acc, counters)
-    ms = mir.ctx.timer_stop()
+    call_ms = mir.ctx.timer_stop()
+    # device time of the K step kernels: events on the library stream
+    # right before the first and right after the last (sl_last_step_ms);
+    # call_ms adds the call's status reset / read-back around them
+    ms = mir.ctx.last_step_ms()
     clk = clocks.stop()
     stats = mir.ctx.stats()
     launches = stats["kernel_launches"] - launches0
@@ -418,6 +429,29 @@ def main():
         total_springs = int(reduce_(springs, dist.ReduceOp.SUM, torch.int64))
     value = total_springs * args.steps / sec
     ms_per_step = 1e3 * sec / args.steps
+
+    # fp64 parity mode (bit-exact with the reference) on the same workload:
+    # the like-for-like (fp64 vs fp64) figure beside the reference arm
+    fp64 = None
+    if (args.config == "B" and args.precision != "fp64" and world == 1
+            and not args.no_fp64):
+        m64 = engine.DeviceMirror(local, "fp64")  # not the store's cache
+        m64.push(st, env)
+        c64 = np.zeros(3, np.int64)
+        k64 = min(args.steps, 200)
+        t64 = np.arange(max(3, args.warmup) + k64, dtype=np.float64) * dt
+        m64.ctx.step(t64[:max(3, args.warmup)], dt, acc, c64)
+        m64.ctx.sync()
+        m64.ctx.step(t64[max(3, args.warmup):], dt, acc, c64)
+        s64 = m64.ctx.last_step_ms() / 1e3
+        st64 = m64.ctx.stats()
+        fp64 = {"value": springs * k64 / s64, "unit": unit,
+                "ms_per_step": 1e3 * s64 / k64, "steps": k64,
+                "kernel": STEP_PATHS.get(st64["step_path"], "?"),
+                "dtype": "f64",
+                "parity": "bit-exact vs the reference (tests/"
+                          "test_gpu_benchscale.py)"}
+        m64.ctx.close()
 
     # roofline of the dominant kernel (the fused gather step: one launch per
     # step, so its average duration is the per-step device time)
@@ -510,6 +544,8 @@ def main():
                            "parallelism": f"batched instances x{world}"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(launches), "clocks": clk,
+                "call_ms_per_step": call_ms / args.steps,
+                "fp64_parity_mode": fp64,
                 "vs_baseline_ref": "PAPER.md:10 3.0e8 spring updates/s"}
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -299,6 +299,11 @@ int sl_host_masked_extrema(const double *v, const uint8_t *mask, int64_t n,
 /* CUDA events on the context's stream (bench.py measures with these). */
 int sl_timer_start(sl_ctx *ctx);
 int sl_timer_stop(sl_ctx *ctx, float *ms);
+/* Device time of the step kernels of the last sl_step call: CUDA events
+ * recorded on the context stream right before its first step kernel and
+ * right after its last (the call's validation, status reset and status
+ * read-back excluded). */
+int sl_last_step_ms(sl_ctx *ctx, float *ms);
 int sl_sync(sl_ctx *ctx);
 
 #ifdef __cplusplus

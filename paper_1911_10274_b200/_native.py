@@ -33,6 +33,7 @@ EXPORTS = (
     "sl_spring_pass", "sl_mass_pass", "sl_download_masses",
     "sl_download_springs", "sl_snapshot_begin", "sl_snapshot_ready",
     "sl_snapshot_wait", "sl_timer_start", "sl_timer_stop", "sl_sync",
+    "sl_last_step_ms",
     "sl_step_async", "sl_step_finish", "sl_mark_ghosts", "sl_state_pointers",
     "sl_state_lo", "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
@@ -98,6 +99,7 @@ def load_library(path: str = LIB_PATH):
             "sl_snapshot_wait": ([P, P, P], I),
             "sl_timer_start": ([P], I),
             "sl_timer_stop": ([P, P], I),
+            "sl_last_step_ms": ([P, P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -505,6 +507,13 @@ class Context:
         ms = C.c_float(0.0)
         self._check(self.lib.sl_timer_stop(self.h, C.byref(ms)),
                     "sl_timer_stop")
+        return float(ms.value)
+
+    def last_step_ms(self) -> float:
+        """Device time of the step kernels of the last step() call."""
+        ms = C.c_float(0.0)
+        self._check(self.lib.sl_last_step_ms(self.h, C.byref(ms)),
+                    "sl_last_step_ms")
         return float(ms.value)
 
     def sync(self):

@@ -79,6 +79,9 @@ struct sl_ctx {
   int prec = PREC_FP64;
   size_t rsz = 8, fsz = 8;  // sizeof(R), sizeof(F)
   cudaStream_t st = nullptr, side = nullptr;
+  // k0 / k1 bracket the step kernels of the last sl_step call
+  cudaEvent_t k0 = nullptr, k1 = nullptr;
+  bool k_valid = false;
   cudaEvent_t t0 = nullptr, t1 = nullptr, snap_ev = nullptr,
               snap_done = nullptr;
   int64_t m_n = 0, s_n = 0;
@@ -1361,8 +1364,11 @@ int run_fused(sl_ctx *c, const KState &S, int64_t n, const double *times,
   f.n_steps = n;
   f.cur = c->cur;
   f.write_acc = 1;
+  CK(cudaEventRecord(c->k0, c->st));
   launchers(c->prec).fused(S, c->env, f, dt, c->fz_smem, c->st);
   CKL();
+  CK(cudaEventRecord(c->k1, c->st));
+  c->k_valid = true;
   c->launches++;
   c->fz_launches++;
   CK(cudaMemcpyAsync(c->h_status, c->status.p, 8 * 8, cudaMemcpyDeviceToHost,
@@ -1670,6 +1676,8 @@ int sl_create(int device, int precision, sl_ctx **out) {
     e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&c->t0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->t1);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->k0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->k1);
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
@@ -1723,6 +1731,8 @@ int sl_destroy(sl_ctx *c) {
   if (c->snap_host) cudaFreeHost(c->snap_host);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
+  if (c->k0) cudaEventDestroy(c->k0);
+  if (c->k1) cudaEventDestroy(c->k1);
   if (c->snap_ev) cudaEventDestroy(c->snap_ev);
   if (c->snap_done) cudaEventDestroy(c->snap_done);
   if (c->st) cudaStreamDestroy(c->st);
@@ -2217,6 +2227,8 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
       return SL_OK;
     }
   }
+  c->k_valid = false;
+  CK(cudaEventRecord(c->k0, c->st));
   for (int64_t n = 0; n < n_steps; n++) {
     StepP T;
     T.sim_t = sim_times[n];
@@ -2251,6 +2263,8 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     }
   }
   CKL();
+  CK(cudaEventRecord(c->k1, c->st));
+  c->k_valid = true;
   int64_t err = 0;
   if ((rc = finish_status(c, counters, &err))) return rc;
   int64_t done = n_steps;
@@ -2635,6 +2649,14 @@ int sl_timer_stop(sl_ctx *c, float *ms) {
   CK(cudaEventRecord(c->t1, c->st));
   CK(cudaEventSynchronize(c->t1));
   CK(cudaEventElapsedTime(ms, c->t0, c->t1));
+  return SL_OK;
+}
+
+int sl_last_step_ms(sl_ctx *c, float *ms) {
+  if (!c || !ms) return fail(c, SL_EINVAL, "NULL argument");
+  if (!c->k_valid) return fail(c, SL_ESTATE, "no sl_step call timed yet");
+  CK(cudaEventSynchronize(c->k1));
+  CK(cudaEventElapsedTime(ms, c->k0, c->k1));
   return SL_OK;
 }
 
