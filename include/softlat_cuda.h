@@ -214,6 +214,15 @@ int sl_spring_pass(sl_ctx *ctx, double sim_t, int accumulation,
 /* Single mass pass only (engine.mass_pass, engine.py:218-255). */
 int sl_mass_pass(sl_ctx *ctx, double dt, int64_t *err_slot);
 
+/* Opt-in spring damping (north_star "Hooke plus damping"): damping[s] =
+ * c >= 0 (N s / m) for every spring slot [0, s_n); the force on m1 gains
+ * c ((v2 - v1) . d^) d^ (equal and opposite on m2).  No reference
+ * counterpart (kernels.py:66 is Hooke only): c = 0 everywhere restores the
+ * reference path bit for bit.  A full sl_upload_springs clears the
+ * dampers; damped contexts step the force pass and the mass pass as two
+ * kernels. */
+int sl_set_spring_damping(sl_ctx *ctx, int64_t n, const double *damping);
+
 /* ---------------------------------------------------------------- download */
 /* Copy mass state back into host arrays double[m_n][3]; NULL skips. */
 int sl_download_masses(sl_ctx *ctx, double *pos, double *vel, double *acc,

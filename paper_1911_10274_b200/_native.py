@@ -38,7 +38,7 @@ EXPORTS = (
     "sl_state_lo", "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
     "sl_build_lattice", "sl_host_fill", "sl_host_copy",
-    "sl_host_masked_extrema")
+    "sl_host_masked_extrema", "sl_set_spring_damping")
 
 
 class SlStats(C.Structure):
@@ -100,6 +100,7 @@ def load_library(path: str = LIB_PATH):
             "sl_timer_start": ([P], I),
             "sl_timer_stop": ([P, P], I),
             "sl_last_step_ms": ([P, P], I),
+            "sl_set_spring_damping": ([P, I64, P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -508,6 +509,12 @@ class Context:
         self._check(self.lib.sl_timer_stop(self.h, C.byref(ms)),
                     "sl_timer_stop")
         return float(ms.value)
+
+    def set_spring_damping(self, damping):
+        """Per-spring damping c for slots [0, s_n) (zeros clear it)."""
+        d = _c(damping, np.float64)
+        self._check(self.lib.sl_set_spring_damping(self.h, len(d), _ptr(d)),
+                    "sl_set_spring_damping")
 
     def last_step_ms(self) -> float:
         """Device time of the step kernels of the last step() call."""

@@ -97,6 +97,8 @@ struct sl_ctx {
   bool has_lc = false;
   // spring SoA
   DevBuf ends, kL0, s_alive, s_degen, mode, act, thr, custom, m1gen, m2gen;
+  DevBuf damp;               // per-spring damping (sl_set_spring_damping)
+  bool has_damping = false;  // some spring has c != 0
   // incidence layout
   DevBuf slice_ptr, ent_j, ent_kL0, ent_s, e1, e2;
   int64_t n_slices = 0, n_entries = 0, alive_springs = 0, layout_builds = 0;
@@ -389,7 +391,7 @@ __global__ void k_pack_springs(int64_t n, const int64_t *slots,
     // keep the incidence copies of (k, L0) and the special bit in sync;
     // the split layout runs grouped sine actuation in its fast path
     bool special = (mode[r] != 0 && !(S.split && grp_in[r] != 0)) ||
-                   yield[r] != CUDART_INF;
+                   yield[r] != CUDART_INF || (S.damp && S.damp[s] != 0.0);
     int2 ab = S.ends[s];
     if (special && ab.x >= 0) {
       using R4 = typename Tr<P>::R4;
@@ -600,8 +602,9 @@ __global__ void k_fill_layout(int64_t n, const uint32_t *keys,
   int64_t e = S.slice_ptr[i >> 5] + 32 * rank + (i & 31);
   int2 ab = S.ends[s];
   uint32_t other = side ? (uint32_t)ab.x : (uint32_t)ab.y;
-  bool special =
-      S.mode[s] != 0 || ((const F *)S.thr)[s] != (F)CUDART_INF;
+  bool special = S.mode[s] != 0 ||
+                 ((const F *)S.thr)[s] != (F)CUDART_INF ||
+                 (S.damp && S.damp[s] != 0.0);
   ent_j[e] = other | (side ? EJ_M2 : 0u) | (special ? EJ_SPECIAL : 0u);
   if (special) {
     S.xflags[i] = 1;
@@ -714,7 +717,8 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
     e2[s] = e;
   }
   bool special = (S.mode[s] != 0 && grp[s] == 0) ||
-                 ((const F *)S.thr)[s] != (F)CUDART_INF;
+                 ((const F *)S.thr)[s] != (F)CUDART_INF ||
+                 (S.damp && S.damp[s] != 0.0);
   if (special) {
     S.xflags[owner] = 1;
     or_flags((typename Tr<P>::R4 *)S.vel + owner, MF_SPECIAL);
@@ -746,6 +750,7 @@ KState make_state(sl_ctx *c) {
   S.act = c->act.as<double4>();
   S.thr = c->thr.p;
   S.custom = c->custom.as<double>();
+  S.damp = c->has_damping ? c->damp.as<double>() : nullptr;
   S.slice_ptr = c->slice_ptr.as<int64_t>();
   S.ent_j = c->ent_j.as<uint32_t>();
   S.ent_kL0 = c->ent_kL0.p;
@@ -1976,6 +1981,7 @@ int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
   int rc = ensure_springs(c, s_n);
   if (rc) return rc;
   c->has_special = false;
+  c->has_damping = false;  // a full upload clears the dampers (re-sent)
   c->s_n = s_n;
   c->layout_valid = false;
   rc = upload_springs_impl(c, s_n, nullptr, m1, m2, m1gen, m2gen, rest, k,
@@ -2171,6 +2177,32 @@ int sl_set_local_constraints(sl_ctx *c, int64_t m_n, const int64_t *lc_off,
   return SL_OK;
 }
 
+int sl_set_spring_damping(sl_ctx *c, int64_t n, const double *damping) {
+  if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
+  if (n != c->s_n || (n > 0 && !damping))
+    return fail(c, SL_EINVAL, "sl_set_spring_damping: need s_n values");
+  bool any = false;
+  for (int64_t r = 0; r < n; r++) {
+    if (!(damping[r] >= 0.0) || !std::isfinite(damping[r]))
+      return fail(c, SL_EINVAL, "damping of spring %lld must be finite and "
+                  ">= 0, got %g", (long long)r, damping[r]);
+    any |= damping[r] != 0.0;
+  }
+  CK(cudaSetDevice(c->device));
+  if (any) {
+    CK(c->damp.ensure(8 * n));
+    CK(cudaMemcpyAsync(c->damp.p, damping, 8 * n, cudaMemcpyHostToDevice,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  // damped springs take the exact per-entry path: the special flags of the
+  // incidence layouts change, so the layout is rebuilt at the next step
+  if (any || c->has_damping) c->layout_valid = false;
+  c->has_damping = any;
+  c->has_special |= any;
+  return SL_OK;
+}
+
 int sl_set_custom_factors(sl_ctx *c, int64_t n, const int64_t *slots,
                           const double *factors) {
   if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
@@ -2214,7 +2246,7 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
   KState S = make_state(c);
   if ((rc = upload_state(c, S))) return rc;
   if (accumulation == SL_ACC_GATHER && c->fz_ok && !c->has_ghost &&
-      n_steps >= 2) {
+      !c->has_damping && n_steps >= 2) {
     // small bodies: all n steps in one launch, state on chip
     bool aborted = false;
     if ((rc = run_fused(c, S, n_steps, sim_times, dt, &aborted))) return rc;
@@ -2240,7 +2272,17 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     // aborting step's accelerations, as the reference's mass pass does
     // (kernels.py:368-376)
     T.write_acc = n == n_steps - 1 || c->prec == PREC_FP64;
-    if (accumulation == SL_ACC_GATHER) {
+    T.early = n > 0;
+    if (accumulation == SL_ACC_GATHER && c->has_damping) {
+      // dampers read neighbour velocities: the force pass (into f_ext) and
+      // the mass pass as two kernels, gather order kept
+      if (c->split)
+        L.split_force(S, c->env, T, c->agrp, c->st);
+      else
+        L.force_only(S, c->env, T, c->st);
+      L.mass(S, c->env, T, c->st);
+      c->launches += 2;
+    } else if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
         if (c->win)
           L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);
@@ -2293,6 +2335,7 @@ int sl_spring_pass(sl_ctx *c, double sim_t, int accumulation,
   T.step = 0;
   T.cur = c->cur;
   T.write_acc = 0;
+  T.early = 0;
   if (accumulation == SL_ACC_GATHER) {
     if (c->split)
       L.split_force(S, c->env, T, c->agrp, c->st);
@@ -2323,6 +2366,7 @@ int sl_mass_pass(sl_ctx *c, double dt, int64_t *err_slot) {
   T.step = 0;
   T.cur = c->cur;
   T.write_acc = 1;
+  T.early = 0;
   launchers(c->prec).mass(S, c->env, T, c->st);
   c->launches++;
   CKL();
@@ -2509,7 +2553,17 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
     T.step = base + n;
     T.cur = (int)((cur0 + n) & 1);
     T.write_acc = 1;
-    if (accumulation == SL_ACC_GATHER) {
+    T.early = n > 0;  // a foreign launch (halo) may precede this chunk
+    if (accumulation == SL_ACC_GATHER && c->has_damping) {
+      // dampers read neighbour velocities: the force pass (into f_ext) and
+      // the mass pass as two kernels, gather order kept
+      if (c->split)
+        L.split_force(S, c->env, T, c->agrp, c->st);
+      else
+        L.force_only(S, c->env, T, c->st);
+      L.mass(S, c->env, T, c->st);
+      c->launches += 2;
+    } else if (accumulation == SL_ACC_GATHER) {
       if (c->split) {
         if (c->win)
           L.win(S, c->env, T, c->wcfg, c->win_grid, c->st);

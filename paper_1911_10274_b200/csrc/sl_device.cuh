@@ -91,6 +91,12 @@ struct KState {
   const double4 *act;  // (amp, freq, off, per)
   const void *thr;     // F: yield * area, +inf if no yield
   const double *custom;
+  // per-spring damping c (N s / m) of the opt-in damper along the spring
+  // (north_star "Hooke plus damping"; no reference counterpart,
+  // kernels.py:66 is Hooke only); null when every spring has c = 0.
+  // Damped springs are special (exact per-entry path) and a damped context
+  // steps force pass + mass pass as two kernels (no in-place velocity race)
+  const double *damp;
   // incidence layout
   const int64_t *slice_ptr;
   uint32_t *ent_j;
@@ -139,6 +145,10 @@ struct StepP {
   int64_t step;   // index within the current sl_step call
   int cur;        // pos buffer read this step
   int write_acc;  // store acceleration (final step of a launch)
+  // the previous launch on the stream is a step kernel of this same call
+  // on the same layout (host-set): the window kernel may then request its
+  // first tile's layout data before the grid-dependency wait
+  int early;
 };
 
 // fp64 / mixed state: a position is its R4 record alone
@@ -537,6 +547,22 @@ __device__ __forceinline__ void fixed_mass(const KState &S, const StepP &T,
   }
 }
 
+// Damper term of spring s as a multiple of d = pos[m2] - pos[m1]:
+// c ((v2 - v1) . d) / |d|^2, i.e. c ((v2 - v1) . d^) d^ on m1 (equal and
+// opposite on m2; both endpoints form the same bits).  0 for c = 0.
+template <int P, class F>
+__device__ __forceinline__ F damper_scale(const KState &S, int64_t s, F dx,
+                                          F dy, F dz, F len2) {
+  using R4 = typename Tr<P>::R4;
+  const double c = S.damp[s];
+  if (c == 0.0) return (F)0;
+  const int2 ab = S.ends[s];
+  const R4 v1 = ((const R4 *)S.vel)[ab.x], v2 = ((const R4 *)S.vel)[ab.y];
+  const F vr = (F)(v2.x - v1.x) * dx + (F)(v2.y - v1.y) * dy +
+               (F)(v2.z - v1.z) * dz;
+  return (F)c * vr / len2;
+}
+
 // ---------------------------------------------------------------------------
 // One incidence entry: spring force between this mass and `other`, in the
 // reference's operation order (kernels.py:46-83).  Returns false if the
@@ -593,6 +619,8 @@ __device__ __forceinline__ bool entry_force(
     scale = fmag / len;
   else
     scale = fmag * inv;
+  if ((jr & EJ_SPECIAL) && S.damp)
+    scale += damper_scale<P, F>(S, S.ent_s[e], dx, dy, dz, len2);
   if (is_m2) scale = -scale;  // -(s*d) == (-s)*d exactly; f - g == f + (-g)
   fx += (R)(scale * dx);
   fy += (R)(scale * dy);
@@ -1230,7 +1258,9 @@ static __global__ void __launch_bounds__(256)
     if (S.mode[s] != 0) factor = (F)act_factor(S, s, T.sim_t);
   }
   const F fmag = (F)kl.x * (len - factor * (F)kl.y);
-  const F scale = fmag / len;
+  F scale = fmag / len;
+  if (SPECIAL && S.damp)
+    scale += damper_scale<P, F>(S, s, dx, dy, dz, dx * dx + dy * dy + dz * dz);
   const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
   R4 *fe = (R4 *)S.fext;
   red_add(fe + ab.x, (R)gx, (R)gy, (R)gz);

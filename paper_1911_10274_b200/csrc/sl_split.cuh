@@ -353,7 +353,21 @@ __device__ __forceinline__ void split_entry_exact(
   if (mode != 0) factor = (F)act_factor(*S, s, sim_t);
   const F len = sqrt(len2);
   const F fmag = (F)kl.x * (len - factor * (F)kl.y);
-  const F scale = fmag / len;
+  F scale = fmag / len;
+  if (S->damp) {
+    // damper on d = other - me: c ((v_other - v_me) . d) / |d|^2, the same
+    // bits at both endpoints (both vectors negate)
+    const double c = S->damp[s];
+    if (c != 0.0) {
+      const int2 ab = S->ends[s];
+      using R4 = typename Tr<P>::R4;
+      const R4 vm = ((const R4 *)S->vel)[side_b ? ab.y : ab.x];
+      const R4 vo = ((const R4 *)S->vel)[side_b ? ab.x : ab.y];
+      const F vr = (F)(vo.x - vm.x) * dx + (F)(vo.y - vm.y) * dy +
+                   (F)(vo.z - vm.z) * dz;
+      scale += (F)c * vr / len2;
+    }
+  }
   fx += (R)(scale * dx);
   fy += (R)(scale * dy);
   fz += (R)(scale * dz);

@@ -136,6 +136,13 @@ class DeviceMirror:
                                 len(store._s_journal))
             self._custom_slots = np.array(
                 sorted(k for k in store._s_custom if k < s), dtype=np.int64)
+            self._damp_sent = False  # a full upload clears the dampers
+        if store.has_damping and (key != getattr(self, "_damp_key", None)
+                                  or not getattr(self, "_damp_sent", False)):
+            # opt-in dampers (Spring.damping): the whole column
+            self.ctx.set_spring_damping(store._s_damp[:s])
+            self._damp_key = key
+            self._damp_sent = True
         ckey = (m, store.constraint_version, id(store._m_pos))
         if ckey != self._constraints_key or masses:
             # the CSR is rebuilt only when the constraints change; a mass
