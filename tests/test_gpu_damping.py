@@ -39,8 +39,9 @@ def test_damped_oscillator_known_answer(precision, acc):
     dt, n = 1e-5, 40000  # 0.4 s
     cfg = StepConfig(dt=dt, precision=precision, accumulation=acc)
     xs = []
-    for _ in range(40):
-        engine.run_steps(st, Environment(), cfg, n // 40)
+    for _ in range(40):  # no gravity: a pure axial oscillator
+        engine.run_steps(st, Environment(gravity=Vec3(0, 0, 0)), cfg,
+                         n // 40)
         xs.append(st.get_mass(b).pos.x - 1.0)
     t = np.arange(1, 41) * (n // 40) * dt
     w0 = math.sqrt(k / m)
