@@ -38,19 +38,30 @@ PAPER_RATE = 3.0e8  # PAPER.md:10,20 headline (Titan X); north_star x50 base
 
 
 def parse():
+    args = _parser().parse_args()
+    if args.n is None:
+        args.n = 200 if args.config == "E" else 100
+    return args
+
+
+def _parser():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="B", choices=["A", "B", "D"],
+    ap.add_argument("--config", default="B",
+                    choices=["A", "B", "D", "E"],
                     help="B: one 100^3 lattice per rank (batched instances);"
                          " D: --robots actuated 5^3 robots sharded over "
                          "the ranks (RL batch); A: the reference's bouncing "
-                         "10^3 cube (scenarios/bouncing_cube.ini) per rank")
-    ap.add_argument("--n", "--edge", dest="n", type=int, default=100,
+                         "10^3 cube (scenarios/bouncing_cube.ini) per rank;"
+                         " E: ONE --edge^3 lattice (default 200) split by "
+                         "mass range (x-slabs) over the ranks, in-library "
+                         "halo over mapped peer memory")
+    ap.add_argument("--n", "--edge", dest="n", type=int, default=None,
                     help="lattice edge (--edge under torchrun, whose parser "
-                         "reads --n as ambiguous)")
+                         "reads --n as ambiguous); 100, or 200 for E")
     ap.add_argument("--robots", type=int, default=4096)
     ap.add_argument("--precision", default="fp32",
                     choices=["fp32", "mixed", "fp64"])
@@ -60,7 +71,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp64", action="store_true",
                     help="skip the fp64 parity-mode sub-measurement")
-    return ap.parse_args()
+    return ap
 
 
 # --------------------------------------------------------------- workload
@@ -123,6 +134,11 @@ def describe(args, world: int):
     if args.config == "A":
         return (f"A: 10^3 bouncing cube (scenarios/bouncing_cube.ini) per "
                 f"rank, {args.precision}, {args.accumulation}", "weak", 0)
+    if args.config == "E":
+        return (f"E: one {args.n}^3 lattice (x1.01 stretch, gravity, "
+                f"friction ground plane) split into {world} x-slab(s), "
+                f"in-library halo, {args.precision}, {args.accumulation}",
+                "strong", 0)
     return (f"B: {args.n}^3 lattice on friction ground plane, gravity, "
             f"x1.01 stretch, {args.precision}, {args.accumulation}",
             "weak", 0)
@@ -372,6 +388,9 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    if args.config == "E":
+        return bench_config_e(args, rank, world, local, dist, reduce_)
+
     from paper_1911_10274_b200 import StepConfig, engine
     from paper_1911_10274_b200.control import SimController
 
@@ -547,6 +566,109 @@ def main():
                 "call_ms_per_step": call_ms / args.steps,
                 "fp64_parity_mode": fp64,
                 "vs_baseline_ref": "PAPER.md:10 3.0e8 spring updates/s"}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def bench_config_e(args, rank, world, local, dist, reduce_):
+    """Config E: one lattice partitioned by mass
+    range over the ranks; each rank steps its x-slab (owned masses +
+    ghosts), the halo rides on the step kernels (distributed.HaloRun).
+    value = all springs x K / max over ranks of the step-kernel time."""
+    import torch
+    from paper_1911_10274_b200 import _native
+    from paper_1911_10274_b200.distributed import HaloRun
+    from paper_1911_10274_b200.partition import (even_cuts, halo_plans,
+                                                 partition_case)
+    metric, unit = "spring updates/sec", "spring_updates/s"
+    n = args.n
+    st, env = build_workload(n)
+    case = store_case(st, env)
+    case.update(gc_kind=np.zeros(0, np.int8), gc_vec=np.zeros((0, 3)))
+    springs = st.spring_count
+    cuts = even_cuts(st.mass_count, world, align=n * n)
+    shards = partition_case(case, cuts, ranks=[rank])
+    plans = halo_plans(shards)
+    run = HaloRun(shards[rank], plans, local, args.precision)
+    if world > 1:
+        run.connect_ipc()
+    acc = _native.ACC_GATHER if args.accumulation == "gather" else \
+        _native.ACC_ATOMIC
+    dt = 1e-4
+    warm = max(3, args.warmup)
+    times = np.arange(warm + args.steps, dtype=np.float64) * dt
+    run.step(times[:warm], dt, acc)
+    if dist is not None:
+        dist.barrier()
+    run.ctx.sync()
+    clocks = ClockSampler(local)
+    run.ctx.timer_start()
+    done, err = run.step(times[warm:], dt, acc)
+    call_ms = run.ctx.timer_stop()
+    ms = run.ctx.last_step_ms()
+    clk = clocks.stop()
+    if err:
+        raise SystemExit(f"numerical abort at step {done}")
+    sec = ms / 1e3
+    if dist is not None:
+        sec = float(reduce_(sec, dist.ReduceOp.MAX, torch.float64))
+    value = springs * args.steps / sec
+    local_springs = len(shards[rank].spring_slots)
+    algo = algorithmic_bytes(springs, st.mass_count, args.precision)
+    peak, peak_kind = peak_hbm()
+    stats = run.ctx.stats()
+    # e2e through the same API with host buffers: this rank's state up,
+    # K steps, its owned state down
+    m_loc = len(shards[rank].local_to_global)
+    c = shards[rank].case
+    w0 = time.perf_counter()
+    run.ctx.upload_masses(c["m_pos"], c["m_vel"], c["m_acc"], c["m_fext"],
+                          c["m_load"], c["m_mass"], c["m_fixed"],
+                          c["m_alive"], c["m_gen"])
+    if world > 1:
+        dist.barrier()
+    run.step(times[warm:], dt, acc)
+    pos = np.empty((m_loc, 3))
+    vel = np.empty((m_loc, 3))
+    run.ctx.download_masses(pos, vel)
+    wall = time.perf_counter() - w0
+    if dist is not None:
+        wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
+    run.close()
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": unit,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * sec / args.steps,
+                "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": value / PAPER_RATE,
+                "dtype": "f32" if args.precision == "fp32" else "f64",
+                "data": "synthetic",
+                "config": {"workload": describe(args, world)[0],
+                           "masses": st.mass_count, "springs": springs,
+                           "rank0_springs_incl_cross": local_springs,
+                           "precision": args.precision,
+                           "accumulation": args.accumulation,
+                           "parallelism": f"x-slab partition x{world}",
+                           "l2": "working set > L2 every step"},
+                "roofline": {"bound": "hbm", "achieved":
+                             algo / world / (sec / args.steps) / 1e9,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": algo / world / (sec / args.steps) / 1e9
+                             / peak, "traffic": None, "peak_kind": peak_kind,
+                             "algorithmic_bytes_per_step_per_gpu":
+                                 algo / world,
+                             "kernel": _native.STEP_PATHS.get(
+                                 stats["step_path"], "?") +
+                             (" + k_halo_sync" if world > 1 else "")},
+                "e2e": {"value": springs * args.steps / wall, "unit": unit,
+                        "h2d_bytes_per_step": m_loc * 138 / args.steps,
+                        "d2h_bytes_per_step": m_loc * 48 / args.steps,
+                        "api": "sl_upload_masses + sl_step + "
+                               "sl_download_masses per rank"},
+                "gpu_launches": args.steps * (2 if world > 1 else 1),
+                "call_ms_per_step": call_ms / args.steps,
+                "clocks": clk, "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

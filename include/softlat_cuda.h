@@ -43,7 +43,7 @@ extern "C" {
 
 /* arithmetic of the state and of the spring force (hard part 3) */
 #define SL_PREC_FP64 0  /* double everywhere; parity mode (bit-exact gather) */
-#define SL_PREC_FP32 1  /* float state + float spring math                  */
+#define SL_PREC_FP32 1  /* float spring math; compensated float positions   */
 #define SL_PREC_MIXED 2 /* double mass state, float spring parameters/math  */
 
 /* force accumulation (StepConfig.accumulation, engine.py:40,49):
@@ -266,6 +266,29 @@ int sl_state_pointers(sl_ctx *ctx, void **pos_read, int64_t *rows,
  * is (x, y, z, lx) in this mode, a position is record + low part and the
  * masses live apart.  NULL in fp64 / mixed. */
 int sl_state_lo(sl_ctx *ctx, void **lo_read);
+/* In-library halo of a mass-range partition (config E; replaces the
+ * per-step Python exchange of partition.py).  Each rank's context holds its
+ * owned masses then its ghosts (fixed + sl_mark_ghosts).  dst[2 * i + q]
+ * (q = 0, 1) names where owned mass i's position goes after every step:
+ * (row << 3) | peer, row = the ghost's local index at that peer, or -1.
+ * The step kernels store those rows straight into the peers' position
+ * buffers (mapped with sl_halo_ipc_open across processes, or the pointers
+ * of sl_halo_local within one process), and after every step a one-block
+ * kernel publishes a per-peer step counter and waits for the peers' --
+ * no host round trip, no collective.  Setup: sl_halo_init, then per peer
+ * sl_halo_set_peer(peer, its 5 pointers, the counter slot it reserved for
+ * this rank), then sl_halo_commit.  All ranks must step in lockstep (same
+ * step counts per call) from the same buffer parity; damping is
+ * unsupported (ghost velocities are not exchanged).
+ * The 5 pointers: position records [2], fp32 low parts [2] (NULL in fp64 /
+ * mixed), the counter words [8]. */
+#define SL_IPC_HANDLE_BYTES 64
+int sl_halo_init(sl_ctx *ctx, int n_peers, const int32_t *dst);
+int sl_halo_local(sl_ctx *ctx, void **ptrs5);
+int sl_halo_ipc_handles(sl_ctx *ctx, void *out5x64);
+int sl_halo_ipc_open(sl_ctx *ctx, const void *handles5x64, void **ptrs5);
+int sl_halo_set_peer(sl_ctx *ctx, int peer, void *const *ptrs5, int slot);
+int sl_halo_commit(sl_ctx *ctx);
 /* The context's CUDA stream (cudaStream_t) for ordering foreign work. */
 int sl_get_stream(sl_ctx *ctx, void **stream);
 

@@ -38,7 +38,9 @@ EXPORTS = (
     "sl_state_lo", "sl_get_stream", "sl_energy", "sl_spring_loads", "sl_host_alloc",
     "sl_host_free", "sl_format_snapshot", "sl_lattice_counts",
     "sl_build_lattice", "sl_host_fill", "sl_host_copy",
-    "sl_host_masked_extrema", "sl_set_spring_damping")
+    "sl_host_masked_extrema", "sl_set_spring_damping", "sl_halo_init",
+    "sl_halo_local", "sl_halo_ipc_handles", "sl_halo_ipc_open",
+    "sl_halo_set_peer", "sl_halo_commit")
 
 
 class SlStats(C.Structure):
@@ -101,6 +103,12 @@ def load_library(path: str = LIB_PATH):
             "sl_timer_stop": ([P, P], I),
             "sl_last_step_ms": ([P, P], I),
             "sl_set_spring_damping": ([P, I64, P], I),
+            "sl_halo_init": ([P, I, P], I),
+            "sl_halo_local": ([P, P], I),
+            "sl_halo_ipc_handles": ([P, P], I),
+            "sl_halo_ipc_open": ([P, P, P], I),
+            "sl_halo_set_peer": ([P, I, P, I], I),
+            "sl_halo_commit": ([P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -509,6 +517,39 @@ class Context:
         self._check(self.lib.sl_timer_stop(self.h, C.byref(ms)),
                     "sl_timer_stop")
         return float(ms.value)
+
+    # ---------------------------------------------- in-library halo
+    def halo_init(self, n_peers: int, dst: np.ndarray):
+        """dst: int32 [m_n, 2], (row << 3) | peer or -1 (sl_halo_init)."""
+        d = np.ascontiguousarray(dst, np.int32).reshape(-1)
+        self._check(self.lib.sl_halo_init(self.h, int(n_peers), _ptr(d)),
+                    "sl_halo_init")
+
+    def halo_local(self) -> list[int]:
+        p = (C.c_void_p * 5)()
+        self._check(self.lib.sl_halo_local(self.h, p), "sl_halo_local")
+        return [int(x or 0) for x in p]
+
+    def halo_ipc_handles(self) -> bytes:
+        buf = C.create_string_buffer(5 * 64)
+        self._check(self.lib.sl_halo_ipc_handles(self.h, buf),
+                    "sl_halo_ipc_handles")
+        return buf.raw
+
+    def halo_ipc_open(self, handles: bytes) -> list[int]:
+        buf = C.create_string_buffer(bytes(handles), 5 * 64)
+        p = (C.c_void_p * 5)()
+        self._check(self.lib.sl_halo_ipc_open(self.h, buf, p),
+                    "sl_halo_ipc_open")
+        return [int(x or 0) for x in p]
+
+    def halo_set_peer(self, peer: int, ptrs, slot: int):
+        p = (C.c_void_p * 5)(*[x or None for x in ptrs])
+        self._check(self.lib.sl_halo_set_peer(self.h, int(peer), p,
+                                              int(slot)), "sl_halo_set_peer")
+
+    def halo_commit(self):
+        self._check(self.lib.sl_halo_commit(self.h), "sl_halo_commit")
 
     def set_spring_damping(self, damping):
         """Per-spring damping c for slots [0, s_n) (zeros clear it)."""

@@ -139,6 +139,13 @@ struct sl_ctx {
   // partitioned runs
   DevBuf ghost;
   bool has_ghost = false;
+  // in-library halo (sl_halo_*): device descriptor, per-mass send table,
+  // the peers' counter words of this context, opened IPC mappings
+  HaloDesc halo_host{};
+  DevBuf halo_desc, halo_dst, halo_flags;
+  bool halo_on = false;
+  unsigned long long halo_step = 0;  // steps published so far
+  std::vector<void *> halo_ipc;
   bool async_open = false;
   int64_t async_steps = 0;
   int async_cur0 = 0;
@@ -761,6 +768,7 @@ KState make_state(sl_ctx *c) {
   S.xflags = c->xflags.as<uint8_t>();
   S.fsz8 = c->fsz == 8;
   S.ghost = c->has_ghost ? c->ghost.as<uint8_t>() : nullptr;
+  S.halo = c->halo_on ? c->halo_desc.as<HaloDesc>() : nullptr;
   S.self = c->kdev.as<KState>();
   S.split = c->layout_valid && c->split;
   if (c->split) {
@@ -1731,6 +1739,10 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_gid, &c->diag, &c->fz_perm, &c->fz_cnt,
                     &c->fz_epos, &c->fz_cnt_a,
                     &c->win_fail};
+  for (void *p : c->halo_ipc) cudaIpcCloseMemHandle(p);
+  c->halo_desc.release();
+  c->halo_dst.release();
+  c->halo_flags.release();
   for (DevBuf *b : bufs) b->release();
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->snap_host) cudaFreeHost(c->snap_host);
@@ -2223,6 +2235,36 @@ int sl_set_custom_factors(sl_ctx *c, int64_t n, const int64_t *slots,
   return SL_OK;
 }
 
+// Halo step boundary: publish "my step k's ghost stores are done" to every
+// peer (system-scope fence + release store of k into the peer's counter
+// word for me), then wait until every peer has published k.  One block;
+// thread t serves peer t.  Never triggers dependents early: the next step
+// kernel starts after the wait.
+__global__ void k_halo_sync(const HaloDesc *H, unsigned long long k) {
+  const int t = threadIdx.x;
+  if (t < H->n_peers) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(H->flag_out[t]),
+                 "l"(k)
+                 : "memory");
+    unsigned long long v = 0;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                   : "=l"(v)
+                   : "l"(H->flag_in + t)
+                   : "memory");
+      if (v < k) __nanosleep(100);
+    } while (v < k);
+  }
+  __syncthreads();
+}
+
+static void halo_sync(sl_ctx *c) {
+  c->halo_step++;
+  k_halo_sync<<<1, 32, 0, c->st>>>(c->halo_desc.as<HaloDesc>(), c->halo_step);
+  c->launches++;
+}
+
 int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
             int accumulation, int64_t *counters, int64_t *err_slot,
             int64_t *steps_done) {
@@ -2303,6 +2345,7 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
       L.mass(S, c->env, T, c->st);
       c->launches += 2;
     }
+    if (c->halo_on) halo_sync(c);
   }
   CKL();
   CK(cudaEventRecord(c->k1, c->st));
@@ -2584,6 +2627,7 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
       L.mass(S, c->env, T, c->st);
       c->launches += 2;
     }
+    if (c->halo_on) halo_sync(c);
   }
   CKL();
   return SL_OK;
@@ -2668,6 +2712,108 @@ int sl_mark_ghosts(sl_ctx *c, int64_t n, const int64_t *slots) {
   }
   CK(cudaStreamSynchronize(c->st));
   c->has_ghost = n > 0;
+  return SL_OK;
+}
+
+// ------------------------------------------------ in-library halo (config E)
+int sl_halo_init(sl_ctx *c, int n_peers, const int32_t *dst) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (n_peers < 0 || n_peers > HALO_MAXP || (c->m_n > 0 && !dst))
+    return fail(c, SL_EINVAL, "sl_halo_init: 0..%d peers", HALO_MAXP);
+  for (int64_t r = 0; r < 2 * c->m_n; r++)
+    if (dst[r] >= 0 && (dst[r] & 7) >= n_peers)
+      return fail(c, SL_EINVAL, "halo destination %lld: peer out of range",
+                  (long long)r);
+  CK(cudaSetDevice(c->device));
+  CK(c->halo_flags.ensure(8 * HALO_MAXP));
+  CK(cudaMemset(c->halo_flags.p, 0, 8 * HALO_MAXP));
+  CK(c->halo_dst.ensure(8 * std::max<int64_t>(c->m_n, 1)));
+  if (c->m_n > 0)
+    CK(cudaMemcpy(c->halo_dst.p, dst, 8 * c->m_n, cudaMemcpyHostToDevice));
+  CK(c->halo_desc.ensure(sizeof(HaloDesc)));
+  memset(&c->halo_host, 0, sizeof c->halo_host);
+  c->halo_host.n_peers = n_peers;
+  c->halo_host.flag_in = c->halo_flags.as<unsigned long long>();
+  c->halo_host.dst = c->halo_dst.as<int2>();
+  c->halo_on = false;
+  c->halo_step = 0;
+  return SL_OK;
+}
+
+int sl_halo_local(sl_ctx *c, void **ptrs) {
+  if (!c || !c->masses_set || !c->halo_flags.p)
+    return fail(c, SL_ESTATE, "sl_halo_init first");
+  ptrs[0] = c->pos[0].p;
+  ptrs[1] = c->pos[1].p;
+  ptrs[2] = c->prec == PREC_FP32 ? c->plo[0].p : nullptr;
+  ptrs[3] = c->prec == PREC_FP32 ? c->plo[1].p : nullptr;
+  ptrs[4] = c->halo_flags.p;
+  return SL_OK;
+}
+
+int sl_halo_ipc_handles(sl_ctx *c, void *out) {
+  void *p[5];
+  int rc = sl_halo_local(c, p);
+  if (rc) return rc;
+  CK(cudaSetDevice(c->device));
+  unsigned char *o = (unsigned char *)out;
+  memset(o, 0, 5 * SL_IPC_HANDLE_BYTES);
+  for (int q = 0; q < 5; q++) {
+    if (!p[q]) continue;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, p[q]));
+    memcpy(o + q * SL_IPC_HANDLE_BYTES, &h, sizeof h);
+  }
+  return SL_OK;
+}
+
+int sl_halo_ipc_open(sl_ctx *c, const void *handles, void **ptrs) {
+  if (!c || !handles || !ptrs) return fail(c, SL_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  const unsigned char *in = (const unsigned char *)handles;
+  static const unsigned char zero[SL_IPC_HANDLE_BYTES] = {0};
+  for (int q = 0; q < 5; q++) {
+    ptrs[q] = nullptr;
+    if (!memcmp(in + q * SL_IPC_HANDLE_BYTES, zero, SL_IPC_HANDLE_BYTES))
+      continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, in + q * SL_IPC_HANDLE_BYTES, sizeof h);
+    CK(cudaIpcOpenMemHandle(&ptrs[q], h, cudaIpcMemLazyEnablePeerAccess));
+    c->halo_ipc.push_back(ptrs[q]);
+  }
+  return SL_OK;
+}
+
+int sl_halo_set_peer(sl_ctx *c, int peer, void *const *ptrs, int slot) {
+  if (!c || !ptrs || peer < 0 || peer >= c->halo_host.n_peers || slot < 0 ||
+      slot >= HALO_MAXP)
+    return fail(c, SL_EINVAL, "sl_halo_set_peer: bad arguments");
+  if (!ptrs[0] || !ptrs[1] || !ptrs[4] ||
+      (c->prec == PREC_FP32 && (!ptrs[2] || !ptrs[3])))
+    return fail(c, SL_EINVAL, "sl_halo_set_peer: missing peer buffers");
+  HaloDesc &h = c->halo_host;
+  h.pos[peer][0] = ptrs[0];
+  h.pos[peer][1] = ptrs[1];
+  h.lo[peer][0] = ptrs[2];
+  h.lo[peer][1] = ptrs[3];
+  h.flag_out[peer] = (unsigned long long *)ptrs[4] + slot;
+  return SL_OK;
+}
+
+int sl_halo_commit(sl_ctx *c) {
+  if (!c || !c->halo_desc.p) return fail(c, SL_ESTATE, "sl_halo_init first");
+  const HaloDesc &h = c->halo_host;
+  for (int q = 0; q < h.n_peers; q++)
+    if (!h.pos[q][0] || !h.flag_out[q])
+      return fail(c, SL_ESTATE, "halo peer %d not set", q);
+  if (c->has_damping)
+    return fail(c, SL_EUNSUPPORTED,
+                "damped springs read ghost velocities, which the halo does "
+                "not carry");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpy(c->halo_desc.p, &h, sizeof h, cudaMemcpyHostToDevice));
+  c->halo_on = h.n_peers > 0;
+  c->halo_step = 0;
   return SL_OK;
 }
 

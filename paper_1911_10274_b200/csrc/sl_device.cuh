@@ -68,6 +68,25 @@ struct EnvP {
   int gck[MAXG];
 };
 
+// Halo of a mass-range partition (config E): the owning
+// rank's step kernel, as it stores an owned boundary mass's new position,
+// also stores it straight into the ghost row of every peer that needs it --
+// the peers' position buffers are mapped into this process (CUDA IPC over
+// NVLink, or plain pointers between contexts of one process), so the
+// exchange rides on the mass update itself, tile by tile.  After each step
+// a one-block kernel (k_halo_sync, sl_api.cu) publishes a per-peer step
+// counter with a system-scope release and waits for the peers' counters:
+// the next step reads complete ghost rows.
+constexpr int HALO_MAXP = 8;
+struct HaloDesc {
+  int n_peers;
+  void *pos[HALO_MAXP][2];  // peer's position record buffers (mapped)
+  void *lo[HALO_MAXP][2];   // peer's fp32 low parts (mapped) or null
+  unsigned long long *flag_out[HALO_MAXP];  // our counter word at the peer
+  unsigned long long *flag_in;  // [HALO_MAXP] the peers' counters (local)
+  const int2 *dst;  // per local mass: up to two (row << 3 | peer), -1 none
+};
+
 // All device pointers of one context (type-erased; kernels cast).
 struct KState {
   int64_t m_n, s_n;
@@ -107,6 +126,7 @@ struct KState {
   // ghost masses of a partitioned run (partition.py): spring side effects
   // are counted only where the m1 endpoint is owned; null when no ghosts
   const uint8_t *ghost;
+  const HaloDesc *halo;  // partitioned run with the in-library halo
   // split layout (tolerance modes, sl_split.cuh); split == 0 => exact layout
   const KState *self;  // device-memory copy of this struct (rare paths)
   int split;
@@ -507,6 +527,21 @@ __device__ __forceinline__ void integrate(
                     nv, ax, ay, az);
   if constexpr (P == PREC_FP32)
     ((float2 *)S.plo[T.cur ^ 1])[i] = make_float2(nlo.y, nlo.z);
+  if (S.halo) {  // owned boundary mass: its ghost rows at the peers
+    const int2 d = __ldg(&S.halo->dst[i]);
+    const int dd[2] = {d.x, d.y};
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+      if (dd[q] < 0) continue;
+      const int p = dd[q] & 7;
+      const int64_t row = dd[q] >> 3;
+      ((R4 *)S.halo->pos[p][T.cur ^ 1])[row] = np4;
+      if constexpr (P == PREC_FP32)
+        ((float2 *)S.halo->lo[p][T.cur ^ 1])[row] =
+            make_float2(nlo.y, nlo.z);
+    }
+    if (d.x >= 0) __threadfence_system();
+  }
   const R px = np4.x, py = np4.y, pz = np4.z, vx = nv.x, vy = nv.y,
           vz = nv.z;
   ((R4 *)S.pos[T.cur ^ 1])[i] = np4;

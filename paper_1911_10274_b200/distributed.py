@@ -128,6 +128,80 @@ class PartitionedRun:
         self.ctx.close()
 
 
+class HaloRun:
+    """One shard of a mass-range partition with the IN-LIBRARY halo
+    (sl_halo_*): the owner's step kernel stores boundary positions straight
+    into the peers' ghost rows over mapped peer memory, a one-block kernel
+    per step publishes / awaits per-peer step counters.  A whole
+    ``step(times)`` call is one library call: no Python, no torch, no
+    collective on the step path.  ``connect_local`` wires shards that live
+    in one process; ``connect_ipc`` wires one shard per process (CUDA IPC,
+    the handles travel once over torch.distributed)."""
+
+    def __init__(self, shard: Shard, plans: list, device: int = 0,
+                 precision: str = "fp64"):
+        from .partition import halo_dst_table
+        self.shard = shard
+        self.rank = shard.rank
+        self.ctx = context_for_case(shard.case, device, precision)
+        if len(shard.ghost_local):
+            self.ctx.mark_ghosts(shard.ghost_local)
+        dst, self.peers, self.slots = halo_dst_table(
+            plans, shard.rank, len(shard.local_to_global))
+        self.counters = np.zeros(3, np.int64)
+        # build the device layout now (a zero-step call): nothing may
+        # allocate (cudaMalloc can synchronise the device) once the
+        # shards' step counters wait on one another
+        self.ctx.step(np.zeros(0), 1e-4, _native.ACC_GATHER, self.counters)
+        self.ctx.halo_init(len(self.peers), dst)
+
+    @staticmethod
+    def connect_local(runs: list["HaloRun"]):
+        by_rank = {r.rank: r for r in runs}
+        local = {r.rank: r.ctx.halo_local() for r in runs}
+        for r in runs:
+            for p, q in enumerate(r.peers):
+                r.ctx.halo_set_peer(p, local[q], r.slots[p])
+            r.ctx.halo_commit()
+        return by_rank
+
+    def connect_ipc(self, group=None):
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        mine = self.ctx.halo_ipc_handles()
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        for p, q in enumerate(self.peers):
+            self.ctx.halo_set_peer(p, self.ctx.halo_ipc_open(allh[q]),
+                                   self.slots[p])
+        self.ctx.halo_commit()
+        dist.barrier(group=group)
+
+    def step(self, times: np.ndarray, dt: float,
+             accumulation: int = _native.ACC_GATHER):
+        return self.ctx.step(np.asarray(times, np.float64), dt, accumulation,
+                             self.counters)
+
+    def step_async(self, times: np.ndarray, dt: float,
+                   accumulation: int = _native.ACC_GATHER):
+        self.ctx.step_async(np.asarray(times, np.float64), dt, accumulation)
+
+    def finish(self):
+        return self.ctx.step_finish(self.counters)
+
+    def owned_state(self):
+        m = self.shard.n_owned
+        n = len(self.shard.local_to_global)
+        pos, vel = np.zeros((n, 3)), np.zeros((n, 3))
+        self.ctx.download_masses(pos, vel)
+        alive = np.zeros(len(self.shard.spring_slots), np.uint8)
+        self.ctx.download_springs(alive)
+        return pos[:m], vel[:m], alive
+
+    def close(self):
+        self.ctx.close()
+
+
 def nccl_halo(plan: HaloPlan, pos, group=None):
     """Halo exchange over torch.distributed (NCCL between GPUs)."""
     return exchange(plan, pos, group=group)
@@ -136,24 +210,23 @@ def nccl_halo(plan: HaloPlan, pos, group=None):
 def run_partitioned(case: dict, cuts: list[int], steps: int, dt: float,
                     precision: str = "fp64", device: int | None = None):
     """Multi-process driver (one rank per GPU, torchrun): this rank's shard
-    of ``case`` stepped ``steps`` times with NCCL halo exchange.  Returns
-    (shard, owned positions, owned velocities, spring alive flags,
-    counters, device seconds)."""
+    of ``case`` stepped ``steps`` times with the in-library halo (CUDA IPC
+    peer mappings; torch.distributed only carries the handles once).
+    Returns (shard, owned positions, owned velocities, spring alive flags,
+    counters, device seconds of the step kernels)."""
     import torch
     import torch.distributed as dist
     from .partition import halo_plans, partition_case
     rank = dist.get_rank()
     shards = partition_case(case, cuts)
-    plan = halo_plans(shards)[rank]
+    plans = halo_plans(shards)
     dev = torch.cuda.current_device() if device is None else device
-    run = PartitionedRun(shards[rank], plan, dev, precision)
+    run = HaloRun(shards[rank], plans, dev, precision)
+    run.connect_ipc()
     times = np.arange(steps, dtype=np.float64) * dt
     dist.barrier()
-    torch.cuda.synchronize()
-    run.ctx.timer_start()
-    for t in times:
-        run.step_async(float(t), dt, nccl_halo)
-    done, err = run.finish()
-    ms = run.ctx.timer_stop()
+    run.ctx.sync()
+    done, err = run.step(times, dt)
+    sec = run.ctx.last_step_ms() / 1e3
     pos, vel, alive = run.owned_state()
-    return shards[rank], pos, vel, alive, run.counters.copy(), ms / 1e3
+    return shards[rank], pos, vel, alive, run.counters.copy(), sec

@@ -77,8 +77,12 @@ class HaloPlan:
         return sorted(set(self.send) | set(self.recv))
 
 
-def partition_case(case: dict, cuts: list[int]) -> list[Shard]:
-    """Split a case dict (store arrays, golden/ABI layout) by mass ranges."""
+def partition_case(case: dict, cuts: list[int],
+                   ranks: list[int] | None = None) -> list[Shard]:
+    """Split a case dict (store arrays, golden/ABI layout) by mass ranges.
+    With ``ranks``, only those shards carry their sub-case (``case``); the
+    others are index bookkeeping only (enough for ``halo_plans``) -- one
+    rank of a big partitioned run builds just its own arrays."""
     m_n = len(case["m_mass"])
     s1 = np.asarray(case["s_m1"], np.int64)
     s2 = np.asarray(case["s_m2"], np.int64)
@@ -93,6 +97,12 @@ def partition_case(case: dict, cuts: list[int]) -> list[Shard]:
         ends = np.concatenate([s1[sel], s2[sel]])
         ghosts = np.unique(ends[(ends < lo) | (ends >= hi)])
         l2g = np.concatenate([np.arange(lo, hi, dtype=np.int64), ghosts])
+        if ranks is not None and r not in ranks:
+            shards.append(Shard(rank=r, lo=lo, hi=hi, local_to_global=l2g,
+                                spring_slots=sel, n_owned=hi - lo,
+                                ghost_local=np.arange(hi - lo, len(l2g)),
+                                ghost_owner=owner[ghosts], case=None))
+            continue
         g2l = np.full(m_n, -1, np.int64)
         g2l[l2g] = np.arange(len(l2g))
         sub = {}
@@ -184,3 +194,35 @@ def gather_owned(shards: list[Shard], key: str, parts: list[np.ndarray],
     for s, p in zip(shards, parts):
         out[s.lo:s.hi] = p[:s.n_owned]
     return out
+
+
+def halo_dst_table(plans: list[HaloPlan], rank: int, n_local: int):
+    """The in-library halo's send table of ``rank`` (sl_halo_init): int32
+    [n_local, 2], entry (row << 3) | peer for each peer that holds this
+    mass as a ghost -- peer = index in ``plans[rank].peers``, row = the
+    ghost's local index there (``plans[q].recv[rank]`` lists them in the
+    order of ``plans[rank].send[q]``) -- and -1 elsewhere.  Returns (table,
+    peers, slots): slots[p] = this rank's counter slot at peer p (its
+    index in that peer's peer list)."""
+    plan = plans[rank]
+    peers = plan.peers
+    if len(peers) > 8:
+        raise ValueError("at most 8 halo peers per rank")
+    dst = np.full((n_local, 2), -1, np.int32)
+    for p, q in enumerate(peers):
+        if q not in plan.send:
+            continue
+        src = np.asarray(plan.send[q], np.int64)
+        rows = np.asarray(plans[q].recv[rank], np.int64)
+        if len(src) != len(rows):
+            raise ValueError("halo plans disagree")
+        if len(rows) and rows.max() >= (1 << 28):
+            raise ValueError("ghost row index too large for the halo table")
+        code = (rows << 3 | p).astype(np.int32)
+        free = (dst[src, 0] < 0).astype(np.int64)  # first free column
+        col = np.where(free == 1, 0, 1)
+        if np.any(dst[src[col == 1], 1] >= 0):
+            raise ValueError("a mass is a ghost of more than two peers")
+        dst[src, col] = code
+    slots = [plans[q].peers.index(rank) for q in peers]
+    return dst, peers, slots
