@@ -152,3 +152,34 @@ def test_two_rank_gloo_halo_equals_single_run():
         assert p.exitcode == 0
     assert got[:, :3].tobytes() == np.ascontiguousarray(want_p).tobytes()
     assert got[:, 3:].tobytes() == np.ascontiguousarray(want_v).tobytes()
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 5])
+def test_halo_dst_table_reproduces_exchange(ranks):
+    """The in-library halo's per-mass send table (partition.halo_dst_table,
+    consumed by the step kernels through sl_halo_init) moves exactly the
+    rows the HaloPlan exchange moves: every ghost row of every rank gets
+    its owner's position, nothing else is written."""
+    from paper_1911_10274_b200.partition import halo_dst_table
+    case = lattice_case(8, 5, 4)
+    m = len(case["m_mass"])
+    cuts = even_cuts(m, ranks)
+    shards = partition_case(case, cuts)
+    plans = halo_plans(shards)
+    rng = np.random.default_rng(ranks)
+    truth = rng.normal(size=(m, 3))
+    local = [np.full((len(s.local_to_global), 3), np.nan) for s in shards]
+    for s, loc in zip(shards, local):
+        loc[:s.n_owned] = truth[s.local_to_global[:s.n_owned]]
+    for s in shards:
+        dst, peers, slots = halo_dst_table(plans, s.rank,
+                                           len(s.local_to_global))
+        assert (dst[s.n_owned:] == -1).all()  # ghosts never send
+        for i, j in zip(*np.nonzero(dst >= 0)):
+            code = int(dst[i, j])
+            q = peers[code & 7]
+            local[q][code >> 3] = local[s.rank][i]
+        for p, q in enumerate(peers):  # counter slots are mutual
+            assert plans[q].peers[slots[p]] == s.rank
+    for s, loc in zip(shards, local):
+        assert np.array_equal(loc, truth[s.local_to_global])
