@@ -133,6 +133,7 @@ struct sl_ctx {
       fz_epos, fz_cnt_a;
   DevBuf diag;  // diagnostics scratch (sl_energy / sl_spring_loads)
   bool auto_atomic = false;  // SL_ACC_AUTO resolved to the atomic variant
+  bool atomic_owner = false;  // atomic accumulation: owner-aggregated kernel
   // grouped sine actuation of the split layout's fast path (ActP)
   ActP agrp;
   DevBuf s_grp, sp_actc, sp_acto;
@@ -1558,8 +1559,14 @@ int build_split_layout(sl_ctx *c, bool *used) {
 // measured so far picks the gather.
 constexpr int64_t AUTO_HUB_ENTRIES = 128;  // entries per mass (lattice: 26)
 int resolve_accumulation(sl_ctx *c, int acc) {
-  if (acc != SL_ACC_AUTO) return acc;
   const int64_t widest = c->split ? c->sp_wa + c->sp_wb : c->max_width;
+  // atomic accumulation: the owner-aggregated kernel (one thread per mass,
+  // its m1 springs) on regular meshes; on hub meshes one thread per spring
+  // with warp-aggregated reductions (the hub's thread would serialise)
+  c->atomic_owner = widest <= AUTO_HUB_ENTRIES && c->layout_valid;
+  if (const char *ev = getenv("SL_ATOMIC_KERNEL"))  // tuning / sweeps
+    c->atomic_owner = c->layout_valid && strcmp(ev, "spring") != 0;
+  if (acc != SL_ACC_AUTO) return acc;
   c->auto_atomic = widest > AUTO_HUB_ENTRIES;
   return c->auto_atomic ? SL_ACC_ATOMIC : SL_ACC_GATHER;
 }
@@ -2281,7 +2288,7 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
   if (c->async_open)
     return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
   CK(cudaSetDevice(c->device));
-  int rc = prepare(c, accumulation != SL_ACC_ATOMIC);
+  int rc = prepare(c, true);  // gather and owner-atomic use the layout
   if (rc) return rc;
   accumulation = resolve_accumulation(c, accumulation);
   const Launch &L = launchers(c->prec);
@@ -2341,7 +2348,10 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
       }
       c->launches++;
     } else {
-      L.spring_atomic(S, T, c->has_special, c->st);
+      if (c->atomic_owner)
+        L.owner_atomic(S, T, c->agrp, c->st);
+      else
+        L.spring_atomic(S, T, c->has_special, c->st);
       L.mass(S, c->env, T, c->st);
       c->launches += 2;
     }
@@ -2623,7 +2633,10 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
       }
       c->launches++;
     } else {
-      L.spring_atomic(S, T, c->has_special, c->st);
+      if (c->atomic_owner)
+        L.owner_atomic(S, T, c->agrp, c->st);
+      else
+        L.spring_atomic(S, T, c->has_special, c->st);
       L.mass(S, c->env, T, c->st);
       c->launches += 2;
     }
@@ -2644,7 +2657,7 @@ int sl_step_async(sl_ctx *c, int64_t n_steps, const double *sim_times,
       accumulation != SL_ACC_AUTO)
     return fail(c, SL_EINVAL, "unknown accumulation %d", accumulation);
   CK(cudaSetDevice(c->device));
-  int rc = prepare(c, accumulation != SL_ACC_ATOMIC, !c->async_open);
+  int rc = prepare(c, true, !c->async_open);
   if (rc) return rc;
   accumulation = resolve_accumulation(c, accumulation);
   if (!c->async_open) {

@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 #include <math_constants.h>
 
 namespace sl {
@@ -353,6 +355,29 @@ __device__ __forceinline__ void red_add(double4 *p, double x, double y,
   atomicAdd(&p->x, x);
   atomicAdd(&p->y, y);
   atomicAdd(&p->z, z);
+}
+
+// Warp-aggregated reduction into f_ext[target]: the converged lanes of the
+// warp are partitioned by target mass (match-any); each partition sums its
+// contributions with shuffles and its first lane issues ONE vector RED.
+// Hub meshes (a star's spokes: consecutive slots, one shared endpoint) turn
+// 32 same-address atomics into one; without duplicates (lattices in slot
+// order: consecutive springs have distinct endpoints) the warp takes the
+// plain RED after a single vote.
+template <class R4, class R>
+__device__ __forceinline__ void red_add_agg(R4 *fe, uint32_t target, R x,
+                                            R y, R z) {
+  namespace cg = cooperative_groups;
+  const cg::coalesced_group g = cg::coalesced_threads();
+  const cg::coalesced_group part = cg::labeled_partition(g, target);
+  if (g.all(part.size() == 1)) {  // no shared target in this warp
+    red_add(fe + target, x, y, z);
+    return;
+  }
+  const R sx = cg::reduce(part, x, cg::plus<R>());
+  const R sy = cg::reduce(part, y, cg::plus<R>());
+  const R sz = cg::reduce(part, z, cg::plus<R>());
+  if (part.thread_rank() == 0) red_add(fe + target, sx, sy, sz);
 }
 
 // ---------------------------------------------------------------------------
@@ -1256,6 +1281,55 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
   if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
 }
 
+// Owner-aggregated atomic accumulation on the EXACT layout (fp64 and the
+// exact-layout tolerance contexts): one thread per mass walks the entries
+// it is m1 of (ascending slot), sums their forces in registers, pushes -f
+// to each m2 and its own sum with one reduction each (see k_split_atomic,
+// sl_split.cuh).  Each spring is evaluated once, with entry_force's
+// arithmetic and side effects; a yield break kills both entries.
+template <int P>
+static __global__ void __launch_bounds__(256)
+    k_gather_atomic(const KState S, const StepP T) {
+  pdl_wait();
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  if (stopped(S, T.step)) return;
+  const uint32_t fl = flags_of(((const R4 *)S.vel)[i].w);
+  if (!(fl & MF_ALIVE)) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const void *plo = S.plo[T.cur];
+  const R4 me = pos[i];
+  const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
+  const int64_t w = i >> 5;
+  const int64_t ebase = S.slice_ptr[w] + (i & 31);
+  const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
+  R4 *fe = (R4 *)S.fext;
+  R ox = 0, oy = 0, oz = 0;
+  for (int t = 0; t < width; t++) {
+    const int64_t e = ebase + 32 * (int64_t)t;
+    const uint32_t jr = __ldg(S.ent_j + e);
+    if (jr & (EJ_DEAD | EJ_M2)) continue;  // dead, padding, or m2 side
+    const uint32_t j = jr & EJ_MASK;
+    const R4 o = pos[j];
+    // entry_force on a zeroed accumulator: the m1-side force itself
+    R gx = 0, gy = 0, gz = 0;
+    const int32_t s = S.ent_s[e];
+    const bool was_alive = S.s_alive[s] != 0;
+    if (!entry_force<P>(S, e, jr, me, ml, o, lo_at<P>(o, plo, j),
+                        ((const F2 *)S.ent_kL0)[e], T.sim_t, gx, gy, gz))
+      continue;
+    if (was_alive && !S.s_alive[s]) kill_entries(S, s);  // broke: both
+    ox += gx;
+    oy += gy;
+    oz += gz;
+    red_add(fe + j, -gx, -gy, -gz);
+  }
+  red_add(fe + i, ox, oy, oz);
+}
+
 // Atomic variant, spring side: one thread per spring slot (kernels.py:36-83
 // with the accumulation of the paper's GPU design).
 template <int P, bool SPECIAL>
@@ -1298,8 +1372,8 @@ static __global__ void __launch_bounds__(256)
     scale += damper_scale<P, F>(S, s, dx, dy, dz, dx * dx + dy * dy + dz * dz);
   const F gx = scale * dx, gy = scale * dy, gz = scale * dz;
   R4 *fe = (R4 *)S.fext;
-  red_add(fe + ab.x, (R)gx, (R)gy, (R)gz);
-  red_add(fe + ab.y, -(R)gx, -(R)gy, -(R)gz);
+  red_add_agg(fe, (uint32_t)ab.x, (R)gx, (R)gy, (R)gz);
+  red_add_agg(fe, (uint32_t)ab.y, -(R)gx, -(R)gy, -(R)gz);
   if (SPECIAL && special) {
     const F thr = (F)((const FS *)S.thr)[s];
     const F mag = fmag >= (F)0.0 ? fmag : -fmag;
@@ -1353,6 +1427,9 @@ struct Launch {
   void (*spring_atomic)(const KState &, const StepP &, bool special,
                         cudaStream_t);
   void (*mass)(const KState &, const EnvP &, const StepP &, cudaStream_t);
+  // owner-aggregated atomic force pass (split or exact layout)
+  void (*owner_atomic)(const KState &, const StepP &, const struct ActP &,
+                       cudaStream_t);
   // split layout (tolerance modes; no-ops for fp64)
   void (*split)(const KState &, const EnvP &, const StepP &,
                 const struct ActP &, cudaStream_t);

@@ -57,6 +57,16 @@ struct SplitLaunch {
                      const ActP &A, cudaStream_t st) {
     launch_pdl(k_split_step<P, FO, ACT>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T, A);
   }
+  static void atomic(const KState &S, const StepP &T, const ActP &A,
+                     cudaStream_t st) {
+    if (S.m_n <= 0) return;
+    if (A.n > 1)
+      launch_pdl(k_split_atomic<P, true>, (int)blocks_for(S.m_n), 256, 0, st,
+                 S, T, A);
+    else
+      launch_pdl(k_split_atomic<P, false>, (int)blocks_for(S.m_n), 256, 0,
+                 st, S, T, A);
+  }
   static void step(const KState &S, const EnvP &E, const StepP &T,
                    const ActP &A, cudaStream_t st, bool force_only) {
     if (S.m_n <= 0) return;
@@ -164,6 +174,8 @@ struct SplitLaunch {
 };
 template <>
 struct SplitLaunch<PREC_FP64> {
+  static void atomic(const KState &, const StepP &, const ActP &,
+                     cudaStream_t) {}
   static void step(const KState &, const EnvP &, const StepP &, const ActP &,
                    cudaStream_t, bool) {}
   static void tma(const KState &, const EnvP &, const StepP &,
@@ -235,6 +247,14 @@ struct SplitLaunch<PREC_FP64> {
                  cudaStream_t st) {                                          \
     if (S.m_n > 0) launch_pdl(k_mass<PREC>, (int)blocks_for(S.m_n), 256, 0, st, S, E, T); \
   }                                                                          \
+  void FN##_owner_atomic(const KState &S, const StepP &T, const ActP &A,    \
+                         cudaStream_t st) {                                  \
+    if (S.split)                                                             \
+      SplitLaunch<PREC>::atomic(S, T, A, st);                                \
+    else if (S.m_n > 0)                                                      \
+      launch_pdl(k_gather_atomic<PREC>, (int)blocks_for(S.m_n), 256, 0, st,  \
+                 S, T);                                                      \
+  }                                                                          \
   void FN##_split(const KState &S, const EnvP &E, const StepP &T,           \
                   const ActP &A, cudaStream_t st) {                          \
     SplitLaunch<PREC>::step(S, E, T, A, st, false);                          \
@@ -269,6 +289,7 @@ struct SplitLaunch<PREC_FP64> {
   const Launch &FN() {                                                       \
     static const Launch L = {FN##_gather, FN##_tma, FN##_tma_setup,          \
                              FN##_force, FN##_spring, FN##_mass,             \
+                             FN##_owner_atomic,                              \
                              FN##_split, FN##_split_force, FN##_split_tma,   \
                              FN##_split_setup, FN##_win,                     \
                              FN##_win_setup, FN##_fused, FN##_fused_setup};  \

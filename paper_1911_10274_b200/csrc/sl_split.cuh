@@ -446,6 +446,134 @@ __device__ __forceinline__ void split_forces(
   fz = f.z;
 }
 
+// ---------------------------------------------------------------------------
+// Owner-aggregated ATOMIC accumulation on the split layout (the paper's
+// atomic design; reference linearizable accumulation,
+// kernels.py:28-86 -- order-free, tolerance only): one thread per mass
+// walks its A section (the springs it is m1 of), sums their forces in
+// registers and pushes -f to each m2 with a vector RED, then adds its own
+// sum with one RED -- 14 reductions per lattice mass instead of the 26 of
+// one thread per spring.  Every spring is evaluated exactly once.
+// Special masses (callable waveforms, yield, dampers) take the reference
+// semantics per entry (split_atomic_exact); a yield break kills both of the
+// spring's entries.
+
+// one A entry through the full reference semantics; returns the force on
+// m1 (this mass) in g, false if it contributes nothing
+template <int P>
+__device__ __noinline__ bool split_atomic_exact(
+    const KState *S, int64_t e, typename Tr<P>::R4 me, typename Tr<P>::L ml,
+    typename Tr<P>::R4 other, typename Tr<P>::L ol, typename Tr<P>::F2 kl,
+    double sim_t, typename Tr<P>::M *g) {
+  using F = typename Tr<P>::M;
+  using FS = typename Tr<P>::F;
+  F dx, dy, dz;
+  pdiff<P>(me, ml, other, ol, dx, dy, dz);
+  const F len2 = dx * dx + dy * dy + dz * dz;
+  const int32_t s = S->sp_s[e];
+  if (len2 == (F)0.0) {  // kernels.py:50-54
+    if (!S->s_degen[s]) {
+      S->s_degen[s] = 1;
+      count_spring(*S, 2, s);
+    }
+    return false;
+  }
+  F factor = (F)1.0;
+  if (S->mode[s] != 0) factor = (F)act_factor(*S, s, sim_t);
+  const F len = sqrt(len2);
+  const F fmag = (F)kl.x * (len - factor * (F)kl.y);
+  F scale = fmag / len;
+  if (S->damp) scale += damper_scale<P, F>(*S, s, dx, dy, dz, len2);
+  g[0] = scale * dx;
+  g[1] = scale * dy;
+  g[2] = scale * dz;
+  const F thr = (F)((const FS *)S->thr)[s];
+  const F mag = fmag >= (F)0.0 ? fmag : -fmag;
+  if (mag > thr) {  // breaks after applying its force (kernels.py:77-83)
+    count_spring(*S, 0, s);
+    S->s_alive[s] = 0;
+    S->ends[s] = make_int2(-1, -1);
+    kill_entries(*S, s);
+  }
+  return true;
+}
+
+template <int P, bool ACT>
+static __global__ void __launch_bounds__(256)
+    k_split_atomic(const KState S, const StepP T, const ActP A) {
+  pdl_wait();
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  using F2 = typename Tr<P>::F2;
+  using M = typename Tr<P>::M;
+  __shared__ ActG tab[ACT ? MAX_ACT_GROUPS : 1];
+  if (stopped(S, T.step)) return;  // uniform
+  if constexpr (ACT) act_table(A, T.sim_t, tab);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S.m_n) return;
+  const uint32_t fl = flags_of(((const R4 *)S.vel)[i].w);
+  if (!(fl & MF_ALIVE)) return;
+  const R4 *pos = (const R4 *)S.pos[T.cur];
+  const void *plo = S.plo[T.cur];
+  const R4 me = pos[i];
+  const typename Tr<P>::L ml = lo_at<P>(me, plo, i);
+  const int64_t w = i >> 5;
+  const int wa = (int)(__ldg(S.sp_w + w) & 0xFFFF);
+  const int64_t ea = w * S.sp_rows * 32 + (i & 31);
+  const int64_t kc = (w << (S.sp_a + 5)) | (i & 31);
+  const F2 *kla = (const F2 *)S.sp_kl + kc;
+  const uint32_t sent = S.sp_sent;
+  R4 *fe = (R4 *)S.fext;
+  M ox = 0, oy = 0, oz = 0;
+  const bool special = (fl & MF_SPECIAL) != 0;
+  for (int t = 0; t < wa; t++) {
+    const uint32_t j = __ldg(S.sp_j + ea + 32 * t);
+    if (j == sent) continue;
+    const R4 o = ldg4(pos + j);
+    const typename Tr<P>::L ol = lo_at<P>(o, plo, j);
+    const F2 kl = kla[32 * t];
+    M g[3];
+    if (special) {
+      if (!split_atomic_exact<P>(S.self, ea + 32 * t, me, ml, o, ol, kl,
+                                 T.sim_t, g))
+        continue;
+    } else {
+      M dx, dy, dz;
+      pdiff<P>(me, ml, o, ol, dx, dy, dz);
+      const M len2 = dx * dx + dy * dy + dz * dz;
+      if (len2 == (M)0) {  // zero length: flag it, no force
+        const int32_t s = S.sp_s[ea + 32 * t];
+        if (!S.s_degen[s]) {
+          S.s_degen[s] = 1;
+          count_spring(S, 2, s);
+        }
+        continue;
+      }
+      M r;
+      if constexpr (P == PREC_FP32) {
+        r = rsqrtf(len2);
+      } else {
+        r = (double)rsqrtf((float)len2);
+        r = r * (1.5 - 0.5 * len2 * r * r);
+      }
+      M l0 = (M)kl.y;
+      if constexpr (ACT)
+        l0 = (M)act_fast(tab, S.sp_actc[kc + 32 * t], S.sp_acto,
+                         [&] { return (uint32_t)(kc + 32 * t); }, T.sim_t) *
+             l0;
+      const M sc = (M)kl.x * (len2 * r - l0) * r;
+      g[0] = sc * dx;
+      g[1] = sc * dy;
+      g[2] = sc * dz;
+    }
+    ox += g[0];
+    oy += g[1];
+    oz += g[2];
+    red_add(fe + j, -(R)g[0], -(R)g[1], -(R)g[2]);
+  }
+  red_add(fe + i, (R)ox, (R)oy, (R)oz);
+}
+
 // Plain variant: one thread per mass, entries read from global memory.
 // Serves spring_pass (FORCE_ONLY) and layouts too wide for the TMA stages.
 template <int P, bool FORCE_ONLY, bool ACT>
