@@ -1553,21 +1553,32 @@ int build_split_layout(sl_ctx *c, bool *used) {
   return SL_OK;
 }
 
-// SL_ACC_AUTO: the deterministic gather unless the mesh has hub masses
-// whose incidence lists would serialise one thread (or warp) per mass; then
-// the per-spring atomic variant spreads them.  Every mesh
-// measured so far picks the gather.
-constexpr int64_t AUTO_HUB_ENTRIES = 128;  // entries per mass (lattice: 26)
+// Accumulation variant per mesh (tools/hub_sweep.py, profiles/hub_sweep_r2.txt:
+// gather vs atomic step time on lattices and on hub meshes of degree D).
+// The gather's slice-ELL pads a 32-mass slice to its widest list, so a hub
+// makes its whole slice D wide; the per-spring atomic kernel's cost does
+// not depend on D.  Measured crossover (B200): fp32 / mixed between D = 64
+// (gather 131 us vs atomic 205 us) and 128 (970 vs 203); fp64 between 8
+// (208 vs 297) and 16 (359 vs 278).  A mesh is a "hub mesh" when its
+// widest list exceeds the threshold AND padding more than doubles the
+// stored entries -- uniform meshes (a lattice: 26 entries every mass)
+// never qualify, whatever their width.
+int64_t hub_threshold(const sl_ctx *c) {
+  if (const char *ev = getenv("SL_HUB_ENTRIES")) return atoll(ev);
+  return c->prec == PREC_FP64 ? 12 : 96;
+}
 int resolve_accumulation(sl_ctx *c, int acc) {
   const int64_t widest = c->split ? c->sp_wa + c->sp_wb : c->max_width;
+  const bool hubs = c->layout_valid && widest > hub_threshold(c) &&
+                    c->n_entries > 4 * c->s_n;
   // atomic accumulation: the owner-aggregated kernel (one thread per mass,
   // its m1 springs) on regular meshes; on hub meshes one thread per spring
   // with warp-aggregated reductions (the hub's thread would serialise)
-  c->atomic_owner = widest <= AUTO_HUB_ENTRIES && c->layout_valid;
+  c->atomic_owner = c->layout_valid && !hubs;
   if (const char *ev = getenv("SL_ATOMIC_KERNEL"))  // tuning / sweeps
     c->atomic_owner = c->layout_valid && strcmp(ev, "spring") != 0;
   if (acc != SL_ACC_AUTO) return acc;
-  c->auto_atomic = widest > AUTO_HUB_ENTRIES;
+  c->auto_atomic = hubs;
   return c->auto_atomic ? SL_ACC_ATOMIC : SL_ACC_GATHER;
 }
 

@@ -525,24 +525,50 @@ static __global__ void __launch_bounds__(256)
   const uint32_t sent = S.sp_sent;
   R4 *fe = (R4 *)S.fext;
   M ox = 0, oy = 0, oz = 0;
-  const bool special = (fl & MF_SPECIAL) != 0;
-  for (int t = 0; t < wa; t++) {
-    const uint32_t j = __ldg(S.sp_j + ea + 32 * t);
-    if (j == sent) continue;
-    const R4 o = ldg4(pos + j);
-    const typename Tr<P>::L ol = lo_at<P>(o, plo, j);
-    const F2 kl = kla[32 * t];
-    M g[3];
-    if (special) {
-      if (!split_atomic_exact<P>(S.self, ea + 32 * t, me, ml, o, ol, kl,
-                                 T.sim_t, g))
+  if (fl & MF_SPECIAL) {
+    for (int t = 0; t < wa; t++) {
+      const uint32_t j = __ldg(S.sp_j + ea + 32 * t);
+      if (j == sent) continue;
+      const R4 o = ldg4(pos + j);
+      M g[3];
+      if (!split_atomic_exact<P>(S.self, ea + 32 * t, me, ml, o,
+                                 lo_at<P>(o, plo, j), kla[32 * t], T.sim_t,
+                                 g))
         continue;
-    } else {
+      ox += g[0];
+      oy += g[1];
+      oz += g[2];
+      red_add(fe + j, -(R)g[0], -(R)g[1], -(R)g[2]);
+    }
+    red_add(fe + i, (R)ox, (R)oy, (R)oz);
+    return;
+  }
+  // fast path, U entries per batch: every load of a batch is issued before
+  // any is consumed (the kernel is latency-bound on the dependent partner
+  // gathers, profiles/ncu_k_split_atomic_r2.txt)
+  constexpr int U = 4;
+  for (int t0 = 0; t0 < wa; t0 += U) {
+    uint32_t j[U];
+    R4 o[U];
+    typename Tr<P>::L ol[U];
+    F2 kl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      j[u] = t0 + u < wa ? __ldg(S.sp_j + ea + 32 * (t0 + u)) : sent;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      o[u] = ldg4(pos + j[u]);  // sentinel rows for padding / dead entries
+      ol[u] = lo_at<P>(o[u], plo, j[u]);
+      kl[u] = t0 + u < wa ? kla[32 * (t0 + u)] : F2{};
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (j[u] == sent) continue;
       M dx, dy, dz;
-      pdiff<P>(me, ml, o, ol, dx, dy, dz);
+      pdiff<P>(me, ml, o[u], ol[u], dx, dy, dz);
       const M len2 = dx * dx + dy * dy + dz * dz;
       if (len2 == (M)0) {  // zero length: flag it, no force
-        const int32_t s = S.sp_s[ea + 32 * t];
+        const int32_t s = S.sp_s[ea + 32 * (t0 + u)];
         if (!S.s_degen[s]) {
           S.s_degen[s] = 1;
           count_spring(S, 2, s);
@@ -556,20 +582,19 @@ static __global__ void __launch_bounds__(256)
         r = (double)rsqrtf((float)len2);
         r = r * (1.5 - 0.5 * len2 * r * r);
       }
-      M l0 = (M)kl.y;
+      M l0 = (M)kl[u].y;
       if constexpr (ACT)
-        l0 = (M)act_fast(tab, S.sp_actc[kc + 32 * t], S.sp_acto,
-                         [&] { return (uint32_t)(kc + 32 * t); }, T.sim_t) *
+        l0 = (M)act_fast(tab, S.sp_actc[kc + 32 * (t0 + u)], S.sp_acto,
+                         [&] { return (uint32_t)(kc + 32 * (t0 + u)); },
+                         T.sim_t) *
              l0;
-      const M sc = (M)kl.x * (len2 * r - l0) * r;
-      g[0] = sc * dx;
-      g[1] = sc * dy;
-      g[2] = sc * dz;
+      const M sc = (M)kl[u].x * (len2 * r - l0) * r;
+      const M gx = sc * dx, gy = sc * dy, gz = sc * dz;
+      ox += gx;
+      oy += gy;
+      oz += gz;
+      red_add(fe + j[u], -(R)gx, -(R)gy, -(R)gz);
     }
-    ox += g[0];
-    oy += g[1];
-    oz += g[2];
-    red_add(fe + j, -(R)g[0], -(R)g[1], -(R)g[2]);
   }
   red_add(fe + i, (R)ox, (R)oy, (R)oz);
 }

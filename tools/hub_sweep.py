@@ -47,12 +47,13 @@ def time_variant(case, precision, acc, kernel, steps=200):
         os.environ.pop("SL_ATOMIC_KERNEL", None)
     ctx = case_context(case, precision)
     c = np.zeros(3, np.int64)
-    a = 0 if acc == "gather" else 1
+    a = {"gather": 0, "atomic": 1, "auto": 2}[acc]
     t = np.arange(steps + 10) * 1e-5
     ctx.step(t[:10], 1e-5, a, c)
     ctx.step(t[10:], 1e-5, a, c)
     ms = ctx.last_step_ms() / steps
     st = ctx.stats()
+    st["launches_per_step"] = st["kernel_launches"]
     ctx.close()
     return ms, st
 
@@ -67,7 +68,7 @@ def main():
     for name, case, width in meshes:
         springs = len(case["s_m1"])
         for acc, kernel in (("gather", None), ("atomic", "owner"),
-                            ("atomic", "spring")):
+                            ("atomic", "spring"), ("auto", None)):
             ms, st = time_variant(case, prec, acc, kernel)
             print(json.dumps({"mesh": name, "widest": width,
                               "springs": springs, "precision": prec,
@@ -75,6 +76,7 @@ def main():
                               f"atomic-{kernel}", "us_per_step": 1e3 * ms,
                               "upd_per_s": springs / (ms / 1e3),
                               "step_path": st["step_path"]}), flush=True)
+        os.environ.pop("SL_ATOMIC_KERNEL", None)
 
 
 if __name__ == "__main__":
