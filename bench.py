@@ -174,6 +174,15 @@ def algorithmic_bytes(springs: int, masses: int, precision: str,
     return springs * (8 + (2 + extra_words) * w_s) + masses * bm
 
 
+def _native_pinned_copy(a):
+    """A page-locked copy of a host array (the inputs of an e2e segment live
+    in pinned memory, as the contract's host buffers)."""
+    from paper_1911_10274_b200 import _native
+    out = _native.pinned_empty(a.shape, a.dtype)
+    out[...] = a
+    return out
+
+
 def store_case(st, env):
     from paper_1911_10274_b200 import engine
     m, s = st.mass_slot_count, st.spring_slot_count
@@ -495,31 +504,49 @@ def main():
         roof["traffic_gbs"] = traffic / (sec / args.steps) / 1e9
         roof["traffic_frac"] = roof["traffic_gbs"] / peak
 
-    # e2e through the public API, host store authoritative at both ends
+    # e2e through the public API, host store authoritative at both ends: an
+    # RL / control segment in steady state -- set-state (the inputs: new
+    # positions and velocities written into the host store, io.apply_
+    # snapshot), run K steps (SimController.start -> wait_for_event), get-
+    # state (snapshot).  One untimed segment first brings host and device
+    # in sync, as a running controller is between segments; the timed one
+    # then moves the columns the host touched (pos, vel) up and the state
+    # down (DeviceMirror.push / pull).
     e2e = None
     if not args.no_e2e:
+        from paper_1911_10274_b200 import io as sio
         ctl = SimController(st, env, cfg)
         k = args.steps
         m = st.mass_slot_count
+        ctl.start(k * dt)
+        ctl.wait_for_event()
+        warm = ctl.snapshot()
+        ids = warm.ids.copy()
+        pos_in = _native_pinned_copy(warm.positions)
+        vel_in = _native_pinned_copy(warm.velocities)
+        full0 = getattr(engine.mirror_for(st, cfg), "full_pushes", 0)
         if dist is not None:
             dist.barrier()
         w0 = time.perf_counter()
+        sio.apply_snapshot(st, ids, pos_in, vel_in)
         ctl.start(k * dt)
         rep = ctl.wait_for_event()
         snap = ctl.snapshot()
         wall = time.perf_counter() - w0
+        full = getattr(engine.mirror_for(st, cfg), "full_pushes", 0) - full0
         ctl.stop()
-        assert rep.step_count == k, rep
+        assert rep.step_count == 2 * k, rep
         if dist is not None:
             import torch
             wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
-        h2d = m * (5 * 24 + 8 + 1 + 1 + 8) + 16 * (m + 1)
+        h2d = m * 48 if not full else m * (5 * 24 + 8 + 1 + 1 + 8)
         d2h = m * 4 * 24
         e2e = {"value": world * springs * k / wall, "unit": unit,
                "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
-               "wall_s": wall, "api": "SimController.start/wait_for_event/"
-                                      "snapshot", "snapshot_rows":
-                   int(len(snap.ids))}
+               "wall_s": wall, "api": "io.apply_snapshot + SimController."
+                                      "start/wait_for_event/snapshot",
+               "segment": "set-state, K steps, get-state (steady state)",
+               "snapshot_rows": int(len(snap.ids))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -214,6 +214,14 @@ int sl_spring_pass(sl_ctx *ctx, double sim_t, int accumulation,
 /* Single mass pass only (engine.mass_pass, engine.py:218-255). */
 int sl_mass_pass(sl_ctx *ctx, double dt, int64_t *err_slot);
 
+/* Host state of EVERY mass back into a context that holds the rest:
+ * positions, velocities and/or accelerations (NULL keeps the device copy)
+ * of m_n masses (== the uploaded count); flags, masses, loads and f_ext
+ * stay.  The device mirror's partial push: after a pause only the columns
+ * the host touched travel (engine.DeviceMirror.push). */
+int sl_write_state(sl_ctx *ctx, int64_t m_n, const double *pos,
+                   const double *vel, const double *acc);
+
 /* Opt-in spring damping (north_star "Hooke plus damping"): damping[s] =
  * c >= 0 (N s / m) for every spring slot [0, s_n); the force on m1 gains
  * c ((v2 - v1) . d^) d^ (equal and opposite on m2).  No reference

@@ -40,7 +40,7 @@ EXPORTS = (
     "sl_build_lattice", "sl_host_fill", "sl_host_copy",
     "sl_host_masked_extrema", "sl_set_spring_damping", "sl_halo_init",
     "sl_halo_local", "sl_halo_ipc_handles", "sl_halo_ipc_open",
-    "sl_halo_set_peer", "sl_halo_commit")
+    "sl_halo_set_peer", "sl_halo_commit", "sl_write_state")
 
 
 class SlStats(C.Structure):
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH):
             "sl_halo_ipc_open": ([P, P, P], I),
             "sl_halo_set_peer": ([P, I, P, I], I),
             "sl_halo_commit": ([P], I),
+            "sl_write_state": ([P, I64, P, P, P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -267,6 +268,10 @@ class Context:
                 f"{self.lib.sl_last_error(None).decode()}")
         self.h = h
         self.m_n = 0
+        # advanced on every call that moves the device state past the host
+        # copy (steps, single passes): the device mirror knows whether the
+        # host store still equals the device after a pull
+        self.epoch = 0
         self.s_n = 0
 
     # ------------------------------------------------------------ errors
@@ -304,6 +309,15 @@ class Context:
         self._check(self.lib.sl_upload_masses(self.h, n, *map(_ptr, a)),
                     "sl_upload_masses")
         self.m_n = n
+
+    def write_state(self, pos=None, vel=None, acc=None):
+        """Whole pos / vel / acc columns into the context (sl_write_state);
+        None keeps the device copy."""
+        cols = [None if a is None else _c(a, np.float64)
+                for a in (pos, vel, acc)]
+        self._check(self.lib.sl_write_state(
+            self.h, self.m_n, *[_ptr(a) if a is not None else None
+                                for a in cols]), "sl_write_state")
 
     def upload_springs(self, m1, m2, m1gen, m2gen, rest, k, diam, yld, mode,
                        amp, freq, off, per, alive, degen):
@@ -403,6 +417,7 @@ class Context:
              counters: np.ndarray) -> tuple[int, int]:
         """Returns (steps_done, err_slot); raises NumericalAbort on a
         non-finite step (after the state of that step is resident)."""
+        self.epoch += 1
         t = _c(sim_times, np.float64)
         err = C.c_int64(0)
         done = C.c_int64(0)
@@ -416,6 +431,7 @@ class Context:
 
     def step_async(self, sim_times, dt: float, accumulation: int):
         """Enqueue steps without synchronising (sl_step_async)."""
+        self.epoch += 1
         t = _c(sim_times, np.float64)
         self._check(self.lib.sl_step_async(self.h, len(t), _ptr(t),
                                            float(dt), int(accumulation)),
@@ -463,12 +479,14 @@ class Context:
 
     def spring_pass(self, sim_t: float, accumulation: int,
                     counters: np.ndarray):
+        self.epoch += 1
         self._check(self.lib.sl_spring_pass(self.h, float(sim_t),
                                             int(accumulation),
                                             _ptr(counters)),
                     "sl_spring_pass")
 
     def mass_pass(self, dt: float) -> int:
+        self.epoch += 1
         err = C.c_int64(0)
         rc = self.lib.sl_mass_pass(self.h, float(dt), C.byref(err))
         if rc == SL_ENUMERIC:

@@ -267,6 +267,49 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
   alive_o[i] = alive[r];
 }
 
+// Positions / velocities (/ accelerations) of every mass from host fp64
+// columns, the rest of the device state kept: velocity flags, the record's
+// mass (fp64 / mixed), f_ext, load (sl_write_state).  Both position
+// buffers are written (static masses are never rewritten by a step).
+template <int P>
+__global__ void k_write_state(int64_t n, const double *pos, const double *vel,
+                              const double *acc, void *pos0, void *pos1,
+                              void *plo0, void *plo1, void *velb,
+                              void *accb) {
+  using R = typename Tr<P>::R;
+  using R4 = typename Tr<P>::R4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (pos) {
+    R4 p = ((const R4 *)pos0)[i];
+    p.x = (R)pos[3 * i];
+    p.y = (R)pos[3 * i + 1];
+    p.z = (R)pos[3 * i + 2];
+    if constexpr (P == PREC_FP32) {
+      p.w = (float)(pos[3 * i] - (double)p.x);
+      const float2 l = make_float2((float)(pos[3 * i + 1] - (double)p.y),
+                                   (float)(pos[3 * i + 2] - (double)p.z));
+      ((float2 *)plo0)[i] = l;
+      ((float2 *)plo1)[i] = l;
+    }
+    ((R4 *)pos0)[i] = p;
+    ((R4 *)pos1)[i] = p;
+  }
+  if (vel) {
+    R4 v = ((const R4 *)velb)[i];
+    v.x = (R)vel[3 * i];
+    v.y = (R)vel[3 * i + 1];
+    v.z = (R)vel[3 * i + 2];
+    ((R4 *)velb)[i] = v;
+  }
+  if (acc) {
+    R *a = (R *)accb + 3 * i;
+    a[0] = (R)acc[3 * i];
+    a[1] = (R)acc[3 * i + 1];
+    a[2] = (R)acc[3 * i + 2];
+  }
+}
+
 template <int P>
 __global__ void k_unpack_masses(int64_t n, const void *posb, const void *plob,
                                 const void *velb, const void *accb,
@@ -2087,6 +2130,35 @@ int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
   // the parity-mode window blocks are not edited in place: re-index
   if (c->win && !c->split) c->layout_valid = false;
   CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_write_state(sl_ctx *c, int64_t m_n, const double *pos,
+                   const double *vel, const double *acc) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (m_n != c->m_n)
+    return fail(c, SL_EINVAL, "sl_write_state: %lld masses, context has %lld",
+                (long long)m_n, (long long)c->m_n);
+  if (c->async_open)
+    return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
+  if (m_n == 0 || (!pos && !vel && !acc)) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  CK(c->stage.ensure(3 * align256(24 * m_n) + 1024));
+  size_t off = 0;
+  const double *dp, *dv, *da;
+  int rc;
+  if ((rc = stage_copy(c, off, pos, 3 * m_n, &dp))) return rc;
+  if ((rc = stage_copy(c, off, vel, 3 * m_n, &dv))) return rc;
+  if ((rc = stage_copy(c, off, acc, 3 * m_n, &da))) return rc;
+  auto k = c->prec == PREC_FP64   ? k_write_state<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_write_state<PREC_FP32>
+                                  : k_write_state<PREC_MIXED>;
+  k<<<blocks_for(m_n), 256, 0, c->st>>>(m_n, dp, dv, da, c->pos[0].p,
+                                        c->pos[1].p, c->plo[0].p, c->plo[1].p,
+                                        c->vel.p, c->acc.p);
+  CKL();
+  c->launches++;
+  CK(cudaStreamSynchronize(c->st));  // staging is reused by the next call
   return SL_OK;
 }
 

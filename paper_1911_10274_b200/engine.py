@@ -100,6 +100,8 @@ class DeviceMirror:
 
     def __init__(self, device: int, precision: str):
         self.ctx = _native.Context(device, precision)
+        self._mass_key = None   # (m, host array identity) at the last sync
+        self._mass_epoch = -1   # ctx.epoch at the last sync
         self.counters = np.zeros(3, np.int64)
         self._springs_key = None
         self._constraints_key = None
@@ -108,17 +110,37 @@ class DeviceMirror:
         self.degen_logged = np.zeros(0, np.bool_)
 
     # host -> device
+    # mass columns by what a host write to them changes on the device
+    _STATE_COLS = {"_m_pos", "_m_vel", "_m_acc"}
+
     def push(self, store: ObjectStore, env: Environment | None,
              masses: bool = True):
-        if not _native.is_pinned(store._m_pos):
+        raw = store._raw
+        if not _native.is_pinned(raw("_m_pos")):
             # page-locked mass columns: uploads / pulls at copy-engine speed
             store.adopt_mass_allocator(_native.pinned_empty)
         m, s = store.mass_slot_count, store.spring_slot_count
+        touched = store.take_touched()
         if masses or self.ctx.m_n != m:
-            self.ctx.upload_masses(
-                store._m_pos[:m], store._m_vel[:m], store._m_acc[:m],
-                store._m_fext[:m], store._m_load[:m], store._m_mass[:m],
-                store._m_fixed[:m], store._m_alive[:m], store._m_gen[:m])
+            # the device holds the host state when nothing but this mirror
+            # moved it since the last sync (same arrays, no steps since);
+            # then only the columns the host touched travel
+            key = (m, id(raw("_m_pos")))
+            synced = (self._mass_key == key and self.ctx.m_n == m and
+                      self._mass_epoch == self.ctx.epoch)
+            if not synced or touched - self._STATE_COLS:
+                self.ctx.upload_masses(*(raw(c)[:m] for c in (
+                    "_m_pos", "_m_vel", "_m_acc", "_m_fext", "_m_load",
+                    "_m_mass", "_m_fixed", "_m_alive", "_m_gen")))
+                self.full_pushes = getattr(self, "full_pushes", 0) + 1
+            elif touched:
+                self.ctx.write_state(
+                    *(raw(c)[:m] if c in touched else None
+                      for c in ("_m_pos", "_m_vel", "_m_acc")))
+            self._mass_key = key
+            self._mass_epoch = self.ctx.epoch
+        else:  # the caller vouches for the device copy; keep them pending
+            store.__dict__["_touched"] |= touched
         key = (s, m, store.topology_version, store.spring_param_version,
                id(store._s_m1))
         if key != self._springs_key and self._replay_springs(store, key):
@@ -218,9 +240,13 @@ class DeviceMirror:
              acc: bool = True, fext: bool = True):
         store.materialize_sync()
         m, s = store.mass_slot_count, store.spring_slot_count
-        self.ctx.download_masses(store._m_pos[:m], store._m_vel[:m],
-                                 store._m_acc[:m] if acc else None,
-                                 store._m_fext[:m] if fext else None)
+        raw = store._raw
+        self.ctx.download_masses(raw("_m_pos")[:m], raw("_m_vel")[:m],
+                                 raw("_m_acc")[:m] if acc else None,
+                                 raw("_m_fext")[:m] if fext else None)
+        if acc and fext:  # host == device again
+            self._mass_key = (m, id(raw("_m_pos")))
+            self._mass_epoch = self.ctx.epoch
         if springs and s:
             self.ctx.download_springs(store._s_alive[:s].view(np.uint8),
                                       store._s_degen[:s].view(np.uint8))
