@@ -235,6 +235,13 @@ int sl_set_spring_damping(sl_ctx *ctx, int64_t n, const double *damping);
 /* Copy mass state back into host arrays double[m_n][3]; NULL skips. */
 int sl_download_masses(sl_ctx *ctx, double *pos, double *vel, double *acc,
                        double *fext);
+/* As sl_download_masses, but returns once pos / vel have landed: acc and
+ * f_ext (which must be page-locked) keep arriving on the context stream;
+ * sl_download_wait blocks until they have.  Work enqueued afterwards is
+ * ordered after the copies. */
+int sl_download_state(sl_ctx *ctx, double *pos, double *vel, double *acc,
+                      double *fext);
+int sl_download_wait(sl_ctx *ctx);
 /* Spring liveness / zero-length flags back into bool[s_n]; NULL skips. */
 int sl_download_springs(sl_ctx *ctx, uint8_t *alive, uint8_t *degen);
 
@@ -328,6 +335,8 @@ int sl_build_lattice(int64_t nx, int64_t ny, int64_t nz, const double *corner,
  * workers (first touch of fresh store capacity in parallel). */
 int sl_host_fill(void *dst, const void *value, size_t elem_bytes,
                  int64_t count, int threads);
+/* *out = 1 iff ids[i] == i for every i < n (host, `threads` workers). */
+int sl_host_is_iota(const int64_t *ids, int64_t n, int threads, int *out);
 /* memcpy on `threads` workers (snapshot copies into fresh arrays). */
 int sl_host_copy(void *dst, const void *src, size_t bytes, int threads);
 /* min / max of v over mask != 0 (mask may be NULL), NaN-propagating like

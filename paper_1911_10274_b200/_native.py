@@ -40,7 +40,8 @@ EXPORTS = (
     "sl_build_lattice", "sl_host_fill", "sl_host_copy",
     "sl_host_masked_extrema", "sl_set_spring_damping", "sl_halo_init",
     "sl_halo_local", "sl_halo_ipc_handles", "sl_halo_ipc_open",
-    "sl_halo_set_peer", "sl_halo_commit", "sl_write_state")
+    "sl_halo_set_peer", "sl_halo_commit", "sl_write_state",
+    "sl_host_is_iota", "sl_download_state", "sl_download_wait")
 
 
 class SlStats(C.Structure):
@@ -110,6 +111,9 @@ def load_library(path: str = LIB_PATH):
             "sl_halo_set_peer": ([P, I, P, I], I),
             "sl_halo_commit": ([P], I),
             "sl_write_state": ([P, I64, P, P, P], I),
+            "sl_host_is_iota": ([P, I64, I, P], I),
+            "sl_download_state": ([P, P, P, P, P], I),
+            "sl_download_wait": ([P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -217,6 +221,17 @@ def masked_extrema(v: np.ndarray, mask: np.ndarray | None):
     if rc != SL_OK:
         raise SoftlatError(f"sl_host_masked_extrema failed ({rc})")
     return lo.value, hi.value
+
+
+def host_is_iota(ids: np.ndarray) -> bool:
+    """ids == arange(len(ids)) (host threads)."""
+    ids = np.ascontiguousarray(ids, np.int64)
+    out = C.c_int(0)
+    rc = load_library().sl_host_is_iota(_ptr(ids), len(ids), host_threads(),
+                                        C.byref(out))
+    if rc != SL_OK:
+        raise SoftlatError(f"sl_host_is_iota failed ({rc})")
+    return bool(out.value)
 
 
 def host_copy_into(dst: np.ndarray, src: np.ndarray) -> None:
@@ -574,6 +589,16 @@ class Context:
         d = _c(damping, np.float64)
         self._check(self.lib.sl_set_spring_damping(self.h, len(d), _ptr(d)),
                     "sl_set_spring_damping")
+
+    def download_state(self, pos, vel, acc, fext):
+        """pos / vel now; acc / f_ext (page-locked) land asynchronously --
+        download_wait() before reading them."""
+        self._check(self.lib.sl_download_state(
+            self.h, *[_ptr(a) if a is not None else None
+                      for a in (pos, vel, acc, fext)]), "sl_download_state")
+
+    def download_wait(self):
+        self._check(self.lib.sl_download_wait(self.h), "sl_download_wait")
 
     def last_step_ms(self) -> float:
         """Device time of the step kernels of the last step() call."""

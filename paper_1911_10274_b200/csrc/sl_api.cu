@@ -81,6 +81,8 @@ struct sl_ctx {
   cudaStream_t st = nullptr, side = nullptr;
   // k0 / k1 bracket the step kernels of the last sl_step call
   cudaEvent_t k0 = nullptr, k1 = nullptr;
+  cudaEvent_t head_ev = nullptr, tail_ev = nullptr;  // sl_download_state
+  bool tail_pending = false;
   bool k_valid = false;
   cudaEvent_t t0 = nullptr, t1 = nullptr, snap_ev = nullptr,
               snap_done = nullptr;
@@ -1753,6 +1755,10 @@ int sl_create(int device, int precision, sl_ctx **out) {
   if (e == cudaSuccess) e = cudaEventCreate(&c->k0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->k1);
   if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->head_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->tail_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming);
@@ -1811,6 +1817,8 @@ int sl_destroy(sl_ctx *c) {
   if (c->t1) cudaEventDestroy(c->t1);
   if (c->k0) cudaEventDestroy(c->k0);
   if (c->k1) cudaEventDestroy(c->k1);
+  if (c->head_ev) cudaEventDestroy(c->head_ev);
+  if (c->tail_ev) cudaEventDestroy(c->tail_ev);
   if (c->snap_ev) cudaEventDestroy(c->snap_ev);
   if (c->snap_done) cudaEventDestroy(c->snap_done);
   if (c->st) cudaStreamDestroy(c->st);
@@ -2598,6 +2606,47 @@ int sl_download_masses(sl_ctx *c, double *pos, double *vel, double *acc,
   if (fext)
     CK(cudaMemcpyAsync(fext, df, 24 * m, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  return SL_OK;
+}
+
+int sl_download_state(sl_ctx *c, double *pos, double *vel, double *acc,
+                      double *fext) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  const int64_t m = c->m_n;
+  if (m == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  size_t vb = align256(24 * m);
+  CK(c->stage.ensure(4 * vb));
+  double *dp = pos ? (double *)c->stage.p : nullptr;
+  double *dv = vel ? (double *)((char *)c->stage.p + vb) : nullptr;
+  double *da = acc ? (double *)((char *)c->stage.p + 2 * vb) : nullptr;
+  double *df = fext ? (double *)((char *)c->stage.p + 3 * vb) : nullptr;
+  auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                  : k_unpack_masses<PREC_MIXED>;
+  k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p,
+                                      c->plo[c->cur].p, c->vel.p, c->acc.p,
+                                      c->fext.p, dp, dv, da, df);
+  CKL();
+  c->launches++;
+  if (pos) CK(cudaMemcpyAsync(pos, dp, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (vel) CK(cudaMemcpyAsync(vel, dv, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->head_ev, c->st));
+  if (acc) CK(cudaMemcpyAsync(acc, da, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (fext)
+    CK(cudaMemcpyAsync(fext, df, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->tail_ev, c->st));
+  c->tail_pending = acc || fext;
+  CK(cudaEventSynchronize(c->head_ev));  // positions / velocities landed
+  return SL_OK;
+}
+
+int sl_download_wait(sl_ctx *c) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!c->tail_pending) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(c->tail_ev));
+  c->tail_pending = false;
   return SL_OK;
 }
 

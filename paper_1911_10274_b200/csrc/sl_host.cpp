@@ -6,6 +6,7 @@
 // row; this formats rows with the C library's correctly rounded "%.17g"
 // (the same digits) on several threads.  Non-finite values follow Python:
 // "inf", "-inf", "nan" (never "-nan").
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -271,6 +272,23 @@ extern "C" int sl_host_copy(void *dst, const void *src, size_t bytes,
                [&](int64_t lo, int64_t hi) {
                  std::memcpy(d + lo, s + lo, (size_t)(hi - lo));
                });
+  return SL_OK;
+}
+
+// *out = 1 when ids[i] == i for all i < n (a snapshot of every slot in
+// order: io.apply_snapshot then copies whole columns), else 0.
+extern "C" int sl_host_is_iota(const int64_t *ids, int64_t n, int threads,
+                               int *out) {
+  if (n < 0 || !out || (n > 0 && !ids)) return SL_EINVAL;
+  std::atomic<int> bad{0};
+  parallel_for(n, threads, (int64_t)1 << 20, [&](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; i++)
+      if (ids[i] != i) {
+        bad.store(1, std::memory_order_relaxed);
+        return;
+      }
+  });
+  *out = bad.load() ? 0 : 1;
   return SL_OK;
 }
 

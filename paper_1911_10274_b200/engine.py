@@ -241,9 +241,20 @@ class DeviceMirror:
         store.materialize_sync()
         m, s = store.mass_slot_count, store.spring_slot_count
         raw = store._raw
-        self.ctx.download_masses(raw("_m_pos")[:m], raw("_m_vel")[:m],
-                                 raw("_m_acc")[:m] if acc else None,
-                                 raw("_m_fext")[:m] if fext else None)
+        if acc and fext and _native.is_pinned(raw("_m_acc")) and \
+                _native.is_pinned(raw("_m_fext")):
+            # positions / velocities now; accelerations and f_ext keep
+            # landing in the page-locked columns while the caller goes on
+            # (store._settle waits for them on first access)
+            self.ctx.download_state(raw("_m_pos")[:m], raw("_m_vel")[:m],
+                                    raw("_m_acc")[:m], raw("_m_fext")[:m])
+            ctx = self.ctx
+            store.__dict__["_pending_tail"] = \
+                lambda: ctx.download_wait() if ctx.h else None
+        else:
+            self.ctx.download_masses(raw("_m_pos")[:m], raw("_m_vel")[:m],
+                                     raw("_m_acc")[:m] if acc else None,
+                                     raw("_m_fext")[:m] if fext else None)
         if acc and fext:  # host == device again
             self._mass_key = (m, id(raw("_m_pos")))
             self._mass_epoch = self.ctx.epoch

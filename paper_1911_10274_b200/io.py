@@ -113,12 +113,11 @@ def apply_snapshot(store: ObjectStore, ids: np.ndarray, positions: np.ndarray,
     """Overwrite positions/velocities of the given alive slots (io.py:52-59)."""
     n = store.mass_slot_count
     ids = np.asarray(ids)
+    from . import _native
     if len(ids) == n and store.mass_count == n and len(ids) and \
-            ids[0] == 0 and ids[-1] == n - 1 and \
-            np.array_equal(ids, np.arange(n)):
+            ids[0] == 0 and ids[-1] == n - 1 and _native.host_is_iota(ids):
         # every slot, in order: whole-column copies (threaded, into the
         # page-locked store columns)
-        from . import _native
         _native.host_copy_into(store._m_pos[:n], np.ascontiguousarray(
             positions, np.float64).reshape(n, 3))
         _native.host_copy_into(store._m_vel[:n], np.ascontiguousarray(
