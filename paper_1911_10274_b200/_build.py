@@ -56,6 +56,8 @@ def _deps() -> list[str]:
 def up_to_date() -> bool:
     if not os.path.exists(LIB_PATH):
         return False
+    if any(k.startswith("SL_NVCC_") for k in os.environ):
+        return False
     t = os.path.getmtime(LIB_PATH)
     return all(os.path.getmtime(d) <= t for d in _deps())
 
@@ -69,6 +71,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for unit, extra in UNITS.items():
         obj = os.path.join(OBJ_DIR, os.path.splitext(unit)[0] + ".o")
+        # tuning sweeps: extra flags for one unit, e.g.
+        # SL_NVCC_sl_kernels_fp64="-DWIN_XU=3 -DSL_WIN64_T=11"
+        tune = os.environ.get("SL_NVCC_" + os.path.splitext(unit)[0])
+        if tune:
+            extra = extra + tune.split()
         cmd = [cc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit),
                "-o", obj]
         if verbose:
