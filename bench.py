@@ -508,8 +508,8 @@ def main():
     # RL / control segment in steady state -- set-state (the inputs: new
     # positions and velocities written into the host store, io.apply_
     # snapshot), run K steps (SimController.start -> wait_for_event), get-
-    # state (snapshot).  One untimed segment first brings host and device
-    # in sync, as a running controller is between segments; the timed one
+    # state (snapshot).  Untimed segments first bring host and device in
+    # sync, as a running controller is between segments; the timed one
     # then moves the columns the host touched (pos, vel) up and the state
     # down (DeviceMirror.push / pull).
     e2e = None
@@ -518,12 +518,14 @@ def main():
         ctl = SimController(st, env, cfg)
         k = args.steps
         m = st.mass_slot_count
-        ctl.start(k * dt)
-        ctl.wait_for_event()
-        warm = ctl.snapshot()
+        for _ in range(2):  # untimed segments: steady state (pools warm)
+            ctl.start(k * dt)
+            ctl.wait_for_event()
+            warm = ctl.snapshot()
         ids = warm.ids.copy()
         pos_in = _native_pinned_copy(warm.positions)
         vel_in = _native_pinned_copy(warm.velocities)
+        del warm
         full0 = getattr(engine.mirror_for(st, cfg), "full_pushes", 0)
         if dist is not None:
             dist.barrier()
@@ -535,7 +537,7 @@ def main():
         wall = time.perf_counter() - w0
         full = getattr(engine.mirror_for(st, cfg), "full_pushes", 0) - full0
         ctl.stop()
-        assert rep.step_count == 2 * k, rep
+        assert rep.step_count == 3 * k, rep
         if dist is not None:
             import torch
             wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))

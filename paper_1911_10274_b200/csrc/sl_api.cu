@@ -1127,10 +1127,12 @@ int build_window_layout(sl_ctx *c) {
       tt = v == 4 || v == 8 || v == 12 || v == 20 || v == 24 ? v : 16;
     return build_window_tt(c, tt);
   }
+  // fp32 with compensated positions (larger windows): 16-slice tiles fit 2
+  // ring stages; measured against 12-slice tiles with 3 stages, 46.7 vs
+  // 47.6 us/step (config B, profiles/r2/sweep_win2.txt); falls back to 12
+  // when 16 does not fit at all
   if (int rc = build_window_tt(c, tt)) return rc;
-  // fp32 (compensated positions: larger windows): a ring of 3 stages of
-  // 12-slice tiles beats 2 stages of 16 (config B 47.8 vs 53.1 us/step)
-  if (c->prec == PREC_FP32 && tt == 16 && (!c->win || c->wcfg.nst < 3))
+  if (c->prec == PREC_FP32 && tt == 16 && !c->win)
     return build_window_tt(c, 12);
   return SL_OK;
 }
