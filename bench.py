@@ -582,6 +582,13 @@ def main():
                            "per_gpu_instances": (
                                "robot shard" if args.config == "D" else 1),
                            "precision": args.precision,
+                           "precision_detail": {
+                               "fp32": "fp32 arithmetic; positions "
+                                       "compensated (fp32 + fp32 low part)",
+                               "mixed": "fp64 state and force arithmetic, "
+                                        "fp32 (k, L0) storage",
+                               "fp64": "fp64, bit-exact with the reference"
+                           }[args.precision],
                            "accumulation": args.accumulation,
                            "l2": ("working set > 126 MB L2 every step "
                                   "(no flush needed)" if args.config == "B"
