@@ -233,9 +233,9 @@ __global__ void k_pack_masses(int64_t n, const double *pos, const double *vel,
   p.z = (R)pos[3 * r + 2];
   p.w = (R)mass[r];
   if constexpr (P == PREC_FP32) {  // compensated: the residuals x - hi
-    p.w = (float)(pos[3 * r] - (double)p.x);  // lx in the record
-    const float2 l = make_float2((float)(pos[3 * r + 1] - (double)p.y),
-                                 (float)(pos[3 * r + 2] - (double)p.z));
+    p.w = (float)(pos[3 * r + 2] - (double)p.z);  // lz in the record
+    const float2 l = make_float2((float)(pos[3 * r] - (double)p.x),
+                                 (float)(pos[3 * r + 1] - (double)p.y));
     ((float2 *)plo0)[i] = l;
     ((float2 *)plo1)[i] = l;
     pmass_o[i] = (float)mass[r];
@@ -288,9 +288,9 @@ __global__ void k_write_state(int64_t n, const double *pos, const double *vel,
     p.y = (R)pos[3 * i + 1];
     p.z = (R)pos[3 * i + 2];
     if constexpr (P == PREC_FP32) {
-      p.w = (float)(pos[3 * i] - (double)p.x);
-      const float2 l = make_float2((float)(pos[3 * i + 1] - (double)p.y),
-                                   (float)(pos[3 * i + 2] - (double)p.z));
+      p.w = (float)(pos[3 * i + 2] - (double)p.z);
+      const float2 l = make_float2((float)(pos[3 * i] - (double)p.x),
+                                   (float)(pos[3 * i + 1] - (double)p.y));
       ((float2 *)plo0)[i] = l;
       ((float2 *)plo1)[i] = l;
     }
@@ -326,9 +326,9 @@ __global__ void k_unpack_masses(int64_t n, const void *posb, const void *plob,
     double x = (double)p.x, y = (double)p.y, z = (double)p.z;
     if constexpr (P == PREC_FP32) {  // hi + lo, exact in fp64
       const float2 l = ((const float2 *)plob)[i];
-      x += (double)p.w;
-      y += (double)l.x;
-      z += (double)l.y;
+      x += (double)l.x;
+      y += (double)l.y;
+      z += (double)p.w;
     }
     pos[3 * i] = x;
     pos[3 * i + 1] = y;
@@ -521,9 +521,9 @@ __device__ __forceinline__ double3 pos_f64(const KState &S, int cur,
   double3 r = make_double3((double)p.x, (double)p.y, (double)p.z);
   if constexpr (P == PREC_FP32) {
     const float2 l = ((const float2 *)S.plo[cur])[i];
-    r.x += (double)p.w;
-    r.y += (double)l.x;
-    r.z += (double)l.y;
+    r.x += (double)l.x;
+    r.y += (double)l.y;
+    r.z += (double)p.w;
   }
   return r;
 }
@@ -845,8 +845,6 @@ KState make_state(sl_ctx *c) {
       S.win_blk = c->win_blk.as<unsigned char>();
       S.win_zero = c->win_zero.as<uint8_t>();
       S.win_sb = c->wcfg.bl.slice_bytes;
-      S.win_oac = c->wcfg.bl.off_acode;
-      S.win_obc = c->wcfg.bl.off_bcode;
       S.win_tt = c->wcfg.tile_slices;
     }
   }
@@ -1120,7 +1118,7 @@ int build_window_layout(sl_ctx *c) {
   // latency-bound per tile, so 8-slice tiles spread them over more SMs
   // (10^3..30^3: 8.2 -> 6.2 us/step; 50^3 and up keep 16)
   int tt = c->n_slices <= (int64_t)8 * c->sm_count ? 8 : 16;
-  if (c->prec == PREC_MIXED) tt = 16;  // the one mixed instantiation
+  if (c->prec == PREC_MIXED) tt = 16;  // mixed instantiations: 16, 12
   if (const char *ev = getenv("SL_WIN_T")) {
     const int v = atoi(ev);
     if (c->prec != PREC_MIXED)
@@ -1132,8 +1130,9 @@ int build_window_layout(sl_ctx *c) {
   // 47.6 us/step (config B, profiles/r2/sweep_win2.txt); falls back to 12
   // when 16 does not fit at all
   if (int rc = build_window_tt(c, tt)) return rc;
-  if (c->prec == PREC_FP32 && tt == 16 && !c->win)
-    return build_window_tt(c, 12);
+  // (mixed: fp64 windows of 32 B records -- 16-slice tiles of 32-bit entry
+  // words leave room for one stage only)
+  if (tt == 16 && !c->win) return build_window_tt(c, 12);
   return SL_OK;
 }
 
@@ -1145,12 +1144,12 @@ int build_window_tt(sl_ctx *c, int tt) {
   w.tile_slices = tt;
   w.cap_a = (int)std::max<int64_t>(c->sp_wa, 1);
   w.cap_b = (int)std::max<int64_t>(c->sp_wb, 1);
-  // slice block: A indices | A codes | B indices | B codes (16 B aligned)
-  auto al16 = [](uint32_t x) { return (x + 15) / 16 * 16; };
-  w.bl.off_acode = al16((uint32_t)w.cap_a * 64);
-  w.bl.off_b16 = al16(w.bl.off_acode + (uint32_t)w.cap_a * 32);
-  w.bl.off_bcode = al16(w.bl.off_b16 + (uint32_t)w.cap_b * 64);
-  w.bl.slice_bytes = al16(w.bl.off_bcode + (uint32_t)w.cap_b * 32);
+  // slice block: entry words (sl_window.cuh ew_word), the slice's A rows
+  // then its B rows, row pairs interleaved per lane; capacity wa + wb rows
+  // (rounded up to even) of 32 lanes x 4 B
+  const uint32_t cap_rows = (uint32_t)((w.cap_a + w.cap_b + 1) / 2 * 2);
+  w.bl.off_acode = w.bl.off_b16 = w.bl.off_bcode = 0;
+  w.bl.slice_bytes = cap_rows * 128u;
   CK(c->win_rec.ensure(sizeof(TileRec) * n_tiles));
   CK(c->win_dict.ensure(8 * WIN_DMAX * n_tiles));
   CK(c->win_actb.ensure((size_t)WIN_ACTB * n_tiles));
@@ -2250,6 +2249,15 @@ int sl_set_environment(sl_ctx *c, const double *gravity, double drag,
     E.gck[g] = gc_kind[g];
     for (int q = 0; q < 3; q++) E.gcv[g][q] = gc_vec[3 * g + q];
   }
+  auto f32 = [](double x) {  // (float) x, denormals flushed as under -ftz
+    const float f = (float)x;
+    return std::fpclassify(f) == FP_SUBNORMAL ? std::copysign(0.0f, f) : f;
+  };
+  for (int q = 0; q < 3; q++) E.gf[q] = f32(E.g[q]);
+  E.dragf = f32(drag);
+  E.v_stickf = f32(v_stick);
+  for (int p = 0; p < n_planes; p++)
+    for (int q = 0; q < 7; q++) E.plf[p][q] = f32(E.pl[p][q]);
   c->env_set = true;
   return SL_OK;
 }

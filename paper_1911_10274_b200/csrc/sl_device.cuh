@@ -68,7 +68,21 @@ struct EnvP {
   double bl[MAXB][5];
   double gcv[MAXG][3];
   int gck[MAXG];
+  // fp32 copies (rounded once on the host, denormals flushed as the -ftz
+  // fp32 unit would): the per-mass update reads them directly instead of
+  // converting the fp64 parameters for every mass
+  float gf[3], dragf, v_stickf;
+  float plf[MAXP][7];
 };
+// environment parameter in the mass update's arithmetic type
+template <class R>
+__device__ __forceinline__ R env_g(const EnvP &E, int q) {
+  if constexpr (sizeof(R) == 4) return E.gf[q]; else return (R)E.g[q];
+}
+template <class R>
+__device__ __forceinline__ R env_pl(const EnvP &E, int p, int q) {
+  if constexpr (sizeof(R) == 4) return E.plf[p][q]; else return (R)E.pl[p][q];
+}
 
 // Halo of a mass-range partition (config E): the owning
 // rank's step kernel, as it stores an owned boundary mass's new position,
@@ -148,7 +162,7 @@ struct KState {
   // blocks (A / B code rows at win_oac / win_obc) and each tile's zero code
   unsigned char *win_blk;
   const uint8_t *win_zero;
-  uint32_t win_sb, win_oac, win_obc;
+  uint32_t win_sb;  // split-window slice block bytes (entry words)
   int win_tt;
   // multi-step fused groups (sl_fused.cuh; null when not built): material
   // codes [group][rows][maxm], group of every mass, group starts / zero codes
@@ -242,7 +256,7 @@ __device__ __forceinline__ void or_flags(double4 *v, uint32_t f) {
 // ---------------------------------------------------------------------------
 // fp32 mode: compensated positions.  A position is hi + lo, hi the fp32
 // coordinates and lo their rounding residuals, all fp32:
-//   pos[b][i] = (x_hi, y_hi, z_hi, lx)   plo[b][i] = (ly, lz)
+//   pos[b][i] = (x_hi, y_hi, z_hi, lz)   plo[b][i] = (lx, ly)
 // (the mass lives in pmass).  Spring vectors are formed as
 // (o_hi - me_hi) + (o_lo - me_lo): the first difference is exact for
 // neighbouring masses (Sterbenz), so |d| carries ~2^-48 of |x| instead of
@@ -256,7 +270,7 @@ __device__ __forceinline__ typename Tr<P>::L lo_at(
     const typename Tr<P>::R4 &o, const void *plo, int64_t j) {
   if constexpr (P == PREC_FP32) {
     const float2 b = __ldg((const float2 *)plo + j);
-    return make_float3(o.w, b.x, b.y);
+    return make_float3(b.x, b.y, o.w);
   } else {
     return {};
   }
@@ -410,21 +424,22 @@ __device__ __forceinline__ void integrate_vals(
     fy = fy + (R)0.0;
     fz = fz + (R)0.0;
   }
-  fx = fx + mm * (R)E.g[0];
-  fy = fy + mm * (R)E.g[1];
-  fz = fz + mm * (R)E.g[2];
-  const R drag = (R)E.drag;
+  fx = fx + mm * env_g<R>(E, 0);
+  fy = fy + mm * env_g<R>(E, 1);
+  fz = fz + mm * env_g<R>(E, 2);
+  const R drag = sizeof(R) == 4 ? (R)E.dragf : (R)E.drag;
   fx = fx - drag * vx;
   fy = fy - drag * vy;
   fz = fz - drag * vz;
   // contact planes with Coulomb friction on the running force
   for (int p = 0; p < E.np; p++) {
-    const R nx = (R)E.pl[p][0], ny = (R)E.pl[p][1], nz = (R)E.pl[p][2];
-    R depth = (R)E.pl[p][3] - (px * nx + py * ny + pz * nz);
+    const R nx = env_pl<R>(E, p, 0), ny = env_pl<R>(E, p, 1),
+            nz = env_pl<R>(E, p, 2);
+    R depth = env_pl<R>(E, p, 3) - (px * nx + py * ny + pz * nz);
     if constexpr (P == PREC_FP32)
       depth = depth - (lo.x * nx + lo.y * ny + lo.z * nz);
     if (depth > (R)0.0) {
-      const R nmag = (R)E.pl[p][4] * depth;
+      const R nmag = env_pl<R>(E, p, 4) * depth;
       fx += nmag * nx;
       fy += nmag * ny;
       fz += nmag * nz;
@@ -434,18 +449,18 @@ __device__ __forceinline__ void integrate_vals(
       const R fn = fx * nx + fy * ny + fz * nz;
       const R tfx = fx - fn * nx, tfy = fy - fn * ny, tfz = fz - fn * nz;
       const R tf = sqrt(tfx * tfx + tfy * tfy + tfz * tfz);
-      const R vs = (R)E.v_stick;
-      if (tv < vs && tf <= (R)E.pl[p][5] * nmag) {
+      const R vs = sizeof(R) == 4 ? (R)E.v_stickf : (R)E.v_stick;
+      if (tv < vs && tf <= env_pl<R>(E, p, 5) * nmag) {
         fx -= tfx;
         fy -= tfy;
         fz -= tfz;
       } else if (tv >= vs) {
-        const R sc = (R)E.pl[p][6] * nmag / tv;
+        const R sc = env_pl<R>(E, p, 6) * nmag / tv;
         fx -= sc * tvx;
         fy -= sc * tvy;
         fz -= sc * tvz;
       } else if (tf > (R)0.0) {
-        const R sc = (R)E.pl[p][6] * nmag / tf;
+        const R sc = env_pl<R>(E, p, 6) * nmag / tf;
         fx -= sc * tfx;
         fy -= sc * tfy;
         fz -= sc * tfz;
@@ -528,7 +543,7 @@ __device__ __forceinline__ void integrate_vals(
   np4.y = py;
   np4.z = pz;
   if constexpr (P == PREC_FP32)
-    np4.w = nlo.x;  // the record carries lx
+    np4.w = nlo.z;  // the record carries lz
   else
     np4.w = mm;
   nv.x = vx;
@@ -551,7 +566,7 @@ __device__ __forceinline__ void integrate(
   integrate_vals<P>(S, E, T.dt, i, me, lo, mm, v, fl, fx, fy, fz, np4, nlo,
                     nv, ax, ay, az);
   if constexpr (P == PREC_FP32)
-    ((float2 *)S.plo[T.cur ^ 1])[i] = make_float2(nlo.y, nlo.z);
+    ((float2 *)S.plo[T.cur ^ 1])[i] = make_float2(nlo.x, nlo.y);
   if (S.halo) {  // owned boundary mass: its ghost rows at the peers
     const int2 d = __ldg(&S.halo->dst[i]);
     const int dd[2] = {d.x, d.y};
@@ -563,7 +578,7 @@ __device__ __forceinline__ void integrate(
       ((R4 *)S.halo->pos[p][T.cur ^ 1])[row] = np4;
       if constexpr (P == PREC_FP32)
         ((float2 *)S.halo->lo[p][T.cur ^ 1])[row] =
-            make_float2(nlo.y, nlo.z);
+            make_float2(nlo.x, nlo.y);
     }
     if (d.x >= 0) __threadfence_system();
   }
@@ -1258,21 +1273,25 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
       }
     }
     if (S.win_blk) {  // window layout: both entries get the zero code
+      // (entry word: sl_window.cuh ew_word; merged rows A then B)
       const int a = S.sp_a;
+      auto zero_code = [&](int64_t sl, int row, int lane) {
+        uint32_t *wp = (uint32_t *)(S.win_blk + sl * S.win_sb +
+                                    (row >> 1) * 256 + lane * 8 + (row & 1) * 4);
+        *wp = (*wp & ((1u << 26) - 1u)) |
+              ((uint32_t)S.win_zero[sl / S.win_tt] << 26);
+      };
       if (S.e1[s] >= 0) {
         const uint32_t kli = S.sp_ekl[s];
         const int64_t sl = kli >> (a + 5);
-        const int r = (int)((kli >> 5) & ((1u << a) - 1));
-        S.win_blk[sl * S.win_sb + S.win_oac + r * 32 + (kli & 31)] =
-            S.win_zero[sl / S.win_tt];
+        zero_code(sl, (int)((kli >> 5) & ((1u << a) - 1)), (int)(kli & 31));
       }
       if (S.e2[s] >= 0) {
         const int64_t per = (int64_t)S.sp_rows * 32, e = S.e2[s];
         const int64_t sl = e / per;
         const int rem = (int)(e - sl * per);
         const int rb = (rem >> 5) - (1 << a);
-        S.win_blk[sl * S.win_sb + S.win_obc + rb * 32 + (rem & 31)] =
-            S.win_zero[sl / S.win_tt];
+        zero_code(sl, (int)(S.sp_w[sl] & 0xFFFF) + rb, rem & 31);
       }
     }
     return;

@@ -237,7 +237,7 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
     v.x = v.y = v.z = v.w = (R)0;
   }
   sp4[li] = me;
-  sl2[li] = make_float2(ml.y, ml.z);
+  sl2[li] = make_float2(ml.x, ml.y);
   if (li == 0) {
     R4 far;
     far.x = far.y = far.z = (R)SENTINEL_POS;
@@ -301,23 +301,25 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
         v.x = v.y = v.z = (R)0;
         ax = ay = az = (R)0;
       } else {
-        R gx = 0, gy = 0, gz = 0, bx = 0, by = 0, bz = 0;
+        float2 gxy = make_float2(0.f, 0.f), bxy = gxy;
+        R gz = 0, bz = 0;
+        const float2 mlxy = make_float2(ml.x, ml.y);
         const uint32_t *e = sen + t;
         // this mass's own entries only (compacted at build), A and B
         // sections summed separately as the window / split kernels do
 #pragma unroll 4
         for (int q = 0; q < n_a; q++) {
           const uint32_t w = e[q * M];
-          win_body(me, ml, pp[w & 0xFFFFu], pl[w & 0xFFFFu], tab[w >> 16],
-                   gx, gy, gz);
+          win_body(me, mlxy, ml.z, pp[w & 0xFFFFu], pl[w & 0xFFFFu],
+                   tab[w >> 16], gxy, gz);
         }
 #pragma unroll 4
         for (int q = n_a; q < n_ent; q++) {
           const uint32_t w = e[q * M];
-          win_body(me, ml, pp[w & 0xFFFFu], pl[w & 0xFFFFu], tab[w >> 16],
-                   bx, by, bz);
+          win_body(me, mlxy, ml.z, pp[w & 0xFFFFu], pl[w & 0xFFFFu],
+                   tab[w >> 16], bxy, bz);
         }
-        const R fx = f0x + (gx + bx), fy = f0y + (gy + by),
+        const R fx = f0x + (gxy.x + bxy.x), fy = f0y + (gxy.y + bxy.y),
                 fz = f0z + (gz + bz);
         f0x = f0y = f0z = (R)0;
         R4 nv;
@@ -332,7 +334,7 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
       }
     }
     sp4[(b ^ 1) * (M + 1) + li] = np;
-    sl2[(b ^ 1) * (M + 1) + li] = make_float2(ml.y, ml.z);
+    sl2[(b ^ 1) * (M + 1) + li] = make_float2(ml.x, ml.y);
     me = np;
     eff_table(k + 1);  // the other buffer: nobody reads it this step
     __syncthreads();
@@ -344,7 +346,7 @@ static __global__ void __launch_bounds__(M, M <= 512 ? 2 : 1)
   }
   if (!mine) return;
   ((R4 *)S.pos[C.cur ^ 1])[i] = me;
-  ((float2 *)S.plo[C.cur ^ 1])[i] = make_float2(ml.y, ml.z);
+  ((float2 *)S.plo[C.cur ^ 1])[i] = make_float2(ml.x, ml.y);
   R4 vo = v;
   set_flags(vo.w, fl & ~MF_FEXT);
   ((R4 *)C.vel_out)[i] = vo;

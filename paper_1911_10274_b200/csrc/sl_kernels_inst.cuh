@@ -117,8 +117,11 @@ struct SplitLaunch {
   // call f(kernel) for the instantiation of T
   template <class Fn>
   static void win_dispatch(int tt, Fn f) {
-    if constexpr (P == PREC_MIXED) {  // fp64 windows: T = 16 only
-      f(k_win_tma<P, 16>);
+    if constexpr (P == PREC_MIXED) {  // fp64 windows: T = 16 or 12
+      if (tt == 12)
+        f(k_win_tma<P, 12>);
+      else
+        f(k_win_tma<P, 16>);
     } else {
       switch (tt) {
         case 4: f(k_win_tma<P, 4>); return;   // small meshes: more CTAs
