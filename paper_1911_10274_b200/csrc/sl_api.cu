@@ -880,7 +880,10 @@ int ensure_masses(sl_ctx *c, int64_t m_n) {
       CK(cudaMemsetAsync(c->plo[b].p, 0, 8 * (m_n + 32), c->st));
       CK(c->pmass.ensure(4 * (m_n + 32)));
     }
-  CK(c->vel.ensure(r4 * m_n));
+  // padded to whole slices (+32): the window kernels bulk-copy whole slices
+  // of velocity records; the padding reads as dead masses (flags 0)
+  CK(c->vel.ensure(r4 * (m_n + 32)));
+  CK(cudaMemsetAsync((char *)c->vel.p + r4 * m_n, 0, r4 * 32, c->st));
   CK(c->acc.ensure(3 * c->rsz * m_n));
   CK(c->fext.ensure(r4 * m_n));
   CK(c->load.ensure(3 * c->rsz * m_n));
@@ -1192,6 +1195,17 @@ int build_window_tt(sl_ctx *c, int tt) {
   w.off_slice = (win_end + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
   const int64_t bar = 8 * 2 * WIN_MAXST + 8 * WIN_MAXST * WIN_DMAX;
+  // stage the tile's velocities with the windows when 2 stages still fit
+  // (SL_WIN_VSTAGE=0: keep the consumers' register prefetch)
+  {
+    const uint32_t vb = (uint32_t)(32 * 4 * c->rsz) * (uint32_t)tt;
+    const char *ev = getenv("SL_WIN_VSTAGE");
+    const bool want = ev ? atoi(ev) != 0 : c->prec == PREC_MIXED;
+    if (want && ((int64_t)c->smem_optin - bar) / (w.stage_bytes + vb) >= 2) {
+      w.off_vel = w.stage_bytes;
+      w.stage_bytes += vb;
+    }
+  }
   int nst = (int)std::min<int64_t>(
       WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
   if (const char *ev = getenv("SL_WIN_STAGES"))  // tuning override
@@ -1270,6 +1284,10 @@ int build_window_exact(sl_ctx *c) {
   w.off_slice = (w.off_win + 32 * w.cap_rec + 127) / 128 * 128;
   w.stage_bytes = w.off_slice + (uint32_t)tt * w.bl.slice_bytes;
   const int64_t bar = 8 * 2 * WIN_MAXST + 16 * WIN_MAXST * WIN_DMAX;
+  // the tile's velocities staged by the producer (frees the consumers'
+  // register prefetch, which spilled at 128 registers) when 2 stages fit
+  w.off_vel = w.stage_bytes;  // (the fp64 kernel always stages them)
+  w.stage_bytes += 32 * 32 * tt;
   int nst = (int)std::min<int64_t>(
       WIN_MAXST, ((int64_t)c->smem_optin - bar) / w.stage_bytes);
   if (nst < 2) return SL_OK;
@@ -1418,6 +1436,8 @@ int run_fused(sl_ctx *c, const KState &S, int64_t n, const double *times,
   CK(cudaMemcpyAsync(c->fz_times.p, times, 8 * n, cudaMemcpyHostToDevice,
                      c->st));
   CK(c->vel2.ensure(c->vel.bytes));
+  CK(cudaMemsetAsync((char *)c->vel2.p + 16 * c->m_n, 0, 16 * 32,
+                     c->st));  // the padding records (window bulk copies)
   FzCfg f = c->fcfg;
   f.vel_out = c->vel2.p;
   f.times = c->fz_times.as<double>();
