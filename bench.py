@@ -542,7 +542,10 @@ def main():
             import torch
             wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
         h2d = m * 48 if not full else m * (5 * 24 + 8 + 1 + 1 + 8)
-        d2h = m * 4 * 24
+        # the pause moves the snapshot's positions / velocities; the store's
+        # state columns stay on the device until the host reads them
+        # (engine._DeferredPull) -- nothing reads them in this segment
+        d2h = m * 2 * 24
         e2e = {"value": world * springs * k / wall, "unit": unit,
                "h2d_bytes_per_step": h2d / k, "d2h_bytes_per_step": d2h / k,
                "wall_s": wall, "api": "io.apply_snapshot + SimController."

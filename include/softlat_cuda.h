@@ -221,6 +221,13 @@ int sl_mass_pass(sl_ctx *ctx, double dt, int64_t *err_slot);
  * the host touched travel (engine.DeviceMirror.push). */
 int sl_write_state(sl_ctx *ctx, int64_t m_n, const double *pos,
                    const double *vel, const double *acc);
+/* The same, returning once the copies and the conversion are enqueued on
+ * the context's stream: the host arrays (page-locked for a true overlap)
+ * must stay unchanged until sl_sync(ctx) returns.  io.apply_snapshot's
+ * write-through: the upload runs while the host copies the same columns
+ * into the store. */
+int sl_write_state_async(sl_ctx *ctx, int64_t m_n, const double *pos,
+                         const double *vel, const double *acc);
 
 /* Opt-in spring damping (north_star "Hooke plus damping"): damping[s] =
  * c >= 0 (N s / m) for every spring slot [0, s_n); the force on m1 gains
@@ -235,6 +242,25 @@ int sl_set_spring_damping(sl_ctx *ctx, int64_t n, const double *damping);
 /* Copy mass state back into host arrays double[m_n][3]; NULL skips. */
 int sl_download_masses(sl_ctx *ctx, double *pos, double *vel, double *acc,
                        double *fext);
+/* The pause-time pull of engine.DeviceMirror.pull (control.py pause):
+ * like sl_download_state, plus optional EXTRA page-locked destinations
+ * pos2 / vel2 (a snapshot's own buffers) copied first.  wait_head = 0
+ * returns as soon as everything is enqueued: sl_download_wait_extra waits
+ * for pos2 / vel2, sl_download_wait for all of it (the host store settles
+ * on first access).  The destinations must stay allocated until then. */
+int sl_download_state_ex(sl_ctx *ctx, double *pos, double *vel, double *acc,
+                         double *fext, double *pos2, double *vel2,
+                         int wait_head);
+int sl_download_wait_extra(sl_ctx *ctx);
+/* Stash the current mass state (positions, velocities, accelerations,
+ * f_ext as fp64) in a device buffer, enqueued on the context stream -- the
+ * next run's step kernels do not wait for anything.  sl_download_stash
+ * copies (parts of) the stash into host arrays on the side stream and
+ * waits for them: the host store's lock-time state, fetched only when a
+ * reader needs it (ObjectStore.lock_for_run). */
+int sl_stash_state(sl_ctx *ctx);
+int sl_download_stash(sl_ctx *ctx, double *pos, double *vel, double *acc,
+                      double *fext);
 /* As sl_download_masses, but returns once pos / vel have landed: acc and
  * f_ext (which must be page-locked) keep arriving on the context stream;
  * sl_download_wait blocks until they have.  Work enqueued afterwards is

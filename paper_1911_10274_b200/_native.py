@@ -41,7 +41,10 @@ EXPORTS = (
     "sl_host_masked_extrema", "sl_set_spring_damping", "sl_halo_init",
     "sl_halo_local", "sl_halo_ipc_handles", "sl_halo_ipc_open",
     "sl_halo_set_peer", "sl_halo_commit", "sl_write_state",
-    "sl_host_is_iota", "sl_download_state", "sl_download_wait")
+    "sl_write_state_async",
+    "sl_host_is_iota", "sl_download_state", "sl_download_wait",
+    "sl_download_state_ex", "sl_download_wait_extra",
+    "sl_stash_state", "sl_download_stash")
 
 
 class SlStats(C.Structure):
@@ -111,9 +114,14 @@ def load_library(path: str = LIB_PATH):
             "sl_halo_set_peer": ([P, I, P, I], I),
             "sl_halo_commit": ([P], I),
             "sl_write_state": ([P, I64, P, P, P], I),
+            "sl_write_state_async": ([P, I64, P, P, P], I),
             "sl_host_is_iota": ([P, I64, I, P], I),
             "sl_download_state": ([P, P, P, P, P], I),
             "sl_download_wait": ([P], I),
+            "sl_download_state_ex": ([P, P, P, P, P, P, P, C.c_int], I),
+            "sl_download_wait_extra": ([P], I),
+            "sl_stash_state": ([P], I),
+            "sl_download_stash": ([P, P, P, P, P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -259,8 +267,13 @@ def host_touch(a: np.ndarray) -> None:
 
 def is_pinned(a: np.ndarray) -> bool:
     base = a
-    while isinstance(base, np.ndarray) and base.base is not None:
-        base = base.base
+    while True:
+        if isinstance(base, np.ndarray) and base.base is not None:
+            base = base.base
+        elif isinstance(getattr(base, "_raw", None), np.ndarray):
+            base = base._raw  # an owner object (control._Lease)
+        else:
+            break
     return isinstance(base, _PinnedBlock)
 
 
@@ -333,6 +346,21 @@ class Context:
         self._check(self.lib.sl_write_state(
             self.h, self.m_n, *[_ptr(a) if a is not None else None
                                 for a in cols]), "sl_write_state")
+
+    def write_state_async(self, pos=None, vel=None, acc=None):
+        """sl_write_state_async: enqueued only; the arrays (contiguous fp64,
+        page-locked) must stay unchanged until sync()."""
+        for a in (pos, vel, acc):
+            if a is not None and not (isinstance(a, np.ndarray) and
+                                      a.dtype == np.float64 and
+                                      a.flags.c_contiguous and
+                                      a.size == 3 * self.m_n):
+                raise InvalidValueError("write_state_async: pass contiguous "
+                                        "float64 (m, 3) arrays")
+        self._check(self.lib.sl_write_state_async(
+            self.h, self.m_n, *[_ptr(a) if a is not None else None
+                                for a in (pos, vel, acc)]),
+            "sl_write_state_async")
 
     def upload_springs(self, m1, m2, m1gen, m2gen, rest, k, diam, yld, mode,
                        amp, freq, off, per, alive, degen):
@@ -596,6 +624,41 @@ class Context:
         self._check(self.lib.sl_download_state(
             self.h, *[_ptr(a) if a is not None else None
                       for a in (pos, vel, acc, fext)]), "sl_download_state")
+
+    def download_state_ex(self, pos, vel, acc, fext, pos2=None, vel2=None,
+                          wait_head=False):
+        """sl_download_state_ex: every destination page-locked and kept
+        alive by the caller until download_wait() (pos2 / vel2:
+        download_wait_extra())."""
+        for a in (pos, vel, acc, fext, pos2, vel2):
+            if a is not None and not (a.dtype == np.float64 and
+                                      a.flags.c_contiguous and
+                                      a.size == 3 * self.m_n):
+                raise InvalidValueError("download_state_ex: contiguous "
+                                        "float64 (m, 3) arrays")
+        self._check(self.lib.sl_download_state_ex(
+            self.h, *[_ptr(a) if a is not None else None
+                      for a in (pos, vel, acc, fext, pos2, vel2)],
+            1 if wait_head else 0), "sl_download_state_ex")
+
+    def stash_state(self):
+        self._check(self.lib.sl_stash_state(self.h), "sl_stash_state")
+
+    def download_stash(self, pos=None, vel=None, acc=None, fext=None):
+        """Stashed state (sl_stash_state) into host arrays; waits."""
+        for a in (pos, vel, acc, fext):
+            if a is not None and not (a.dtype == np.float64 and
+                                      a.flags.c_contiguous and
+                                      a.size == 3 * self.m_n):
+                raise InvalidValueError("download_stash: contiguous "
+                                        "float64 (m, 3) arrays")
+        self._check(self.lib.sl_download_stash(
+            self.h, *[_ptr(a) if a is not None else None
+                      for a in (pos, vel, acc, fext)]), "sl_download_stash")
+
+    def download_wait_extra(self):
+        self._check(self.lib.sl_download_wait_extra(self.h),
+                    "sl_download_wait_extra")
 
     def download_wait(self):
         self._check(self.lib.sl_download_wait(self.h), "sl_download_wait")

@@ -82,6 +82,10 @@ struct sl_ctx {
   // k0 / k1 bracket the step kernels of the last sl_step call
   cudaEvent_t k0 = nullptr, k1 = nullptr;
   cudaEvent_t head_ev = nullptr, tail_ev = nullptr;  // sl_download_state
+  cudaEvent_t extra_ev = nullptr;  // sl_download_state_ex: extra copies
+  // sl_download_state_side: unpacked on the stream, copied on c->side
+  cudaEvent_t side_ev = nullptr, side_done = nullptr;
+  bool side_pending = false, stash_set = false;
   bool tail_pending = false;
   bool k_valid = false;
   cudaEvent_t t0 = nullptr, t1 = nullptr, snap_ev = nullptr,
@@ -158,6 +162,7 @@ struct sl_ctx {
   bool khost_valid = false;
   // scratch
   DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
+  DevBuf stage2;  // sl_stash_state: the fp64 state at the last stash
   DevBuf status;
   unsigned long long *h_status = nullptr;
   DevBuf snap_dev;
@@ -1780,6 +1785,12 @@ int sl_create(int device, int precision, sl_ctx **out) {
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->tail_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->extra_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->side_done, cudaEventDisableTiming);
+  if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming);
@@ -1826,7 +1837,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
                     &c->fz_gid, &c->diag, &c->fz_perm, &c->fz_cnt,
                     &c->fz_epos, &c->fz_cnt_a,
-                    &c->win_fail};
+                    &c->win_fail, &c->stage2};
   for (void *p : c->halo_ipc) cudaIpcCloseMemHandle(p);
   c->halo_desc.release();
   c->halo_dst.release();
@@ -1840,6 +1851,9 @@ int sl_destroy(sl_ctx *c) {
   if (c->k1) cudaEventDestroy(c->k1);
   if (c->head_ev) cudaEventDestroy(c->head_ev);
   if (c->tail_ev) cudaEventDestroy(c->tail_ev);
+  if (c->extra_ev) cudaEventDestroy(c->extra_ev);
+  if (c->side_ev) cudaEventDestroy(c->side_ev);
+  if (c->side_done) cudaEventDestroy(c->side_done);
   if (c->snap_ev) cudaEventDestroy(c->snap_ev);
   if (c->snap_done) cudaEventDestroy(c->snap_done);
   if (c->st) cudaStreamDestroy(c->st);
@@ -1879,7 +1893,7 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
                           &c->ent_s, &c->e1, &c->e2, &c->stage, &c->sort_tmp,
                           &c->keys[0], &c->keys[1], &c->vals[0], &c->vals[1],
                           &c->deg, &c->width, &c->sp_j, &c->sp_kl, &c->sp_s,
-                          &c->sp_w, &c->sp_ekl, &c->degB};
+                          &c->sp_w, &c->sp_ekl, &c->degB, &c->stage2};
   for (const DevBuf *b : bufs) o->device_bytes += (int64_t)b->bytes;
   if (c->springs_set) {
     std::vector<uint8_t> al(c->s_n);
@@ -2162,8 +2176,18 @@ int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
   return SL_OK;
 }
 
+static int write_state_impl(sl_ctx *c, int64_t m_n, const double *pos,
+                            const double *vel, const double *acc, bool wait);
 int sl_write_state(sl_ctx *c, int64_t m_n, const double *pos,
                    const double *vel, const double *acc) {
+  return write_state_impl(c, m_n, pos, vel, acc, true);
+}
+int sl_write_state_async(sl_ctx *c, int64_t m_n, const double *pos,
+                         const double *vel, const double *acc) {
+  return write_state_impl(c, m_n, pos, vel, acc, false);
+}
+static int write_state_impl(sl_ctx *c, int64_t m_n, const double *pos,
+                            const double *vel, const double *acc, bool wait) {
   if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
   if (m_n != c->m_n)
     return fail(c, SL_EINVAL, "sl_write_state: %lld masses, context has %lld",
@@ -2187,7 +2211,9 @@ int sl_write_state(sl_ctx *c, int64_t m_n, const double *pos,
                                         c->vel.p, c->acc.p);
   CKL();
   c->launches++;
-  CK(cudaStreamSynchronize(c->st));  // staging is reused by the next call
+  // staging is reused by the next call (which is stream-ordered after this
+  // one); the synchronous form also releases the caller's host arrays
+  if (wait) CK(cudaStreamSynchronize(c->st));
   return SL_OK;
 }
 
@@ -2668,6 +2694,98 @@ int sl_download_state(sl_ctx *c, double *pos, double *vel, double *acc,
   CK(cudaEventRecord(c->tail_ev, c->st));
   c->tail_pending = acc || fext;
   CK(cudaEventSynchronize(c->head_ev));  // positions / velocities landed
+  return SL_OK;
+}
+
+int sl_download_state_ex(sl_ctx *c, double *pos, double *vel, double *acc,
+                         double *fext, double *pos2, double *vel2,
+                         int wait_head) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  const int64_t m = c->m_n;
+  if (m == 0) return SL_OK;
+  if (c->tail_pending) CK(cudaEventSynchronize(c->tail_ev));
+  c->tail_pending = false;
+  CK(cudaSetDevice(c->device));
+  size_t vb = align256(24 * m);
+  CK(c->stage.ensure(4 * vb));
+  const bool want_p = pos || pos2, want_v = vel || vel2;
+  double *dp = want_p ? (double *)c->stage.p : nullptr;
+  double *dv = want_v ? (double *)((char *)c->stage.p + vb) : nullptr;
+  double *da = acc ? (double *)((char *)c->stage.p + 2 * vb) : nullptr;
+  double *df = fext ? (double *)((char *)c->stage.p + 3 * vb) : nullptr;
+  auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                  : k_unpack_masses<PREC_MIXED>;
+  k<<<blocks_for(m), 256, 0, c->st>>>(m, c->pos[c->cur].p,
+                                      c->plo[c->cur].p, c->vel.p, c->acc.p,
+                                      c->fext.p, dp, dv, da, df);
+  CKL();
+  c->launches++;
+  // the extra destinations first (a snapshot waits for them alone), then
+  // the primary positions / velocities, then accelerations and f_ext
+  if (pos2) CK(cudaMemcpyAsync(pos2, dp, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (vel2) CK(cudaMemcpyAsync(vel2, dv, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->extra_ev, c->st));
+  if (pos) CK(cudaMemcpyAsync(pos, dp, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (vel) CK(cudaMemcpyAsync(vel, dv, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->head_ev, c->st));
+  if (acc) CK(cudaMemcpyAsync(acc, da, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  if (fext)
+    CK(cudaMemcpyAsync(fext, df, 24 * m, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaEventRecord(c->tail_ev, c->st));
+  c->tail_pending = true;
+  if (wait_head) CK(cudaEventSynchronize(c->head_ev));
+  return SL_OK;
+}
+
+int sl_stash_state(sl_ctx *c) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  const int64_t m = c->m_n;
+  if (m == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  const size_t vb = align256(24 * m);
+  // a previous stash may still be read by sl_download_stash (side stream)
+  if (c->side_pending) CK(cudaEventSynchronize(c->side_done));
+  c->side_pending = false;
+  CK(c->stage2.ensure(4 * vb));
+  char *b = (char *)c->stage2.p;
+  auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                  : k_unpack_masses<PREC_MIXED>;
+  k<<<blocks_for(m), 256, 0, c->st>>>(
+      m, c->pos[c->cur].p, c->plo[c->cur].p, c->vel.p, c->acc.p, c->fext.p,
+      (double *)b, (double *)(b + vb), (double *)(b + 2 * vb),
+      (double *)(b + 3 * vb));
+  CKL();
+  c->launches++;
+  CK(cudaEventRecord(c->side_ev, c->st));
+  c->stash_set = true;
+  return SL_OK;
+}
+
+int sl_download_stash(sl_ctx *c, double *pos, double *vel, double *acc,
+                      double *fext) {
+  if (!c || !c->stash_set) return fail(c, SL_ESTATE, "no stashed state");
+  const int64_t m = c->m_n;
+  if (m == 0) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  const size_t vb = align256(24 * m);
+  const char *b = (const char *)c->stage2.p;
+  CK(cudaStreamWaitEvent(c->side, c->side_ev, 0));
+  double *dst[4] = {pos, vel, acc, fext};
+  for (int q = 0; q < 4; q++)
+    if (dst[q])
+      CK(cudaMemcpyAsync(dst[q], b + q * vb, 24 * m, cudaMemcpyDeviceToHost,
+                         c->side));
+  CK(cudaEventRecord(c->side_done, c->side));
+  CK(cudaEventSynchronize(c->side_done));
+  return SL_OK;
+}
+
+int sl_download_wait_extra(sl_ctx *c) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(c->extra_ev));
   return SL_OK;
 }
 

@@ -268,7 +268,7 @@ extern "C" int sl_host_copy(void *dst, const void *src, size_t bytes,
   if (bytes && (!dst || !src)) return SL_EINVAL;
   unsigned char *d = (unsigned char *)dst;
   const unsigned char *s = (const unsigned char *)src;
-  parallel_for((int64_t)bytes, threads, (int64_t)4 << 20,
+  parallel_for((int64_t)bytes, threads, (int64_t)1 << 20,
                [&](int64_t lo, int64_t hi) {
                  std::memcpy(d + lo, s + lo, (size_t)(hi - lo));
                });

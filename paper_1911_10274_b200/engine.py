@@ -92,6 +92,41 @@ class StepConfig:
 
 
 # ----------------------------------------------------------- device mirror
+_STATE_NAMES = ("_m_pos", "_m_vel", "_m_acc", "_m_fext")
+
+
+class _DeferredPull:
+    """State columns of a store that only a device holds (after a controller
+    pause, or after io.apply_snapshot wrote them straight to the device):
+    ``cols`` maps column name -> the store's array.  run() copies them in
+    now; stash() -- before the device state changes (lock_for_run) -- keeps
+    a device-side copy and returns the pull that reads from it."""
+
+    def __init__(self, ctx, cols: dict, stashed: bool = False):
+        self.ctx, self.cols, self.stashed = ctx, dict(cols), stashed
+
+    def _args(self):
+        return [self.cols.get(n) for n in _STATE_NAMES]
+
+    def run(self):
+        if not self.ctx.h:
+            return
+        if self.stashed:
+            self.ctx.download_stash(*self._args())
+        else:
+            self.ctx.download_masses(*self._args())
+
+    def stash(self) -> "_DeferredPull":
+        if self.stashed or not self.ctx.h:
+            return self
+        self.ctx.stash_state()
+        return _DeferredPull(self.ctx, self.cols, stashed=True)
+
+    def without(self, names) -> "_DeferredPull | None":
+        rest = {k: v for k, v in self.cols.items() if k not in names}
+        return _DeferredPull(self.ctx, rest, self.stashed) if rest else None
+
+
 class DeviceMirror:
     """The device-resident copy of one store (the analogue of the reference's
     per-store engine cache, engine.py:71-102), keyed on the store's version
@@ -116,7 +151,7 @@ class DeviceMirror:
     def push(self, store: ObjectStore, env: Environment | None,
              masses: bool = True):
         raw = store._raw
-        if not _native.is_pinned(raw("_m_pos")):
+        if not _native.is_pinned(store.__dict__["_c_m_pos"]):
             # page-locked mass columns: uploads / pulls at copy-engine speed
             store.adopt_mass_allocator(_native.pinned_empty)
         m, s = store.mass_slot_count, store.spring_slot_count
@@ -124,8 +159,9 @@ class DeviceMirror:
         if masses or self.ctx.m_n != m:
             # the device holds the host state when nothing but this mirror
             # moved it since the last sync (same arrays, no steps since);
-            # then only the columns the host touched travel
-            key = (m, id(raw("_m_pos")))
+            # then only the columns the host touched travel (raw() -- which
+            # waits for copies still landing -- only for columns sent)
+            key = (m, store._column_id("_m_pos"))
             synced = (self._mass_key == key and self.ctx.m_n == m and
                       self._mass_epoch == self.ctx.epoch)
             if not synced or touched - self._STATE_COLS:
@@ -165,7 +201,7 @@ class DeviceMirror:
             self.ctx.set_spring_damping(store._s_damp[:s])
             self._damp_key = key
             self._damp_sent = True
-        ckey = (m, store.constraint_version, id(store._m_pos))
+        ckey = (m, store.constraint_version, store._column_id("_m_pos"))
         if ckey != self._constraints_key or masses:
             # the CSR is rebuilt only when the constraints change; a mass
             # upload re-sends the cached one
@@ -174,6 +210,13 @@ class DeviceMirror:
             self.ctx.set_local_constraints(*self._lc_csr)
             self._constraints_key = ckey
         self.set_env(store, env or Environment())
+
+    def in_sync(self, store: ObjectStore) -> bool:
+        """The device holds the host's mass state (same arrays, no device
+        steps since the last sync): only host-touched columns differ."""
+        m = store.mass_slot_count
+        return (self._mass_key == (m, store._column_id("_m_pos")) and
+                self.ctx.m_n == m and self._mass_epoch == self.ctx.epoch)
 
     def _replay_springs(self, store: ObjectStore, key) -> bool:
         """O(edits) spring sync: replay the store's spring journal since the
@@ -237,10 +280,39 @@ class DeviceMirror:
 
     # device -> host
     def pull(self, store: ObjectStore, springs: bool = True,
-             acc: bool = True, fext: bool = True):
+             acc: bool = True, fext: bool = True, extra=None) -> bool:
+        """Device state into the host store.  ``extra`` = (positions,
+        velocities) page-locked (m, 3) buffers (a snapshot's): when given,
+        the pull only enqueues -- the extra buffers first, then every store
+        column -- and returns True; the store settles on first access and
+        the caller waits ctx.download_wait_extra() for the extra buffers."""
         store.materialize_sync()
         m, s = store.mass_slot_count, store.spring_slot_count
         raw = store._raw
+        d = store.__dict__
+        if extra is not None and m and all(_native.is_pinned(a) for a in (
+                *(d["_c" + n] for n in _STATE_NAMES), *extra)):
+            # only the extra buffers travel now; the store's state columns
+            # stay on the device until the host first needs them
+            # (store._settle runs the deferred pull; io.apply_snapshot,
+            # rewriting positions / velocities, leaves them there)
+            store._drop_deferred()
+            cols = {n: d["_c" + n][:m] for n in _STATE_NAMES}
+            key = (m, store._column_id("_m_pos"))
+            self.ctx.download_state_ex(None, None, None, None,
+                                       extra[0], extra[1])
+            store._defer_state_columns(_DeferredPull(self.ctx, cols))
+            # host == device (deferred): earlier touches are moot
+            d["_touched"].difference_update(_STATE_NAMES)
+            self._mass_key = key
+            self._mass_epoch = self.ctx.epoch
+            if springs and s:
+                self.ctx.download_springs(store._s_alive[:s].view(np.uint8),
+                                          store._s_degen[:s].view(np.uint8))
+                store._deaths_maybe = True
+            return True
+        if acc and fext:
+            store._drop_deferred()  # every state column is rewritten below
         if acc and fext and _native.is_pinned(raw("_m_acc")) and \
                 _native.is_pinned(raw("_m_fext")):
             # positions / velocities now; accelerations and f_ext keep
@@ -256,12 +328,13 @@ class DeviceMirror:
                                      raw("_m_acc")[:m] if acc else None,
                                      raw("_m_fext")[:m] if fext else None)
         if acc and fext:  # host == device again
-            self._mass_key = (m, id(raw("_m_pos")))
+            self._mass_key = (m, store._column_id("_m_pos"))
             self._mass_epoch = self.ctx.epoch
         if springs and s:
             self.ctx.download_springs(store._s_alive[:s].view(np.uint8),
                                       store._s_degen[:s].view(np.uint8))
             store._deaths_maybe = True
+        return False
 
     def log_degenerate(self, store: ObjectStore):
         """engine._log_degenerate (engine.py:205-215)."""
@@ -294,8 +367,59 @@ def mirror_for(store: ObjectStore, cfg: StepConfig) -> DeviceMirror:
     return mir
 
 
+def write_through_begin(store: ObjectStore, pos: np.ndarray,
+                        vel: np.ndarray) -> list:
+    """Start uploading whole position / velocity columns (page-locked,
+    (m, 3) fp64) to every mirror of a paused store that holds the rest of
+    its state, while the caller copies the same columns into the store
+    (io.apply_snapshot).  Returns the mirrors to pass to
+    write_through_end."""
+    per = _mirrors.get(store)
+    if not per or store._locked:
+        return []
+    if not (_native.is_pinned(pos) and _native.is_pinned(vel)):
+        return []
+    started = []
+    for mir in per.values():
+        if mir.in_sync(store):
+            mir.ctx.write_state_async(pos, vel, None)
+            started.append(mir)
+    return started
+
+
+def write_through_covers(store: ObjectStore, started: list) -> bool:
+    """Every mirror of the store took the write-through."""
+    return bool(started) and len(started) == len(_mirrors.get(store) or {})
+
+
+def write_through_end(store: ObjectStore, started: list,
+                      host_copied: bool = True) -> None:
+    """Wait for write_through_begin's uploads (the caller's arrays are free
+    again).  With the host copy done, positions / velocities no longer count
+    as host-touched; without it (host_copied False, every mirror covered)
+    the store columns are deferred to the first mirror's device copy."""
+    for mir in started:
+        mir.ctx.sync()
+    if not write_through_covers(store, started):
+        return
+    touched = store.__dict__["_touched"]
+    touched.discard("_m_pos")
+    touched.discard("_m_vel")
+    if not host_copied:
+        # positions / velocities plus whatever the store still deferred
+        # (the device holds all of it)
+        m = store.mass_slot_count
+        d = store.__dict__
+        names = {"_m_pos", "_m_vel", *store._deferred_columns()}
+        store._defer_state_columns(_DeferredPull(
+            started[0].ctx, {n: d["_c" + n][:m] for n in names}))
+
+
 def drop_mirrors(store: ObjectStore):
     """Release the device buffers held for ``store``."""
+    if per := _mirrors.get(store):
+        if not store._locked:
+            store._settle()  # state still only on a device comes home first
     per = _mirrors.pop(store, None)
     for mir in (per or {}).values():
         mir.ctx.close()

@@ -117,11 +117,24 @@ def apply_snapshot(store: ObjectStore, ids: np.ndarray, positions: np.ndarray,
     if len(ids) == n and store.mass_count == n and len(ids) and \
             ids[0] == 0 and ids[-1] == n - 1 and _native.host_is_iota(ids):
         # every slot, in order: whole-column copies (threaded, into the
-        # page-locked store columns)
-        _native.host_copy_into(store._m_pos[:n], np.ascontiguousarray(
-            positions, np.float64).reshape(n, 3))
-        _native.host_copy_into(store._m_vel[:n], np.ascontiguousarray(
-            velocities, np.float64).reshape(n, 3))
+        # page-locked store columns); a device mirror holding the rest of
+        # the state receives the same columns meanwhile, straight from
+        # page-locked inputs (engine.write_through_begin)
+        from . import engine
+        pos = np.ascontiguousarray(positions, np.float64).reshape(n, 3)
+        vel = np.ascontiguousarray(velocities, np.float64).reshape(n, 3)
+        started = engine.write_through_begin(store, pos, vel)
+        # every device copy took the columns: the store's own copy is
+        # deferred (filled from the device on first host need) instead of
+        # paying a host memory copy now
+        copy = not engine.write_through_covers(store, started)
+        try:
+            if copy:
+                dst_pos, dst_vel = store._overwrite_state_columns()
+                _native.host_copy_into(dst_pos[:n], pos)
+                _native.host_copy_into(dst_vel[:n], vel)
+        finally:
+            engine.write_through_end(store, started, host_copied=copy)
         return
     if np.any(ids < 0) or np.any(ids >= n) or not np.all(store._m_alive[ids]):
         raise ScenarioError("snapshot ids do not match alive store slots")

@@ -328,3 +328,68 @@ def test_pinned_mass_columns_and_lock_time_reads():
         st.create_mass(Mass(pos=Vec3(0, 0, 1), m=1.0))
     assert _native.is_pinned(st._m_pos) and st.mass_is_live(grown)
     ctl.stop()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_apply_snapshot_write_through_matches_full_push(pinned):
+    """io.apply_snapshot on a paused controller uploads page-locked
+    positions / velocities straight to the device while copying them into
+    the store (engine.write_through_begin); the next segment must be bit
+    for bit the one a fresh upload of the same state runs."""
+    from paper_1911_10274_b200 import _native, engine
+    from paper_1911_10274_b200 import io as sio
+    ctl, st, _ = controller(n=4, stretch=1.02)
+    ctl.start(10 * 1e-4)
+    ctl.wait_for_event(timeout=120)
+    snap = ctl.snapshot()
+    rng = np.random.default_rng(3)
+    pos = snap.positions + rng.normal(0, 1e-4, snap.positions.shape)
+    vel = snap.velocities + rng.normal(0, 1e-2, snap.velocities.shape)
+    if pinned:
+        p2, v2 = _native.pinned_empty(pos.shape, np.float64), \
+            _native.pinned_empty(vel.shape, np.float64)
+        p2[...] = pos
+        v2[...] = vel
+        pos, vel = p2, v2
+    mir = engine.mirror_for(st, ctl._cfg)
+    full0 = getattr(mir, "full_pushes", 0)
+    sio.apply_snapshot(st, snap.ids, pos, vel)
+    if pinned:  # the device already has them: nothing left to send
+        assert "_m_pos" not in st.__dict__["_touched"]
+    ctl.start(10 * 1e-4)
+    ctl.wait_for_event(timeout=120)
+    got = ctl.snapshot()
+    assert getattr(mir, "full_pushes", 0) == full0
+    ctl.stop()
+    # the same state through a fresh store / context
+    st2, _ = make_lattice(4, stretch=1.02)
+    n = st2.mass_slot_count
+    st2._m_pos[:n] = np.asarray(pos)
+    st2._m_vel[:n] = np.asarray(vel)
+    ref = SimController(st2, free_env(), StepConfig(dt=1e-4))
+    ref.start(10 * 1e-4)
+    ref.wait_for_event(timeout=120)
+    want = ref.snapshot()
+    ref.stop()
+    assert got.positions.tobytes() == want.positions.tobytes()
+    assert got.velocities.tobytes() == want.velocities.tobytes()
+
+
+@pytest.mark.parametrize("touch", [False, True])
+def test_pause_pull_fills_snapshot_arena(touch):
+    """A pause enqueues the state pull and returns; the next snapshot's
+    page-locked arena is filled first (control._pull(pause=True)).  The
+    snapshot must equal the store's state, and a host write to the store
+    between the pause and the snapshot must show up in it."""
+    ctl, st, _ = controller(n=42, stretch=1.01)   # > 65536 masses: arena
+    for _ in range(3):
+        ctl.start(5 * 1e-4)
+        ctl.wait_for_event(timeout=120)
+        if touch:
+            st._m_pos[7] += 1e-3
+        snap = ctl.snapshot()
+        n = st.mass_slot_count
+        assert snap.positions.tobytes() == st._m_pos[:n].tobytes()
+        assert snap.velocities.tobytes() == st._m_vel[:n].tobytes()
+        assert np.array_equal(snap.ids, np.arange(n))
+    ctl.stop()
