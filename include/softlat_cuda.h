@@ -77,6 +77,9 @@ typedef struct sl_stats {
   int32_t win_tile_slices; /* window kernel: slices per tile = consumer
                               warps (the k_win_tma<P, T> instantiation)   */
   int32_t win_stages;      /* window kernel: tile stages in the ring      */
+  int64_t inplace_edits;   /* spring record writes applied to the live
+                              layout in place (sl_write_springs: O(edits),
+                              no re-index)                                 */
 } sl_stats;
 
 /* sl_stats.step_path */

@@ -56,7 +56,8 @@ class SlStats(C.Structure):
                 ("step_path", C.c_int32), ("split_batch", C.c_int32),
                 ("fused_groups", C.c_int64), ("fused_launches", C.c_int64),
                 ("fused_aborts", C.c_int64),
-                ("win_tile_slices", C.c_int32), ("win_stages", C.c_int32)]
+                ("win_tile_slices", C.c_int32), ("win_stages", C.c_int32),
+                ("inplace_edits", C.c_int64)]
 
 STEP_PATHS = {0: "none", 1: "k_gather_step", 2: "k_gather_tma",
               3: "k_split_step", 4: "k_split_tma", 5: "k_win_tma",

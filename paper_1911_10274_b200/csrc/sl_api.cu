@@ -163,6 +163,8 @@ struct sl_ctx {
   // scratch
   DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
   DevBuf stage2;  // sl_stash_state: the fp64 state at the last stash
+  DevBuf inc_buf;  // insert_incremental: slots, touched tiles, fail flag
+  int64_t inc_edits = 0;  // record writes applied in place
   DevBuf status;
   unsigned long long *h_status = nullptr;
   DevBuf snap_dev;
@@ -780,6 +782,142 @@ __global__ void k_split_fill(int64_t n, const uint32_t *keys,
   if (special) {
     S.xflags[owner] = 1;
     or_flags((typename Tr<P>::R4 *)S.vel + owner, MF_SPECIAL);
+  }
+}
+
+// O(edits) topology sync on a live split layout (sl_split.cuh): the
+// written slots (created, re-used or re-wired springs -- DeviceMirror's
+// journal replay) get their A / B cells in place, from the free rows of
+// their endpoints' lanes (the device-side free list: a dead or padding cell
+// is sent / nul), instead of a full re-index.  One warp, slots in order; a
+// lane probes one row.  Cells of the slot's previous wiring are released;
+// a slot whose endpoints did not change keeps its cells and gets the new
+// (k, L0) (+ actuation cell).  The tiles of every touched slice are
+// listed for the window layout's partial rebuild.  fail = 1: a lane has no
+// free row within the layout's widths -- the caller re-indexes everything.
+template <int P>
+__global__ void k_split_insert(int64_t n, const int64_t *slots, KState S,
+                               int cap_wa, int cap_wb, int tt,
+                               float4 *sp_actc, double *sp_acto,
+                               const uint8_t *grp, int32_t *tiles,
+                               int *fail) {
+  using F = typename Tr<P>::F;
+  using F2 = typename Tr<P>::F2;
+  const int lane = threadIdx.x;
+  const int a = S.sp_a;
+  const int64_t rows = S.sp_rows, wa_stride = (int64_t)1 << a;
+  const uint32_t sent = S.sp_sent, nul = S.sp_null;
+  // the layout arrays, writable here (KState carries them read-only)
+  int64_t *E1 = (int64_t *)S.e1, *E2 = (int64_t *)S.e2;
+  int32_t *SPS = (int32_t *)S.sp_s;
+  uint32_t *SPW = (uint32_t *)S.sp_w, *EKL = (uint32_t *)S.sp_ekl;
+  F2 *SKL = (F2 *)S.sp_kl;
+  auto cell = [&](int64_t sl, int64_t r, int ln) {
+    return (sl * rows + r) * 32 + ln;
+  };
+  auto kl_of = [&](int64_t e) {  // kl index of A cell e
+    const int64_t sl = e / (rows * 32), rem = e - sl * rows * 32;
+    return (uint32_t)((sl << (a + 5)) | rem);
+  };
+  // lowest row r in [r0, r0 + cap) of lane ln of slice sl holding `free_w`
+  auto probe = [&](int64_t sl, int ln, int64_t r0, int cap,
+                   uint32_t free_w) -> int {
+    for (int base = 0; base < cap; base += 32) {
+      const int r = base + lane;
+      const bool ok = r < cap && S.sp_j[cell(sl, r0 + r, ln)] == free_w;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (m) return base + __ffs(m) - 1;
+    }
+    return -1;
+  };
+  for (int64_t q = 0; q < n; q++) {
+    const int64_t s = slots[q];
+    const int2 ab = S.ends[s];
+    const int64_t eA = S.e1[s], eB = S.e2[s];
+    const bool ownA = eA >= 0 && S.sp_s[eA] == (int32_t)s && S.sp_j[eA] != sent;
+    const bool ownB = eB >= 0 && S.sp_s[eB] == (int32_t)s && S.sp_j[eB] != nul;
+    int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
+    if (ownA) t0 = (int32_t)(eA / (rows * 32) / tt);
+    if (ownB) t1 = (int32_t)(eB / (rows * 32) / tt);
+    const bool same = ab.x >= 0 && ownA && ownB &&
+                      (eA & 31) == (ab.x & 31) &&
+                      eA / (rows * 32) == (ab.x >> 5) &&
+                      S.sp_j[eA] == (uint32_t)ab.y &&
+                      (eB & 31) == (ab.y & 31) &&
+                      eB / (rows * 32) == (ab.y >> 5);
+    int rA = -1, rB = -1;
+    if (ab.x >= 0 && !same) {
+      rA = probe(ab.x >> 5, ab.x & 31, 0, cap_wa, sent);
+      rB = probe(ab.y >> 5, ab.y & 31, wa_stride, cap_wb, nul);
+      if (rA < 0 || rB < 0) {
+        if (lane == 0) *fail = 1;
+        return;
+      }
+    }
+    if (lane == 0) {
+      if (!same) {  // release the previous wiring's cells
+        if (ownA) {
+          S.sp_j[eA] = sent;
+          SKL[kl_of(eA)] = F2{};
+          SPS[eA] = -1;
+        }
+        if (ownB) {
+          S.sp_j[eB] = nul;
+          SPS[eB] = -1;
+        }
+        E1[s] = -1;
+        E2[s] = -1;
+      }
+      if (ab.x >= 0) {
+        const int64_t sl1 = ab.x >> 5, sl2 = ab.y >> 5;
+        int64_t ea = eA, eb = eB;
+        if (!same) {
+          ea = cell(sl1, rA, ab.x & 31);
+          eb = cell(sl2, wa_stride + rB, ab.y & 31);
+        }
+        const uint32_t kli = kl_of(ea);
+        SKL[kli] = ((const F2 *)S.kL0)[s];
+        if (sp_actc) {
+          const double4 ac = S.act[s];
+          sp_actc[kli] = act_cell(ac.z, ac.y, ac.w, grp[s]);
+          sp_acto[kli] = ac.z;
+        }
+        if (!same) {
+          S.sp_j[ea] = (uint32_t)ab.y;
+          SPS[ea] = (int32_t)s;
+          S.sp_j[eb] = kli;
+          SPS[eb] = (int32_t)s;
+          EKL[s] = kli;
+          E1[s] = ea;
+          E2[s] = eb;
+          uint32_t w1 = S.sp_w[sl1];
+          if ((uint32_t)rA + 1 > (w1 & 0xFFFFu))
+            w1 = (w1 & 0xFFFF0000u) | (uint32_t)(rA + 1);
+          SPW[sl1] = w1;
+          uint32_t w2 = S.sp_w[sl2];
+          if ((uint32_t)rB + 1 > (w2 >> 16))
+            w2 = (w2 & 0xFFFFu) | ((uint32_t)(rB + 1) << 16);
+          SPW[sl2] = w2;
+        }
+        t2 = (int32_t)(sl1 / tt);
+        t3 = (int32_t)(sl2 / tt);
+        const bool special = (S.mode[s] != 0 && grp[s] == 0) ||
+                             ((const F *)S.thr)[s] != (F)CUDART_INF ||
+                             (S.damp && S.damp[s] != 0.0);
+        if (special) {
+          S.xflags[ab.x] = 1;
+          S.xflags[ab.y] = 1;
+          or_flags((typename Tr<P>::R4 *)S.vel + ab.x, MF_SPECIAL);
+          or_flags((typename Tr<P>::R4 *)S.vel + ab.y, MF_SPECIAL);
+        }
+      }
+      int32_t *tq = tiles + 4 * q;
+      tq[0] = t0;
+      tq[1] = t1;
+      tq[2] = t2;
+      tq[3] = t3;
+    }
+    __syncwarp();
   }
 }
 
@@ -1837,7 +1975,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
                     &c->fz_gid, &c->diag, &c->fz_perm, &c->fz_cnt,
                     &c->fz_epos, &c->fz_cnt_a,
-                    &c->win_fail, &c->stage2};
+                    &c->win_fail, &c->stage2, &c->inc_buf};
   for (void *p : c->halo_ipc) cudaIpcCloseMemHandle(p);
   c->halo_desc.release();
   c->halo_dst.release();
@@ -1885,6 +2023,7 @@ int sl_get_stats(sl_ctx *c, sl_stats *o) {
   o->fused_aborts = c->fz_aborts;
   o->win_tile_slices = c->win ? c->wcfg.tile_slices : 0;
   o->win_stages = c->win ? c->wcfg.nst : 0;
+  o->inplace_edits = c->inc_edits;
   const DevBuf *bufs[] = {&c->pos[0], &c->pos[1], &c->plo[0], &c->plo[1], &c->pmass, &c->vel, &c->acc,
                           &c->fext, &c->load, &c->m_gen, &c->m_alive,
                           &c->ends, &c->kL0, &c->s_alive, &c->s_degen,
@@ -2109,6 +2248,77 @@ int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
   return SL_OK;
 }
 
+// O(edits) re-wiring of a live split + window layout after a record write
+// of n slots (k_split_insert, then k_win_build on the touched tiles only).
+// Leaves c->layout_valid false -- the full device re-index at the next
+// step -- whenever the edit does not fit in place.
+static int insert_incremental(sl_ctx *c, int64_t n, const int64_t *slots) {
+  const WinCfg &w = c->wcfg;
+  const int tt = w.tile_slices;
+  CK(c->inc_buf.ensure(align256(8 * n) + align256(16 * n) + 256));
+  int64_t *dsl = c->inc_buf.as<int64_t>();
+  int32_t *dtiles = (int32_t *)((char *)c->inc_buf.p + align256(8 * n));
+  int *dfail = (int *)((char *)dtiles + align256(16 * n));
+  CK(cudaMemcpyAsync(dsl, slots, 8 * n, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(dfail, 0, sizeof(int), c->st));
+  CK(cudaMemsetAsync(dtiles, 0xFF, 16 * n, c->st));
+  KState S = make_state(c);
+  S.split = true;
+  const bool act = c->agrp.n > 1;
+  auto k = c->prec == PREC_FP32 ? k_split_insert<PREC_FP32>
+                                : k_split_insert<PREC_MIXED>;
+  k<<<1, 32, 0, c->st>>>(n, dsl, S, (int)c->sp_wa, (int)c->sp_wb, tt,
+                         act ? c->sp_actc.as<float4>() : nullptr,
+                         c->sp_acto.as<double>(), c->s_grp.as<uint8_t>(),
+                         dtiles, dfail);
+  CKL();
+  c->launches++;
+  int failed = 0;
+  std::vector<int32_t> tiles(4 * n);
+  CK(cudaMemcpyAsync(&failed, dfail, sizeof(int), cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaMemcpyAsync(tiles.data(), dtiles, 16 * n, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (failed) {
+    c->layout_valid = false;
+    return SL_OK;
+  }
+  std::sort(tiles.begin(), tiles.end());
+  tiles.erase(std::unique(tiles.begin(), tiles.end()), tiles.end());
+  if (!tiles.empty() && tiles[0] < 0) tiles.erase(tiles.begin());
+  if (tiles.empty()) {
+    c->inc_edits++;
+    return SL_OK;
+  }
+  CK(cudaMemcpyAsync(dtiles, tiles.data(), 4 * tiles.size(),
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->win_fail.p, 0, 24, c->st));
+  const int64_t m_pad = c->n_slices * 32;
+  k_win_build<<<(unsigned)tiles.size(), 256, 0, c->st>>>(
+      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
+      c->n_slices, c->m_n, c->sp_a, c->sp_rows, (uint32_t)m_pad,
+      (uint32_t)(c->n_slices << (c->sp_a + 5)), tt, w.bl, w.cap_a, w.cap_b,
+      c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
+      c->s_grp.as<uint8_t>(), c->win_rec.as<TileRec>(),
+      c->win_dict.as<float2>(), c->win_actb.as<unsigned char>(),
+      c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
+      c->prec == PREC_MIXED ? 1 : 0, c->win_fail.as<unsigned long long>(),
+      dtiles);
+  CKL();
+  c->launches++;
+  unsigned long long res[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(res, c->win_fail.p, 24, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  const bool act_block = w.off_win > w.off_act;
+  if (res[0] || res[1] > w.cap_rec || (res[2] && !act_block)) {
+    c->layout_valid = false;  // a tile outgrew the stage: full re-index
+    return SL_OK;
+  }
+  c->inc_edits++;
+  return SL_OK;
+}
+
 int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
                      const int64_t *m1, const int64_t *m2,
                      const int64_t *m1gen, const int64_t *m2gen,
@@ -2128,10 +2338,20 @@ int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
                   (long long)slots[r]);
   if (n == 0) return SL_OK;
   CK(cudaSetDevice(c->device));
-  c->layout_valid = false;  // re-indexed on the device at the next step
-  return upload_springs_impl(c, n, slots, m1, m2, m1gen, m2gen, rest, k,
-                             diam, yield, mode, amp, freq, off, per, alive,
-                             degen, false);
+  // in place when the live layout is the split + window one (the fp32 /
+  // mixed production path) and the edit is small; else re-indexed on the
+  // device at the next step
+  static const bool no_inc = getenv("SL_NO_INCREMENTAL") != nullptr;
+  const bool inc = !no_inc && c->layout_valid && c->split && c->win &&
+                   !c->fz_ok && n <= 256;  // (serial insert: above, the re-index is faster)
+  const int groups_before = c->agrp.n;
+  c->layout_valid = false;
+  int rc = upload_springs_impl(c, n, slots, m1, m2, m1gen, m2gen, rest, k,
+                               diam, yield, mode, amp, freq, off, per, alive,
+                               degen, false);
+  if (rc || !inc || c->agrp.n != groups_before) return rc;
+  c->layout_valid = true;
+  return insert_incremental(c, n, slots);
 }
 
 int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
@@ -2148,9 +2368,19 @@ int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
     if (slots[r] < 0 || slots[r] >= c->s_n)
       return fail(c, SL_EINVAL, "spring slot %lld out of range",
                   (long long)slots[r]);
-  return upload_springs_impl(c, n, slots, nullptr, nullptr, nullptr, nullptr,
-                             rest, k, diam, yield, mode, amp, freq, off, per,
-                             nullptr, nullptr, true);
+  // the window layout's material tables hold (k, L0) by value: refreshed
+  // for the touched tiles in place (insert_incremental keeps a slot's
+  // cells when its endpoints are unchanged), else a full re-index
+  static const bool no_inc = getenv("SL_NO_INCREMENTAL") != nullptr;
+  const bool inc = !no_inc && c->layout_valid && c->split && c->win &&
+                   !c->fz_ok && n <= 256;  // (serial insert: above, the re-index is faster)
+  const int groups_before = c->agrp.n;
+  int rc = upload_springs_impl(c, n, slots, nullptr, nullptr, nullptr,
+                               nullptr, rest, k, diam, yield, mode, amp, freq,
+                               off, per, nullptr, nullptr, true);
+  if (rc || !inc || c->agrp.n != groups_before) return rc;
+  c->layout_valid = true;
+  return insert_incremental(c, n, slots);
 }
 
 int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {

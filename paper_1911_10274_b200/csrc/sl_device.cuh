@@ -1246,17 +1246,24 @@ static __global__ void __launch_bounds__(384)
 // the split layout's (k, L0) cell can be zeroed as well).
 __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
   if (S.split) {
-    if (S.e1[s] >= 0) {
-      S.sp_j[S.e1[s]] = S.sp_sent;
+    // cells another spring took over since this one died (in-place topology
+    // sync, k_split_insert) are not this spring's to kill
+    const int64_t e1 = S.e1[s] >= 0 && S.sp_s[S.e1[s]] == (int32_t)s ? S.e1[s]
+                                                                       : -1;
+    const int64_t e2 = S.e2[s] >= 0 && S.sp_s[S.e2[s]] == (int32_t)s ? S.e2[s]
+                                                                       : -1;
+    if (e1 < 0 && e2 < 0) return;
+    if (e1 >= 0) {
+      S.sp_j[e1] = S.sp_sent;
       if (S.fsz8)
         ((double2 *)S.sp_kl)[S.sp_ekl[s]] = make_double2(0.0, 0.0);
       else
         ((float2 *)S.sp_kl)[S.sp_ekl[s]] = make_float2(0.f, 0.f);
     }
-    if (S.e2[s] >= 0) S.sp_j[S.e2[s]] = S.sp_null;
+    if (e2 >= 0) S.sp_j[e2] = S.sp_null;
     if (S.fz_code) {  // fused groups: both entries get the zero code
       const int64_t per = (int64_t)S.sp_rows * 32;
-      const int64_t es[2] = {S.e1[s], S.e2[s]};
+      const int64_t es[2] = {e1, e2};
       for (int q = 0; q < 2; q++) {
         if (es[q] < 0) continue;
         const int64_t sl = es[q] / per;
@@ -1281,13 +1288,13 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
         *wp = (*wp & ((1u << 26) - 1u)) |
               ((uint32_t)S.win_zero[sl / S.win_tt] << 26);
       };
-      if (S.e1[s] >= 0) {
+      if (e1 >= 0) {
         const uint32_t kli = S.sp_ekl[s];
         const int64_t sl = kli >> (a + 5);
         zero_code(sl, (int)((kli >> 5) & ((1u << a) - 1)), (int)(kli & 31));
       }
-      if (S.e2[s] >= 0) {
-        const int64_t per = (int64_t)S.sp_rows * 32, e = S.e2[s];
+      if (e2 >= 0) {
+        const int64_t per = (int64_t)S.sp_rows * 32, e = e2;
         const int64_t sl = e / per;
         const int rem = (int)(e - sl * per);
         const int rb = (rem >> 5) - (1 << a);

@@ -48,7 +48,7 @@ def test_abi_version_and_constants():
         key = {"fp64": "SL_PREC_FP64", "fp32": "SL_PREC_FP32",
                "mixed": "SL_PREC_MIXED"}[name]
         assert int(consts[key]) == code
-    assert C.sizeof(_native.SlStats) == 8 * 8 + 4 * 4 + 3 * 8 + 2 * 4
+    assert C.sizeof(_native.SlStats) == 8 * 8 + 4 * 4 + 3 * 8 + 2 * 4 + 8
 
 
 @pytest.mark.skipif(_native.device_count() > 0, reason="GPU present")
