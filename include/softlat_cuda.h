@@ -262,6 +262,17 @@ int sl_download_wait_extra(sl_ctx *ctx);
  * waits for them: the host store's lock-time state, fetched only when a
  * reader needs it (ObjectStore.lock_for_run). */
 int sl_stash_state(sl_ctx *ctx);
+/* Speculative predicate checks (control.py condition breakpoints): keep a
+ * device copy of the current state (positions, velocities, accelerations,
+ * f_ext, the ping-pong index) and, when view_pos / view_vel are given
+ * (page-locked double[m_n][3]), copy positions / velocities there on the
+ * side stream -- the next run goes on while the host evaluates the
+ * predicate; sl_checkpoint_view_wait waits for the view.  sl_restore puts
+ * the checkpointed state back (the run after it is undone; the caller
+ * guarantees no topology change happened in between). */
+int sl_checkpoint(sl_ctx *ctx, double *view_pos, double *view_vel);
+int sl_checkpoint_view_wait(sl_ctx *ctx);
+int sl_restore(sl_ctx *ctx);
 int sl_download_stash(sl_ctx *ctx, double *pos, double *vel, double *acc,
                       double *fext);
 /* As sl_download_masses, but returns once pos / vel have landed: acc and

@@ -44,7 +44,8 @@ EXPORTS = (
     "sl_write_state_async",
     "sl_host_is_iota", "sl_download_state", "sl_download_wait",
     "sl_download_state_ex", "sl_download_wait_extra",
-    "sl_stash_state", "sl_download_stash")
+    "sl_stash_state", "sl_download_stash", "sl_checkpoint",
+    "sl_checkpoint_view_wait", "sl_restore")
 
 
 class SlStats(C.Structure):
@@ -123,6 +124,9 @@ def load_library(path: str = LIB_PATH):
             "sl_download_wait_extra": ([P], I),
             "sl_stash_state": ([P], I),
             "sl_download_stash": ([P, P, P, P, P], I),
+            "sl_checkpoint": ([P, P, P], I),
+            "sl_checkpoint_view_wait": ([P], I),
+            "sl_restore": ([P], I),
             "sl_sync": ([P], I),
             "sl_step_async": ([P, I64, P, D, I], I),
             "sl_step_finish": ([P, P, P, P], I),
@@ -656,6 +660,27 @@ class Context:
         self._check(self.lib.sl_download_stash(
             self.h, *[_ptr(a) if a is not None else None
                       for a in (pos, vel, acc, fext)]), "sl_download_stash")
+
+    def checkpoint(self, view_pos=None, view_vel=None):
+        """sl_checkpoint (views: page-locked (m, 3) fp64, kept alive until
+        checkpoint_view_wait())."""
+        for a in (view_pos, view_vel):
+            if a is not None and not (a.dtype == np.float64 and
+                                      a.flags.c_contiguous and
+                                      a.size == 3 * self.m_n):
+                raise InvalidValueError("checkpoint: contiguous float64 "
+                                        "(m, 3) arrays")
+        self._check(self.lib.sl_checkpoint(
+            self.h, *[_ptr(a) if a is not None else None
+                      for a in (view_pos, view_vel)]), "sl_checkpoint")
+
+    def checkpoint_view_wait(self):
+        self._check(self.lib.sl_checkpoint_view_wait(self.h),
+                    "sl_checkpoint_view_wait")
+
+    def restore(self):
+        self.epoch += 1
+        self._check(self.lib.sl_restore(self.h), "sl_restore")
 
     def download_wait_extra(self):
         self._check(self.lib.sl_download_wait_extra(self.h),

@@ -164,6 +164,11 @@ struct sl_ctx {
   DevBuf stage, sort_tmp, keys[2], vals[2], deg, width, start;
   DevBuf stage2;  // sl_stash_state: the fp64 state at the last stash
   DevBuf inc_buf;  // insert_incremental: slots, touched tiles, fail flag
+  // sl_checkpoint: device copy of the state a speculative run may undo
+  DevBuf ck_pos, ck_plo, ck_vel, ck_acc, ck_fext, ck_view;
+  int ck_cur = -1;
+  cudaEvent_t ck_ev = nullptr, ck_done = nullptr;
+  bool ck_pending = false;
   int64_t inc_edits = 0;  // record writes applied in place
   DevBuf status;
   unsigned long long *h_status = nullptr;
@@ -1927,6 +1932,10 @@ int sl_create(int device, int precision, sl_ctx **out) {
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming);
   if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->ck_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&c->ck_done, cudaEventDisableTiming);
+  if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->side_done, cudaEventDisableTiming);
   if (e == cudaSuccess)
     e = cudaEventCreateWithFlags(&c->snap_ev, cudaEventDisableTiming);
@@ -1975,7 +1984,7 @@ int sl_destroy(sl_ctx *c) {
                     &c->fz_times, &c->fz_diff, &c->vel2, &c->fz_zero,
                     &c->fz_gid, &c->diag, &c->fz_perm, &c->fz_cnt,
                     &c->fz_epos, &c->fz_cnt_a,
-                    &c->win_fail, &c->stage2, &c->inc_buf};
+                    &c->win_fail, &c->stage2, &c->inc_buf, &c->ck_pos, &c->ck_plo, &c->ck_vel, &c->ck_acc, &c->ck_fext, &c->ck_view};
   for (void *p : c->halo_ipc) cudaIpcCloseMemHandle(p);
   c->halo_desc.release();
   c->halo_dst.release();
@@ -1991,6 +2000,8 @@ int sl_destroy(sl_ctx *c) {
   if (c->tail_ev) cudaEventDestroy(c->tail_ev);
   if (c->extra_ev) cudaEventDestroy(c->extra_ev);
   if (c->side_ev) cudaEventDestroy(c->side_ev);
+  if (c->ck_ev) cudaEventDestroy(c->ck_ev);
+  if (c->ck_done) cudaEventDestroy(c->ck_done);
   if (c->side_done) cudaEventDestroy(c->side_done);
   if (c->snap_ev) cudaEventDestroy(c->snap_ev);
   if (c->snap_done) cudaEventDestroy(c->snap_done);
@@ -2990,6 +3001,97 @@ int sl_stash_state(sl_ctx *c) {
   c->launches++;
   CK(cudaEventRecord(c->side_ev, c->st));
   c->stash_set = true;
+  return SL_OK;
+}
+
+int sl_checkpoint(sl_ctx *c, double *view_pos, double *view_vel) {
+  if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
+  if (c->async_open)
+    return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
+  const int64_t m = c->m_n;
+  CK(cudaSetDevice(c->device));
+  const int64_t mp = (m + 31) / 32 * 32 + 32;
+  const size_t r4 = 4 * c->rsz;
+  CK(c->ck_pos.ensure(r4 * mp));
+  CK(c->ck_vel.ensure(r4 * (m + 32)));
+  CK(c->ck_acc.ensure(3 * c->rsz * m + 16));
+  CK(c->ck_fext.ensure(r4 * m + 16));
+  auto d2d = [&](DevBuf &dst, const void *src, size_t bytes) -> int {
+    if (bytes)
+      CK(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyDeviceToDevice, c->st));
+    return SL_OK;
+  };
+  int rc;
+  if ((rc = d2d(c->ck_pos, c->pos[c->cur].p, r4 * mp))) return rc;
+  if (c->prec == PREC_FP32) {
+    CK(c->ck_plo.ensure(8 * mp));
+    if ((rc = d2d(c->ck_plo, c->plo[c->cur].p, 8 * mp))) return rc;
+  }
+  if ((rc = d2d(c->ck_vel, c->vel.p, r4 * (m + 32)))) return rc;
+  if ((rc = d2d(c->ck_acc, c->acc.p, 3 * c->rsz * m))) return rc;
+  if ((rc = d2d(c->ck_fext, c->fext.p, r4 * m))) return rc;
+  c->ck_cur = c->cur;
+  if (m && (view_pos || view_vel)) {  // the predicate's view, side stream
+    if (c->ck_pending) CK(cudaEventSynchronize(c->ck_done));
+    const size_t vb = align256(24 * m);
+    CK(c->ck_view.ensure(2 * vb));
+    char *b = (char *)c->ck_view.p;
+    auto k = c->prec == PREC_FP64   ? k_unpack_masses<PREC_FP64>
+             : c->prec == PREC_FP32 ? k_unpack_masses<PREC_FP32>
+                                    : k_unpack_masses<PREC_MIXED>;
+    k<<<blocks_for(m), 256, 0, c->st>>>(
+        m, c->pos[c->cur].p, c->plo[c->cur].p, c->vel.p, nullptr, nullptr,
+        view_pos ? (double *)b : nullptr,
+        view_vel ? (double *)(b + vb) : nullptr, nullptr, nullptr);
+    CKL();
+    c->launches++;
+    CK(cudaEventRecord(c->ck_ev, c->st));
+    CK(cudaStreamWaitEvent(c->side, c->ck_ev, 0));
+    if (view_pos)
+      CK(cudaMemcpyAsync(view_pos, b, 24 * m, cudaMemcpyDeviceToHost,
+                         c->side));
+    if (view_vel)
+      CK(cudaMemcpyAsync(view_vel, b + vb, 24 * m, cudaMemcpyDeviceToHost,
+                         c->side));
+    CK(cudaEventRecord(c->ck_done, c->side));
+    c->ck_pending = true;
+  }
+  return SL_OK;
+}
+
+int sl_checkpoint_view_wait(sl_ctx *c) {
+  if (!c) return fail(c, SL_EINVAL, "NULL context");
+  if (!c->ck_pending) return SL_OK;
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventSynchronize(c->ck_done));
+  c->ck_pending = false;
+  return SL_OK;
+}
+
+int sl_restore(sl_ctx *c) {
+  if (!c || c->ck_cur < 0) return fail(c, SL_ESTATE, "no checkpoint");
+  if (c->async_open)
+    return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
+  CK(cudaSetDevice(c->device));
+  const int64_t m = c->m_n;
+  const int64_t mp = (m + 31) / 32 * 32 + 32;
+  const size_t r4 = 4 * c->rsz;
+  const int b = c->ck_cur;
+  CK(cudaMemcpyAsync(c->pos[b].p, c->ck_pos.p, r4 * mp,
+                     cudaMemcpyDeviceToDevice, c->st));
+  if (c->prec == PREC_FP32)
+    CK(cudaMemcpyAsync(c->plo[b].p, c->ck_plo.p, 8 * mp,
+                       cudaMemcpyDeviceToDevice, c->st));
+  CK(cudaMemcpyAsync(c->vel.p, c->ck_vel.p, r4 * (m + 32),
+                     cudaMemcpyDeviceToDevice, c->st));
+  if (m) {
+    CK(cudaMemcpyAsync(c->acc.p, c->ck_acc.p, 3 * c->rsz * m,
+                       cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaMemcpyAsync(c->fext.p, c->ck_fext.p, r4 * m,
+                       cudaMemcpyDeviceToDevice, c->st));
+  }
+  c->cur = b;
+  CK(cudaStreamSynchronize(c->st));
   return SL_OK;
 }
 

@@ -393,3 +393,43 @@ def test_pause_pull_fills_snapshot_arena(touch):
         assert snap.velocities.tobytes() == st._m_vel[:n].tobytes()
         assert np.array_equal(snap.ids, np.arange(n))
     ctl.stop()
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_speculative_condition_checks_match_synchronous(precision,
+                                                        monkeypatch):
+    """Condition breakpoints checked speculatively (the next batch runs
+    while the predicate looks at a checkpoint; a hit undoes it, sl_restore)
+    pause at the same step with the same state as the synchronous checks
+    (reference control.py:579-600): fp64 bit for bit."""
+    def run(spec):
+        if spec:
+            monkeypatch.delenv("SL_NO_SPECULATE", raising=False)
+        else:
+            monkeypatch.setenv("SL_NO_SPECULATE", "1")
+        env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
+            normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
+            static_friction=1.0, kinetic_friction=0.8)])
+        st, _ = make_lattice(n=6, corner=Vec3(0, 0, 0.004))
+        ctl = SimController(st, env, StepConfig(dt=1e-4, precision=precision))
+        z0 = float(st._m_pos[:st.mass_slot_count, 2].min())
+        ctl.set_breakpoint(Breakpoint.on_condition(
+            lambda v: float(v.positions[:, 2].min()) < z0 - 2e-4, every=7))
+        ctl.start(0.5)
+        rep = ctl.wait_for_event(timeout=120)
+        snap = ctl.snapshot()
+        undos = getattr(ctl, "speculative_undos", 0)
+        ctl.stop()
+        return rep, snap, undos
+
+    rep_s, snap_s, undos = run(True)
+    rep_n, snap_n, _ = run(False)
+    assert rep_s.reason == rep_n.reason == "breakpoint"
+    assert rep_s.step_count == rep_n.step_count
+    assert undos >= 1
+    if precision == "fp64":
+        assert snap_s.positions.tobytes() == snap_n.positions.tobytes()
+        assert snap_s.velocities.tobytes() == snap_n.velocities.tobytes()
+    else:
+        d = np.abs(snap_s.positions - snap_n.positions).max()
+        assert d < 1e-5 * np.abs(snap_n.positions).max()
