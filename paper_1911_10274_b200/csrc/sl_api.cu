@@ -1273,7 +1273,9 @@ int build_window_layout(sl_ctx *c) {
   if (const char *ev = getenv("SL_WIN_T")) {
     const int v = atoi(ev);
     if (c->prec != PREC_MIXED)
-      tt = v == 4 || v == 8 || v == 12 || v == 20 || v == 24 ? v : 16;
+      tt = v == 4 || v == 8 || v == 10 || v == 12 || v == 20 || v == 24
+               ? v
+               : 16;
     return build_window_tt(c, tt);
   }
   // fp32 with compensated positions (larger windows): 16-slice tiles fit 2
@@ -1401,12 +1403,11 @@ int build_window_exact(sl_ctx *c) {
   WinCfg w{};
   w.n_tiles = n_tiles;
   w.tile_slices = tt;
-  w.cap_a = (int)c->max_width;
+  w.cap_a = (int)((c->max_width + 1) / 2 * 2);  // entry-word row pairs
   w.cap_b = 0;
-  auto al16 = [](uint32_t x) { return (x + 15) / 16 * 16; };
-  w.bl.off_acode = al16((uint32_t)w.cap_a * 64);
-  w.bl.off_b16 = w.bl.off_bcode = al16(w.bl.off_acode + (uint32_t)w.cap_a * 32);
-  w.bl.slice_bytes = w.bl.off_bcode;
+  // slice block: entry words (sl_window.cuh ew_word64), row pairs per lane
+  w.bl.off_acode = w.bl.off_b16 = w.bl.off_bcode = 0;
+  w.bl.slice_bytes = (uint32_t)w.cap_a * 128u;
   CK(c->win_rec.ensure(sizeof(TileRec) * n_tiles));
   CK(c->win_dict.ensure(16 * WIN_DMAX * n_tiles));
   CK(c->win_blk.ensure((size_t)w.bl.slice_bytes * n_tiles * tt));

@@ -126,6 +126,7 @@ struct SplitLaunch {
       switch (tt) {
         case 4: f(k_win_tma<P, 4>); return;   // small meshes: more CTAs
         case 8: f(k_win_tma<P, 8>); return;
+        case 10: f(k_win_tma<P, 10>); return;  // 3 ring stages (sweeps)
         case 12: f(k_win_tma<P, 12>); return;
         case 20: f(k_win_tma<P, 20>); return;
         case 24: f(k_win_tma<P, 24>); return;

@@ -604,14 +604,21 @@ def check_stability(store: ObjectStore, dt: float,
             if n_alive else np.inf
         k_springs = 0.0
         kc = getattr(store, "_kmax_cache", None)
-        if sn and kc is not None and kc[0] == (store.topology_version,
-                                               store.spring_param_version,
-                                               sn):
+        kt = store.__dict__.get("_kmax_track")
+        if sn and kt is not None and store._s_alive_count > 0:
+            # exact through edits (ObjectStore._kmax_add / _kmax_remove)
+            k_springs = max(kt[0], 0.0)
+        elif sn and kc is not None and kc[0] == (store.topology_version,
+                                                 store.spring_param_version,
+                                                 sn):
             k_springs = max(kc[1], 0.0) if kc[1] == kc[1] else kc[1]
         elif sn:  # np.max(..., initial=0.0): NaN propagates
-            hi = _native.masked_extrema(store._s_k[:sn],
-                                        store._s_alive[:sn])[1]
+            alive_s = store._s_alive[:sn]
+            hi = _native.masked_extrema(store._s_k[:sn], alive_s)[1]
             k_springs = hi if (hi != hi or hi > 0.0) else 0.0
+            if hi == hi and hi > -np.inf:  # re-seed the tracker
+                store.__dict__["_kmax_track"] = [hi, int(np.count_nonzero(
+                    (store._s_k[:sn] == hi) & alive_s.astype(bool)))]
         store._stability_cache = (key, n_alive, k_springs, m_min)
     if n_alive == 0:
         return 0.0

@@ -196,3 +196,40 @@ def test_lattice_counts_and_connectivity(n):
                 want.add((p, q))
     got = {(min(x, y), max(x, y)) for x, y in zip(a.tolist(), b.tolist())}
     assert got == want and len(got) == len(a)
+
+
+def test_stiffness_max_tracker_exact_through_edits():
+    """ObjectStore keeps the largest alive stiffness exact through creates,
+    deletes and retunes (engine.check_stability's k_max without an O(S)
+    scan per edit): equal to the brute-force masked max at every step."""
+    import numpy as np
+    from paper_1911_10274_b200 import (Mass, ObjectStore, Spring, Vec3,
+                                       engine)
+    rng = np.random.default_rng(5)
+    st = ObjectStore()
+    ms = [st.create_mass(Mass(pos=Vec3(float(i), 0.0, 0.0), m=1.0))
+          for i in range(40)]
+    springs = []
+    for step in range(300):
+        op = rng.integers(0, 3)
+        if op == 0 or not springs:
+            a, b = rng.choice(40, 2, replace=False)
+            k = float(rng.choice([5.0, 7.0, 9.0, float(rng.uniform(0, 10))]))
+            springs.append(st.create_spring(Spring(
+                m1=ms[a], m2=ms[b], rest_length=1.0, stiffness=k)))
+        elif op == 1:
+            st.delete_spring(springs.pop(int(rng.integers(len(springs)))))
+        else:
+            h = springs[int(rng.integers(len(springs)))]
+            st.set_spring_field(h, "stiffness",
+                                float(rng.choice([9.0, float(rng.uniform(0, 10))])))
+        s = st.spring_slot_count
+        alive = st._s_alive[:s].astype(bool)
+        want = float(st._s_k[:s][alive].max()) if alive.any() else None
+        t = st.__dict__.get("_kmax_track")
+        if t is not None and want is not None:
+            assert t[0] == want, (step, t, want)
+        # the stability ratio uses the same k_max as a fresh scan
+        r = engine.check_stability(st, 1e-3)
+        if want is not None:
+            assert abs(r - 1e-3 * (want / 1.0) ** 0.5) < 1e-15
