@@ -24,6 +24,7 @@ timeout 600 python tools/e2e_settle.py --steps 20 --config D > $out/e2e_settle_D
 timeout 600 python tools/predicate_bench.py > $out/predicate.txt 2>&1
 timeout 900 python tools/edit_latency.py > $out/edit_latency.txt 2>&1
 SL_NO_INCREMENTAL=1 timeout 900 python tools/edit_latency.py > $out/edit_latency_full.txt 2>&1
+timeout 900 python tools/build_timing.py > $out/build_timing.txt 2>&1
 # the ncu launch list of the driver's command (20 steps): shares, not times
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $out/launches_n20.csv python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu-baseline --no-fp64 > /dev/null 2>&1

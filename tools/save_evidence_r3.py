@@ -26,7 +26,7 @@ with open(os.path.join(DST, "bench_lines.json"), "w") as fh:
     json.dump(lines, fh, indent=1)
 for f in ("pytest.txt", "smoke.txt", "sanitizer.txt", "e2e_settle_B.txt",
           "e2e_settle_D.txt", "predicate.txt", "edit_latency.txt",
-          "edit_latency_full.txt"):
+          "edit_latency_full.txt", "build_timing.txt"):
     if os.path.exists(os.path.join(SRC, f)):
         shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
 
