@@ -433,3 +433,25 @@ def test_speculative_condition_checks_match_synchronous(precision,
     else:
         d = np.abs(snap_s.positions - snap_n.positions).max()
         assert d < 1e-5 * np.abs(snap_n.positions).max()
+
+
+def test_lock_time_reads_of_deferred_state():
+    """With the pause-time pull deferred (store big enough for the snapshot
+    arena), lock-time readers during the next run -- a stale snapshot and
+    get_mass -- still see the state of the pause (fetched from the stash the
+    run kept on the device)."""
+    ctl, st, body = controller(n=42, dt=1e-4, stretch=1.01)
+    ctl.start(5 * 1e-4)
+    ctl.wait_for_event(timeout=120)
+    snap = ctl.snapshot()
+    h = body.mass_handles[123]
+    ctl.start(10.0)
+    stale = ctl.snapshot()
+    m = st.get_mass(h)
+    assert stale.stale
+    assert stale.positions.tobytes() == snap.positions.tobytes()
+    assert stale.velocities.tobytes() == snap.velocities.tobytes()
+    assert np.array_equal(m.pos.as_array(), snap.positions[h.slot])
+    ctl.pause()
+    ctl.wait_for_event(timeout=120)
+    ctl.stop()
