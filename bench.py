@@ -174,6 +174,13 @@ def algorithmic_bytes(springs: int, masses: int, precision: str,
     return springs * (8 + (2 + extra_words) * w_s) + masses * bm
 
 
+# untimed control segments before the timed e2e one: the snapshot pool
+# pages in (page-locked) buffer sets in the background during the first
+# ones, and page-locking stalls the process's CUDA calls while it runs
+E2E_WARM = int(os.environ.get("SL_E2E_WARM", "3"))
+E2E_REPS = 5
+
+
 def _native_pinned_copy(a):
     """A page-locked copy of a host array (the inputs of an e2e segment live
     in pinned memory, as the contract's host buffers)."""
@@ -518,7 +525,7 @@ def main():
         ctl = SimController(st, env, cfg)
         k = args.steps
         m = st.mass_slot_count
-        for _ in range(2):  # untimed segments: steady state (pools warm)
+        for _ in range(E2E_WARM):  # untimed segments: steady state (pools warm)
             ctl.start(k * dt)
             ctl.wait_for_event()
             warm = ctl.snapshot()
@@ -527,17 +534,24 @@ def main():
         vel_in = _native_pinned_copy(warm.velocities)
         del warm
         full0 = getattr(engine.mirror_for(st, cfg), "full_pushes", 0)
-        if dist is not None:
-            dist.barrier()
-        w0 = time.perf_counter()
-        sio.apply_snapshot(st, ids, pos_in, vel_in)
-        ctl.start(k * dt)
-        rep = ctl.wait_for_event()
-        snap = ctl.snapshot()
-        wall = time.perf_counter() - w0
+        # E2E_REPS timed segments (each: set-state, K steps, get-state) and
+        # their median: one ~5 ms segment is at the mercy of host noise
+        walls = []
+        for _ in range(E2E_REPS):
+            if dist is not None:
+                dist.barrier()
+            w0 = time.perf_counter()
+            sio.apply_snapshot(st, ids, pos_in, vel_in)
+            ctl.start(k * dt)
+            rep = ctl.wait_for_event()
+            snap = ctl.snapshot()
+            walls.append(time.perf_counter() - w0)
+            del snap
+        snap_rows = m
+        wall = float(np.median(walls))
         full = getattr(engine.mirror_for(st, cfg), "full_pushes", 0) - full0
         ctl.stop()
-        assert rep.step_count == 3 * k, rep
+        assert rep.step_count == (E2E_WARM + E2E_REPS) * k, rep
         if dist is not None:
             import torch
             wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
@@ -551,7 +565,9 @@ def main():
                "wall_s": wall, "api": "io.apply_snapshot + SimController."
                                       "start/wait_for_event/snapshot",
                "segment": "set-state, K steps, get-state (steady state)",
-               "snapshot_rows": int(len(snap.ids))}
+               "segments": E2E_REPS, "aggregate": "median wall per segment",
+               "segment_walls_s": [round(w, 6) for w in walls],
+               "snapshot_rows": int(snap_rows)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
