@@ -387,6 +387,15 @@ def write_through_begin(store: ObjectStore, pos: np.ndarray,
     return started
 
 
+def write_through_abort(store: ObjectStore, started: list) -> None:
+    """write_through_begin's uploads turned out not to apply (the caller's
+    rows were not every slot in order): wait for them, and let the next
+    start re-send the whole mass state to those mirrors."""
+    for mir in started:
+        mir.ctx.sync()
+        mir._mass_key = None
+
+
 def write_through_covers(store: ObjectStore, started: list) -> bool:
     """Every mirror of the store took the write-through."""
     return bool(started) and len(started) == len(_mirrors.get(store) or {})

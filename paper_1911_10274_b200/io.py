@@ -114,16 +114,23 @@ def apply_snapshot(store: ObjectStore, ids: np.ndarray, positions: np.ndarray,
     n = store.mass_slot_count
     ids = np.asarray(ids)
     from . import _native
+    pos = np.ascontiguousarray(positions, np.float64)
+    vel = np.ascontiguousarray(velocities, np.float64)
     if len(ids) == n and store.mass_count == n and len(ids) and \
-            ids[0] == 0 and ids[-1] == n - 1 and _native.host_is_iota(ids):
-        # every slot, in order: whole-column copies (threaded, into the
-        # page-locked store columns); a device mirror holding the rest of
-        # the state receives the same columns meanwhile, straight from
-        # page-locked inputs (engine.write_through_begin)
+            ids[0] == 0 and ids[-1] == n - 1 and pos.size == 3 * n and \
+            vel.size == 3 * n:
+        # every slot, in order (checked below, while the upload runs):
+        # whole-column copies (threaded, into the page-locked store
+        # columns); a device mirror holding the rest of the state receives
+        # the same columns meanwhile, straight from page-locked inputs
+        # (engine.write_through_begin)
         from . import engine
-        pos = np.ascontiguousarray(positions, np.float64).reshape(n, 3)
-        vel = np.ascontiguousarray(velocities, np.float64).reshape(n, 3)
+        pos = pos.reshape(n, 3)
+        vel = vel.reshape(n, 3)
         started = engine.write_through_begin(store, pos, vel)
+        if not _native.host_is_iota(ids):  # not every slot in order
+            engine.write_through_abort(store, started)
+            return _apply_rows(store, ids, positions, velocities)
         # every device copy took the columns: the store's own copy is
         # deferred (filled from the device on first host need) instead of
         # paying a host memory copy now
@@ -136,6 +143,11 @@ def apply_snapshot(store: ObjectStore, ids: np.ndarray, positions: np.ndarray,
         finally:
             engine.write_through_end(store, started, host_copied=copy)
         return
+    _apply_rows(store, ids, positions, velocities)
+
+
+def _apply_rows(store: ObjectStore, ids, positions, velocities) -> None:
+    n = store.mass_slot_count
     if np.any(ids < 0) or np.any(ids >= n) or not np.all(store._m_alive[ids]):
         raise ScenarioError("snapshot ids do not match alive store slots")
     store._m_pos[ids] = positions

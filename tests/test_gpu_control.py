@@ -455,3 +455,41 @@ def test_lock_time_reads_of_deferred_state():
     ctl.pause()
     ctl.wait_for_event(timeout=120)
     ctl.stop()
+
+
+def test_apply_snapshot_permuted_rows_after_speculative_upload():
+    """io.apply_snapshot starts the write-through before it has checked the
+    ids are every slot in order; rows in another order (first and last in
+    place) must end up where the ids say, on the host and the device."""
+    from paper_1911_10274_b200 import _native
+    from paper_1911_10274_b200 import io as sio
+    ctl, st, _ = controller(n=4, stretch=1.02)
+    ctl.start(5 * 1e-4)
+    ctl.wait_for_event(timeout=120)
+    snap = ctl.snapshot()
+    ids = snap.ids.copy()
+    ids[[3, 7]] = ids[[7, 3]]  # swap two rows, ends in place
+    pos = _native.pinned_empty(snap.positions.shape, np.float64)
+    vel = _native.pinned_empty(snap.velocities.shape, np.float64)
+    pos[...] = snap.positions + 1e-4
+    vel[...] = snap.velocities
+    sio.apply_snapshot(st, ids, pos, vel)
+    n = st.mass_slot_count
+    want = np.empty((n, 3))
+    want[ids] = pos
+    assert st._m_pos[:n].tobytes() == want.tobytes()
+    ctl.start(5 * 1e-4)
+    ctl.wait_for_event(timeout=120)
+    got = ctl.snapshot()
+    ctl.stop()
+    st2, _ = make_lattice(4, stretch=1.02)
+    st2._m_pos[:n] = want
+    wv = np.empty((n, 3))
+    wv[ids] = vel
+    st2._m_vel[:n] = wv
+    ref = SimController(st2, free_env(), StepConfig(dt=1e-4))
+    ref.start(5 * 1e-4)
+    ref.wait_for_event(timeout=120)
+    exp = ref.snapshot()
+    ref.stop()
+    assert got.positions.tobytes() == exp.positions.tobytes()
