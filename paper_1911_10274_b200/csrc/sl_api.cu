@@ -842,8 +842,22 @@ __global__ void k_split_insert(int64_t n, const int64_t *slots, KState S,
     const bool ownA = eA >= 0 && S.sp_s[eA] == (int32_t)s && S.sp_j[eA] != sent;
     const bool ownB = eB >= 0 && S.sp_s[eB] == (int32_t)s && S.sp_j[eB] != nul;
     int32_t t0 = -1, t1 = -1, t2 = -1, t3 = -1;
+    int32_t g0 = -1, g1 = -1, g2 = -1, g3 = -1;  // fused groups touched
+    // mass of cell e: its slice's lane
+    auto mass_of_cell = [&](int64_t e) {
+      return (e / (rows * 32)) * 32 + (e & 31);
+    };
     if (ownA) t0 = (int32_t)(eA / (rows * 32) / tt);
     if (ownB) t1 = (int32_t)(eB / (rows * 32) / tt);
+    if (S.fz_gid) {
+      if (ownA) g0 = S.fz_gid[mass_of_cell(eA)];
+      if (ownB) g1 = S.fz_gid[mass_of_cell(eB)];
+      if (ab.x >= 0 && S.fz_gid[ab.x] != S.fz_gid[ab.y]) {
+        // the edit joins two fused groups: their packing changes
+        if (lane == 0) *fail = 1;
+        return;
+      }
+    }
     const bool same = ab.x >= 0 && ownA && ownB &&
                       (eA & 31) == (ab.x & 31) &&
                       eA / (rows * 32) == (ab.x >> 5) &&
@@ -906,6 +920,10 @@ __global__ void k_split_insert(int64_t n, const int64_t *slots, KState S,
         }
         t2 = (int32_t)(sl1 / tt);
         t3 = (int32_t)(sl2 / tt);
+        if (S.fz_gid) {
+          g2 = S.fz_gid[ab.x];
+          g3 = S.fz_gid[ab.y];
+        }
         const bool special = (S.mode[s] != 0 && grp[s] == 0) ||
                              ((const F *)S.thr)[s] != (F)CUDART_INF ||
                              (S.damp && S.damp[s] != 0.0);
@@ -916,11 +934,15 @@ __global__ void k_split_insert(int64_t n, const int64_t *slots, KState S,
           or_flags((typename Tr<P>::R4 *)S.vel + ab.y, MF_SPECIAL);
         }
       }
-      int32_t *tq = tiles + 4 * q;
+      int32_t *tq = tiles + 8 * q;
       tq[0] = t0;
       tq[1] = t1;
       tq[2] = t2;
       tq[3] = t3;
+      tq[4] = g0;
+      tq[5] = g1;
+      tq[6] = g2;
+      tq[7] = g3;
     }
     __syncwarp();
   }
@@ -1541,7 +1563,7 @@ int build_fused_groups(sl_ctx *c) {
       c->fz_cnt_a.as<uint8_t>(), c->fz_epos.as<uint16_t>(),
       c->fz_dict.as<float2>(), c->fz_actb.as<unsigned char>(),
       c->fz_has.as<uint8_t>(), c->fz_zero.as<uint8_t>(),
-      c->fz_gid.as<int32_t>(), c->fz_fail.as<unsigned long long>());
+      c->fz_gid.as<int32_t>(), c->fz_fail.as<unsigned long long>(), nullptr);
   CKL();
   unsigned long long failed = 0;
   CK(cudaMemcpyAsync(&failed, c->fz_fail.p, 8, cudaMemcpyDeviceToHost,
@@ -2266,14 +2288,14 @@ int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
 // step -- whenever the edit does not fit in place.
 static int insert_incremental(sl_ctx *c, int64_t n, const int64_t *slots) {
   const WinCfg &w = c->wcfg;
-  const int tt = w.tile_slices;
-  CK(c->inc_buf.ensure(align256(8 * n) + align256(16 * n) + 256));
+  const int tt = c->win ? w.tile_slices : 1 << 30;
+  CK(c->inc_buf.ensure(align256(8 * n) + align256(32 * n) + 256));
   int64_t *dsl = c->inc_buf.as<int64_t>();
   int32_t *dtiles = (int32_t *)((char *)c->inc_buf.p + align256(8 * n));
-  int *dfail = (int *)((char *)dtiles + align256(16 * n));
+  int *dfail = (int *)((char *)dtiles + align256(32 * n));
   CK(cudaMemcpyAsync(dsl, slots, 8 * n, cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(dfail, 0, sizeof(int), c->st));
-  CK(cudaMemsetAsync(dtiles, 0xFF, 16 * n, c->st));
+  CK(cudaMemsetAsync(dtiles, 0xFF, 32 * n, c->st));
   KState S = make_state(c);
   S.split = true;
   const bool act = c->agrp.n > 1;
@@ -2286,46 +2308,89 @@ static int insert_incremental(sl_ctx *c, int64_t n, const int64_t *slots) {
   CKL();
   c->launches++;
   int failed = 0;
-  std::vector<int32_t> tiles(4 * n);
+  std::vector<int32_t> out(8 * n);
   CK(cudaMemcpyAsync(&failed, dfail, sizeof(int), cudaMemcpyDeviceToHost,
                      c->st));
-  CK(cudaMemcpyAsync(tiles.data(), dtiles, 16 * n, cudaMemcpyDeviceToHost,
+  CK(cudaMemcpyAsync(out.data(), dtiles, 32 * n, cudaMemcpyDeviceToHost,
                      c->st));
   CK(cudaStreamSynchronize(c->st));
   if (failed) {
     c->layout_valid = false;
     return SL_OK;
   }
-  std::sort(tiles.begin(), tiles.end());
-  tiles.erase(std::unique(tiles.begin(), tiles.end()), tiles.end());
-  if (!tiles.empty() && tiles[0] < 0) tiles.erase(tiles.begin());
-  if (tiles.empty()) {
-    c->inc_edits++;
-    return SL_OK;
+  // touched window tiles and fused groups, each once
+  std::vector<int32_t> tiles, groups;
+  for (int64_t q = 0; q < n; q++)
+    for (int u = 0; u < 4; u++) {
+      if (out[8 * q + u] >= 0) tiles.push_back(out[8 * q + u]);
+      if (out[8 * q + 4 + u] >= 0) groups.push_back(out[8 * q + 4 + u]);
+    }
+  auto uniq = [](std::vector<int32_t> &v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  };
+  uniq(tiles);
+  uniq(groups);
+  if (c->win && !tiles.empty()) {
+    CK(cudaMemcpyAsync(dtiles, tiles.data(), 4 * tiles.size(),
+                       cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->win_fail.p, 0, 24, c->st));
+    const int64_t m_pad = c->n_slices * 32;
+    k_win_build<<<(unsigned)tiles.size(), 256, 0, c->st>>>(
+        c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
+        c->n_slices, c->m_n, c->sp_a, c->sp_rows, (uint32_t)m_pad,
+        (uint32_t)(c->n_slices << (c->sp_a + 5)), tt, w.bl, w.cap_a, w.cap_b,
+        c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
+        c->s_grp.as<uint8_t>(), c->win_rec.as<TileRec>(),
+        c->win_dict.as<float2>(), c->win_actb.as<unsigned char>(),
+        c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
+        c->prec == PREC_MIXED ? 1 : 0, c->win_fail.as<unsigned long long>(),
+        dtiles);
+    CKL();
+    c->launches++;
+    unsigned long long res[3] = {0, 0, 0};
+    CK(cudaMemcpyAsync(res, c->win_fail.p, 24, cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    const bool act_block = w.off_win > w.off_act;
+    if (res[0] || res[1] > w.cap_rec || (res[2] && !act_block)) {
+      c->layout_valid = false;  // a tile outgrew the stage: full re-index
+      return SL_OK;
+    }
   }
-  CK(cudaMemcpyAsync(dtiles, tiles.data(), 4 * tiles.size(),
-                     cudaMemcpyHostToDevice, c->st));
-  CK(cudaMemsetAsync(c->win_fail.p, 0, 24, c->st));
-  const int64_t m_pad = c->n_slices * 32;
-  k_win_build<<<(unsigned)tiles.size(), 256, 0, c->st>>>(
-      c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
-      c->n_slices, c->m_n, c->sp_a, c->sp_rows, (uint32_t)m_pad,
-      (uint32_t)(c->n_slices << (c->sp_a + 5)), tt, w.bl, w.cap_a, w.cap_b,
-      c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
-      c->s_grp.as<uint8_t>(), c->win_rec.as<TileRec>(),
-      c->win_dict.as<float2>(), c->win_actb.as<unsigned char>(),
-      c->win_zero.as<uint8_t>(), c->win_blk.as<unsigned char>(),
-      c->prec == PREC_MIXED ? 1 : 0, c->win_fail.as<unsigned long long>(),
-      dtiles);
-  CKL();
-  c->launches++;
-  unsigned long long res[3] = {0, 0, 0};
-  CK(cudaMemcpyAsync(res, c->win_fail.p, 24, cudaMemcpyDeviceToHost, c->st));
-  CK(cudaStreamSynchronize(c->st));
-  const bool act_block = w.off_win > w.off_act;
-  if (res[0] || res[1] > w.cap_rec || (res[2] && !act_block)) {
-    c->layout_valid = false;  // a tile outgrew the stage: full re-index
-    return SL_OK;
+  if (c->fz_ok && !groups.empty()) {
+    // the fused small-body layout: the touched groups re-derived from the
+    // split layout (their packing is unchanged: the edit stays inside)
+    CK(cudaMemcpyAsync(dtiles, groups.data(), 4 * groups.size(),
+                       cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->fz_fail.p, 0, 8, c->st));
+    const int64_t m_pad = c->n_slices * 32;
+    const FzCfg &f = c->fcfg;
+    auto build = f.maxm > FZ_MAXM ? k_fused_build<FZ_MAXM_L>
+                                  : k_fused_build<FZ_MAXM>;
+    build<<<(unsigned)groups.size(), f.maxm, 0, c->st>>>(
+        c->sp_j.as<uint32_t>(), c->sp_w.as<uint32_t>(), c->sp_kl.as<float2>(),
+        c->sp_s.as<int32_t>(), c->mode.as<int8_t>(), c->act.as<double4>(),
+        c->s_grp.as<uint8_t>(), c->vel.as<float4>(), c->sp_a, c->sp_rows,
+        (uint32_t)m_pad, (uint32_t)(c->n_slices << (c->sp_a + 5)),
+        c->fz_gstart.as<int32_t>(), c->fz_gcount.as<int32_t>(), f.ra, f.rb,
+        c->fz_ent.as<uint16_t>(), c->fz_code.as<uint8_t>(),
+        c->fz_perm.as<uint16_t>(), c->fz_cnt.as<uint8_t>(),
+        c->fz_cnt_a.as<uint8_t>(), c->fz_epos.as<uint16_t>(),
+        c->fz_dict.as<float2>(), c->fz_actb.as<unsigned char>(),
+        c->fz_has.as<uint8_t>(), c->fz_zero.as<uint8_t>(),
+        c->fz_gid.as<int32_t>(), c->fz_fail.as<unsigned long long>(),
+        dtiles);
+    CKL();
+    c->launches++;
+    unsigned long long ffail = 0;
+    CK(cudaMemcpyAsync(&ffail, c->fz_fail.p, 8, cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (ffail) {
+      c->layout_valid = false;
+      return SL_OK;
+    }
   }
   c->inc_edits++;
   return SL_OK;
@@ -2354,8 +2419,10 @@ int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
   // mixed production path) and the edit is small; else re-indexed on the
   // device at the next step
   static const bool no_inc = getenv("SL_NO_INCREMENTAL") != nullptr;
-  const bool inc = !no_inc && c->layout_valid && c->split && c->win &&
-                   !c->fz_ok && n <= 256;  // (serial insert: above, the re-index is faster)
+  const bool inc = !no_inc && c->layout_valid && c->split &&
+                   (c->win || c->fz_ok) && n <= 256;  // (serial insert:
+                                                      // above, the
+                                                      // re-index is faster)
   const int groups_before = c->agrp.n;
   c->layout_valid = false;
   int rc = upload_springs_impl(c, n, slots, m1, m2, m1gen, m2gen, rest, k,
@@ -2384,8 +2451,10 @@ int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
   // for the touched tiles in place (insert_incremental keeps a slot's
   // cells when its endpoints are unchanged), else a full re-index
   static const bool no_inc = getenv("SL_NO_INCREMENTAL") != nullptr;
-  const bool inc = !no_inc && c->layout_valid && c->split && c->win &&
-                   !c->fz_ok && n <= 256;  // (serial insert: above, the re-index is faster)
+  const bool inc = !no_inc && c->layout_valid && c->split &&
+                   (c->win || c->fz_ok) && n <= 256;  // (serial insert:
+                                                      // above, the
+                                                      // re-index is faster)
   const int groups_before = c->agrp.n;
   int rc = upload_springs_impl(c, n, slots, nullptr, nullptr, nullptr,
                                nullptr, rest, k, diam, yield, mode, amp, freq,

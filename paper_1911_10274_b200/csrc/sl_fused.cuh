@@ -70,14 +70,16 @@ static __global__ void __launch_bounds__(M)
                   uint8_t *cnt_a, uint16_t *epos, float2 *dict,
                   unsigned char *actb,
                   uint8_t *has_act, uint8_t *zero, int32_t *gid,
-                  unsigned long long *fail) {
+                  unsigned long long *fail,
+                  const int32_t *group_list = nullptr) {
   __shared__ int16_t scnt[M];
   __shared__ unsigned long long dkey[WIN_DMAX];
   __shared__ float2 dkl[WIN_DMAX];
   __shared__ double4 dact[WIN_DMAX];
   __shared__ int8_t dmode[WIN_DMAX];
   __shared__ int ok;
-  const int64_t g = blockIdx.x;
+  // every group, or (O(edits) topology sync) the listed ones
+  const int64_t g = group_list ? group_list[blockIdx.x] : blockIdx.x;
   const int li = threadIdx.x;
   const int32_t g0 = gstart[g], gn = gcount[g];
   const int64_t i = (int64_t)g0 + li;

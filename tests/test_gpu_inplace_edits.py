@@ -97,3 +97,54 @@ def test_edits_apply_in_place(precision):
     # deletes are kills in place; creations / retunes re-wired in place:
     # no device re-index after the first build
     assert sfin["layout_builds"] == st0["layout_builds"], (st0, sfin)
+
+
+def swarm(n_bodies=24):
+    st = ObjectStore()
+    bodies = []
+    for b in range(n_bodies):
+        bodies.append(build_lattice(LatticeSpec(
+            Vec3(0.4 * (b % 6), 0.4 * (b // 6), 0.002), 4, 4, 4, 0.05,
+            Material(1e5, 1000.0)), st))
+    env = Environment(gravity=Vec3(0, 0, -9.81), contacts=[ContactPlane(
+        normal=Vec3(0, 0, 1), offset=0.0, stiffness=2000.0,
+        static_friction=1.0, kinetic_friction=0.8)])
+    return st, env
+
+
+def test_edits_apply_in_place_on_fused_bodies():
+    """Small bodies run as fused groups (all steps of a call in one launch,
+    sl_fused.cuh); deleting and re-adding springs inside a body re-derives
+    only its group (k_fused_build over a group list) next to the split /
+    window layouts' in-place sync."""
+    rng = np.random.default_rng(11)
+    st, env = swarm()
+    cfg = StepConfig(dt=DT, precision="fp32")
+    t = engine.run_steps(st, env, cfg, 10)
+    mir = engine.mirror_for(st, cfg)
+    s0 = mir.ctx.stats()
+    assert s0["fused_groups"] > 0, s0
+    removed = []
+    for kind in ("delete", "create", "retune", "delete", "create"):
+        edit(st, rng, kind, removed)
+        case = case_of(st, env)
+        n = 30
+        times = engine.step_times(n + 1, DT, t, "accumulate")
+        f0 = mir.ctx.stats()["fused_launches"]
+        t_next = engine.run_steps(st, env, cfg, n, t0=t)
+        assert mir.ctx.stats()["fused_launches"] > f0  # still fused
+        ref = orc.OracleSim(case)
+        for k in range(n):
+            assert ref.step(float(times[k]), DT) == 0
+        m, s = st.mass_slot_count, st.spring_slot_count
+        st.reconcile_spring_deaths()
+        assert np.array_equal(st._s_alive[:s], ref.c["s_alive"]), kind
+        assert rel_maxnorm(st._m_pos[:m], ref.c["m_pos"]) < 1e-4, kind
+        assert rel_maxnorm(st._m_vel[:m], ref.c["m_vel"]) < 1e-4, kind
+        st._m_pos[:m] = ref.c["m_pos"]
+        st._m_vel[:m] = ref.c["m_vel"]
+        st._m_acc[:m] = ref.c["m_acc"]
+        t = t_next
+    sfin = mir.ctx.stats()
+    assert sfin["inplace_edits"] == 3, sfin
+    assert sfin["layout_builds"] == s0["layout_builds"], (s0, sfin)
