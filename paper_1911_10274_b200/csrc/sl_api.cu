@@ -948,6 +948,168 @@ __global__ void k_split_insert(int64_t n, const int64_t *slots, KState S,
   }
 }
 
+// O(edits) topology sync on the EXACT layout (fp64 parity mode): a mass's
+// entries are kept in ascending spring slot (the reference's serial
+// order), so an entry is inserted at its sorted row -- the live entries
+// between it and the nearest free row (dead or padding) move over by one
+// row, their springs' e1 / e2 following.  A written slot whose wiring is
+// unchanged gets its (k, L0) / special bit refreshed in place; a re-wired
+// or dead slot's entries become dead.  One warp, slots in order; the
+// touched window tiles are listed (the fp64 window is re-derived for
+// them).  fail = 1: a lane has no free row within its slice width.
+template <int P>
+__global__ void k_exact_insert(int64_t n, const int64_t *slots, KState S,
+                               int tt, int32_t *tiles, int *fail) {
+  using F = typename Tr<P>::F;
+  using F2 = typename Tr<P>::F2;
+  const int lane = threadIdx.x;
+  int64_t *E1 = (int64_t *)S.e1, *E2 = (int64_t *)S.e2;
+  int32_t *ES = (int32_t *)S.ent_s;
+  F2 *EK = (F2 *)S.ent_kL0;
+  auto mine = [&](int64_t e, int64_t s) {  // entry e is still s's
+    return e >= 0 && ES[e] == (int32_t)s;
+  };
+  auto owned = [&](int64_t e, int64_t s) {  // ... and alive
+    return mine(e, s) && !(S.ent_j[e] & EJ_DEAD);
+  };
+  // insert the entry of spring s at mass i (side 0: m1, 1: m2)
+  auto insert = [&](int64_t s, int64_t i, uint32_t ej) -> int64_t {
+    const int64_t sl = i >> 5, l = i & 31;
+    const int64_t base = S.slice_ptr[sl];
+    const int width = (int)((S.slice_ptr[sl + 1] - base) >> 5);
+    // rows: live with slot < s (before), live with slot > s, free
+    int p = width, f_after = -1, f_before = -1;
+    for (int b = 0; b < width; b += 32) {
+      const int r = b + lane;
+      bool live = false, after = false;
+      if (r < width) {
+        const int64_t e = base + 32 * (int64_t)r + l;
+        live = !(S.ent_j[e] & EJ_DEAD);
+        after = live && ES[e] > (int32_t)s;
+      }
+      const unsigned ma = __ballot_sync(0xffffffffu, after);
+      if (ma && p == width) p = b + __ffs(ma) - 1;
+    }
+    for (int b = 0; b < width; b += 32) {
+      // first free row at or after p, last free row before p
+      const int r = b + lane;
+      const bool fr = r < width &&
+                      (S.ent_j[base + 32 * (int64_t)r + l] & EJ_DEAD);
+      const unsigned fa = __ballot_sync(0xffffffffu, fr && r >= p);
+      const unsigned fb = __ballot_sync(0xffffffffu, fr && r < p);
+      if (fa && f_after < 0) f_after = b + __ffs(fa) - 1;
+      if (fb) f_before = b + 31 - __clz(fb);
+    }
+    if (f_after < 0 && f_before < 0) return -1;
+    int64_t at;
+    if (lane == 0) {
+      auto mv = [&](int from, int to) {  // move a live entry one row
+        const int64_t ef = base + 32 * (int64_t)from + l;
+        const int64_t et = base + 32 * (int64_t)to + l;
+        const uint32_t jr = S.ent_j[ef];
+        const int32_t so = ES[ef];
+        S.ent_j[et] = jr;
+        EK[et] = EK[ef];
+        ES[et] = so;
+        ((jr & EJ_M2) ? E2 : E1)[so] = et;
+      };
+      if (f_after >= 0) {
+        for (int r = f_after; r > p; r--) mv(r - 1, r);
+        at = base + 32 * (int64_t)p + l;
+      } else {
+        for (int r = f_before; r < p - 1; r++) mv(r + 1, r);
+        at = base + 32 * (int64_t)(p - 1) + l;
+      }
+      S.ent_j[at] = ej;
+      EK[at] = ((const F2 *)S.kL0)[s];
+      ES[at] = (int32_t)s;
+    }
+    return __shfl_sync(0xffffffffu, lane == 0 ? at : 0, 0);
+  };
+  for (int64_t q = 0; q < n; q++) {
+    const int64_t s = slots[q];
+    const int2 ab = S.ends[s];
+    const int64_t eA = E1[s], eB = E2[s];
+    const bool ownA = owned(eA, s), ownB = owned(eB, s);
+    int32_t t[4] = {-1, -1, -1, -1};
+    const bool special = ab.x >= 0 &&
+                         (S.mode[s] != 0 ||
+                          ((const F *)S.thr)[s] != (F)CUDART_INF ||
+                          (S.damp && S.damp[s] != 0.0));
+    // entry e sits in mass i's column: i's slice range, i's lane
+    auto at_mass = [&](int64_t e, int64_t i) {
+      return (e & 31) == (i & 31) && e >= S.slice_ptr[i >> 5] &&
+             e < S.slice_ptr[(i >> 5) + 1];
+    };
+    const bool same = ab.x >= 0 && ownA && ownB &&
+                      (S.ent_j[eA] & EJ_MASK) == (uint32_t)ab.y &&
+                      (S.ent_j[eB] & EJ_MASK) == (uint32_t)ab.x &&
+                      at_mass(eA, ab.x) && at_mass(eB, ab.y);
+    if (same) {
+      if (lane == 0) {
+        const F2 kl = ((const F2 *)S.kL0)[s];
+        EK[eA] = kl;
+        EK[eB] = kl;
+        const uint32_t sp = special ? EJ_SPECIAL : 0u;
+        S.ent_j[eA] = (S.ent_j[eA] & ~EJ_SPECIAL) | sp;
+        S.ent_j[eB] = (S.ent_j[eB] & ~EJ_SPECIAL) | sp;
+      }
+    } else {
+      if (lane == 0) {
+        // the previous wiring's entries (live, or killed since: their
+        // partner fields still name the old endpoints, whose tiles the
+        // window re-derives) become dead and unowned
+        int2 old = make_int2(-1, -1);
+        if (mine(eA, s)) {
+          old.y = (int)(S.ent_j[eA] & EJ_MASK);
+          S.ent_j[eA] |= EJ_DEAD;
+          ES[eA] = -1;
+        }
+        if (mine(eB, s)) {
+          old.x = (int)(S.ent_j[eB] & EJ_MASK);
+          S.ent_j[eB] |= EJ_DEAD;
+          ES[eB] = -1;
+        }
+        E1[s] = -1;
+        E2[s] = -1;
+        t[0] = old.x >= 0 ? (int32_t)((old.x >> 5) / tt) : -1;
+        t[1] = old.y >= 0 ? (int32_t)((old.y >> 5) / tt) : -1;
+      }
+      __syncwarp();
+      if (ab.x >= 0) {
+        const uint32_t sp = special ? EJ_SPECIAL : 0u;
+        const int64_t a1 = insert(s, ab.x, (uint32_t)ab.y | sp);
+        __syncwarp();
+        const int64_t a2 =
+            a1 < 0 ? -1 : insert(s, ab.y, (uint32_t)ab.x | EJ_M2 | sp);
+        if (a1 < 0 || a2 < 0) {
+          if (lane == 0) *fail = 1;
+          return;
+        }
+        if (lane == 0) {
+          E1[s] = a1;
+          E2[s] = a2;
+        }
+      }
+    }
+    if (lane == 0) {
+      if (ab.x >= 0) {
+        t[2] = (int32_t)((ab.x >> 5) / tt);
+        t[3] = (int32_t)((ab.y >> 5) / tt);
+        if (special) {
+          S.xflags[ab.x] = 1;
+          S.xflags[ab.y] = 1;
+          or_flags((typename Tr<P>::R4 *)S.vel + ab.x, MF_SPECIAL);
+          or_flags((typename Tr<P>::R4 *)S.vel + ab.y, MF_SPECIAL);
+        }
+      }
+      int32_t *tq = tiles + 8 * q;
+      for (int u = 0; u < 4; u++) tq[u] = t[u];
+    }
+    __syncwarp();
+  }
+}
+
 KState make_state(sl_ctx *c) {
   KState S;
   memset(&S, 0, sizeof S);
@@ -1017,6 +1179,9 @@ KState make_state(sl_ctx *c) {
       S.win_sb = c->wcfg.bl.slice_bytes;
       S.win_tt = c->wcfg.tile_slices;
     }
+  } else if (c->win && c->prec == PREC_FP64) {  // parity-mode window
+    S.win_blk = c->win_blk.as<unsigned char>();
+    S.win_sb = c->wcfg.bl.slice_bytes;
   }
   return S;
 }
@@ -2396,6 +2561,70 @@ static int insert_incremental(sl_ctx *c, int64_t n, const int64_t *slots) {
   return SL_OK;
 }
 
+// The same on the EXACT layout (fp64 parity mode): k_exact_insert keeps
+// each mass's entries in ascending slot order, then the fp64 window layout
+// is re-derived for the touched tiles (k_win64_build over a tile list).
+static int insert_incremental_exact(sl_ctx *c, int64_t n,
+                                    const int64_t *slots) {
+  const WinCfg &w = c->wcfg;
+  const int tt = c->win ? w.tile_slices : 1 << 30;
+  CK(c->inc_buf.ensure(align256(8 * n) + align256(32 * n) + 256));
+  int64_t *dsl = c->inc_buf.as<int64_t>();
+  int32_t *dtiles = (int32_t *)((char *)c->inc_buf.p + align256(8 * n));
+  int *dfail = (int *)((char *)dtiles + align256(32 * n));
+  CK(cudaMemcpyAsync(dsl, slots, 8 * n, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(dfail, 0, sizeof(int), c->st));
+  CK(cudaMemsetAsync(dtiles, 0xFF, 32 * n, c->st));
+  KState S = make_state(c);
+  auto k = c->prec == PREC_FP64   ? k_exact_insert<PREC_FP64>
+           : c->prec == PREC_FP32 ? k_exact_insert<PREC_FP32>
+                                  : k_exact_insert<PREC_MIXED>;
+  k<<<1, 32, 0, c->st>>>(n, dsl, S, tt, dtiles, dfail);
+  CKL();
+  c->launches++;
+  int failed = 0;
+  std::vector<int32_t> out(8 * n);
+  CK(cudaMemcpyAsync(&failed, dfail, sizeof(int), cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaMemcpyAsync(out.data(), dtiles, 32 * n, cudaMemcpyDeviceToHost,
+                     c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (failed) {
+    c->layout_valid = false;
+    return SL_OK;
+  }
+  std::vector<int32_t> tiles;
+  for (int64_t q = 0; q < n; q++)
+    for (int u = 0; u < 4; u++)
+      if (out[8 * q + u] >= 0) tiles.push_back(out[8 * q + u]);
+  std::sort(tiles.begin(), tiles.end());
+  tiles.erase(std::unique(tiles.begin(), tiles.end()), tiles.end());
+  if (c->win && !tiles.empty()) {
+    CK(cudaMemcpyAsync(dtiles, tiles.data(), 4 * tiles.size(),
+                       cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemsetAsync(c->win_fail.p, 0, 16, c->st));
+    const int64_t m_pad = c->n_slices * 32;
+    k_win64_build<<<(unsigned)tiles.size(), 256, 0, c->st>>>(
+        S.slice_ptr, c->ent_j.as<uint32_t>(), c->ent_kL0.as<double2>(),
+        c->n_slices, c->m_n, (uint32_t)m_pad, tt, w.bl, w.cap_a,
+        c->win_rec.as<TileRec>(), c->win_dict.as<double2>(),
+        c->win_blk.as<unsigned char>(), c->win_fail.as<unsigned long long>(),
+        dtiles);
+    CKL();
+    c->launches++;
+    unsigned long long res[2] = {0, 0};
+    CK(cudaMemcpyAsync(res, c->win_fail.p, 16, cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaStreamSynchronize(c->st));
+    if (res[0] || res[1] > w.cap_rec) {
+      c->layout_valid = false;  // a tile outgrew the stage: full re-index
+      return SL_OK;
+    }
+  }
+  c->inc_edits++;
+  return SL_OK;
+}
+
 int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
                      const int64_t *m1, const int64_t *m2,
                      const int64_t *m1gen, const int64_t *m2gen,
@@ -2423,12 +2652,19 @@ int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
                    (c->win || c->fz_ok) && n <= 256;  // (serial insert:
                                                       // above, the
                                                       // re-index is faster)
+  const bool inc_exact = !no_inc && c->layout_valid && !c->split &&
+                         n <= 256;
   const int groups_before = c->agrp.n;
   c->layout_valid = false;
   int rc = upload_springs_impl(c, n, slots, m1, m2, m1gen, m2gen, rest, k,
                                diam, yield, mode, amp, freq, off, per, alive,
                                degen, false);
-  if (rc || !inc || c->agrp.n != groups_before) return rc;
+  if (rc) return rc;
+  if (inc_exact) {
+    c->layout_valid = true;
+    return insert_incremental_exact(c, n, slots);
+  }
+  if (!inc || c->agrp.n != groups_before) return rc;
   c->layout_valid = true;
   return insert_incremental(c, n, slots);
 }
@@ -2455,11 +2691,18 @@ int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
                    (c->win || c->fz_ok) && n <= 256;  // (serial insert:
                                                       // above, the
                                                       // re-index is faster)
+  const bool inc_exact = !no_inc && c->layout_valid && !c->split &&
+                         c->win && n <= 256;
   const int groups_before = c->agrp.n;
   int rc = upload_springs_impl(c, n, slots, nullptr, nullptr, nullptr,
                                nullptr, rest, k, diam, yield, mode, amp, freq,
                                off, per, nullptr, nullptr, true);
-  if (rc || !inc || c->agrp.n != groups_before) return rc;
+  if (rc) return rc;
+  if (inc_exact) {  // (k, L0) refreshed in place; the tiles' tables
+    c->layout_valid = true;
+    return insert_incremental_exact(c, n, slots);
+  }
+  if (!inc || c->agrp.n != groups_before) return rc;
   c->layout_valid = true;
   return insert_incremental(c, n, slots);
 }
@@ -2481,8 +2724,8 @@ int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
   k_kill_springs<<<blocks_for(n), 256, 0, c->st>>>(n, ds, S, c->layout_valid);
   CKL();
   c->launches++;
-  // the parity-mode window blocks are not edited in place: re-index
-  if (c->win && !c->split) c->layout_valid = false;
+  // (the parity-mode window: kill_entries sets the entry words' skip bit;
+  // the tiles' windows and tables stay a valid superset)
   CK(cudaStreamSynchronize(c->st));
   return SL_OK;
 }

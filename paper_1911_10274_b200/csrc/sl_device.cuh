@@ -1311,8 +1311,26 @@ __device__ __forceinline__ void kill_entries(const KState &S, int64_t s) {
     }
     return;
   }
-  if (S.e1[s] >= 0) S.ent_j[S.e1[s]] |= EJ_DEAD;
-  if (S.e2[s] >= 0) S.ent_j[S.e2[s]] |= EJ_DEAD;
+  // (only entries still this spring's: in-place insertion re-uses rows)
+  const int64_t es[2] = {S.e1[s], S.e2[s]};
+  for (int q = 0; q < 2; q++) {
+    const int64_t e = es[q];
+    if (e < 0 || S.ent_s[e] != (int32_t)s) continue;
+    S.ent_j[e] |= EJ_DEAD;
+    if (S.win_blk) {  // parity-mode window: the entry word's skip bit
+      // (k_win64_build: entry e = slice_ptr[w] + 32 row + lane <-> word
+      // ew_off(row, lane) of slice w's block)
+      int64_t lo = 0, hi = (S.m_n + 31) >> 5;  // slice_ptr[lo] <= e < [hi]
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (S.slice_ptr[mid] <= e) lo = mid; else hi = mid;
+      }
+      const int rel = (int)(e - S.slice_ptr[lo]);
+      *(uint32_t *)(S.win_blk + lo * S.win_sb +
+                    (uint32_t)((rel >> 6) * 256 + (rel & 31) * 8 +
+                               ((rel >> 5) & 1) * 4)) |= 1u;
+    }
+  }
 }
 
 // Owner-aggregated atomic accumulation on the EXACT layout (fp64 and the

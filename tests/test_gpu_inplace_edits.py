@@ -64,7 +64,7 @@ def edit(st, rng, kind, removed):
                                 float(rng.uniform(100, 900)))
 
 
-@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+@pytest.mark.parametrize("precision", ["fp32", "mixed", "fp64"])
 def test_edits_apply_in_place(precision):
     rng = np.random.default_rng(7)
     st, env, body = world()
@@ -72,7 +72,7 @@ def test_edits_apply_in_place(precision):
     t = engine.run_steps(st, env, cfg, 10)
     mir = engine.mirror_for(st, cfg)
     st0 = mir.ctx.stats()
-    assert st0["step_path"] == 5, st0  # the window kernel
+    assert st0["step_path"] in (5, 6), st0  # the window kernel
     removed = []
     for kind in ("delete", "create", "retune", "delete", "create"):
         edit(st, rng, kind, removed)
@@ -86,8 +86,12 @@ def test_edits_apply_in_place(precision):
         m, s = st.mass_slot_count, st.spring_slot_count
         st.reconcile_spring_deaths()
         assert np.array_equal(st._s_alive[:s], ref.c["s_alive"]), kind
-        assert rel_maxnorm(st._m_pos[:m], ref.c["m_pos"]) < 1e-4, kind
-        assert rel_maxnorm(st._m_vel[:m], ref.c["m_vel"]) < 1e-4, kind
+        if precision == "fp64":  # the exact layout: bit for bit
+            assert st._m_pos[:m].tobytes() == ref.c["m_pos"].tobytes(), kind
+            assert st._m_vel[:m].tobytes() == ref.c["m_vel"].tobytes(), kind
+        else:
+            assert rel_maxnorm(st._m_pos[:m], ref.c["m_pos"]) < 1e-4, kind
+            assert rel_maxnorm(st._m_vel[:m], ref.c["m_vel"]) < 1e-4, kind
         st._m_pos[:m] = ref.c["m_pos"]
         st._m_vel[:m] = ref.c["m_vel"]
         st._m_acc[:m] = ref.c["m_acc"]
