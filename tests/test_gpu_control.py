@@ -493,3 +493,20 @@ def test_apply_snapshot_permuted_rows_after_speculative_upload():
     exp = ref.snapshot()
     ref.stop()
     assert got.positions.tobytes() == exp.positions.tobytes()
+
+
+def test_batch_cap_follows_device_time_not_first_batch_wall():
+    """A slow first batch (layout build, first touch) must not pin the
+    controller at one-step batches: the cap follows the step kernels'
+    device time, so it recovers and later segments run as one launch."""
+    ctl, st, _ = controller(n=20, stretch=1.01)
+    ctl._sec_per_step = 0.05  # as if a 1-step batch had taken 50 ms
+    launches = []
+    for seg in range(5):
+        before = ctl.device_launches
+        ctl.start(20 * 1e-4)
+        ctl.wait_for_event(timeout=120)
+        launches.append(ctl.device_launches - before)
+    assert launches[0] > 1 and launches[-2:] == [1, 1], launches
+    assert ctl._sec_per_step < 1e-3
+    ctl.stop()
