@@ -336,7 +336,11 @@ __device__ __forceinline__ double act_factor(const KState &S, int64_t s,
 
 __device__ __forceinline__ bool stopped(const KState &S, int64_t step) {
   // a strictly earlier step of this launch went non-finite: do nothing
-  unsigned long long e = *(volatile unsigned long long *)(S.status + 4);
+  // (written only by earlier launches -- every caller reads it after
+  // griddepcontrol.wait -- so an L2 load sees it; a volatile load was a
+  // system-scope LDG.STRONG.SYS per thread, the first stall of k_mass)
+  const unsigned long long e =
+      __ldcg((const unsigned long long *)(S.status + 4));
   return e != 0ull && (int64_t)e - 1 < step;
 }
 
@@ -1448,12 +1452,18 @@ static __global__ void __launch_bounds__(256)
   using R4 = typename Tr<P>::R4;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S.m_n) return;
-  if (stopped(S, T.step)) return;
+  // every load of the mass issued up front (one round trip, not a chain
+  // of flag -> f_ext -> position; the r3 ncu: long-scoreboard 149 per issue)
+  const bool stop = stopped(S, T.step);
   const R4 v = ((const R4 *)S.vel)[i];
-  const uint32_t fl = flags_of(v.w);
-  if (!(fl & MF_ALIVE)) return;
   R4 *fe = (R4 *)S.fext + i;
   const R4 f0 = *fe;
+  const R4 me = ((const R4 *)S.pos[T.cur])[i];
+  const auto ml = lo_at<P>(me, S.plo[T.cur], i);
+  const R mass = mass_of<P>(S, me, i);
+  if (stop) return;
+  const uint32_t fl = flags_of(v.w);
+  if (!(fl & MF_ALIVE)) return;
   if (fl & MF_FIXED) {
     fixed_mass<P>(S, T, i, v, fl | MF_FEXT);
     return;
@@ -1461,9 +1471,7 @@ static __global__ void __launch_bounds__(256)
   R4 z;
   z.x = z.y = z.z = z.w = (R)0.0;
   *fe = z;
-  const R4 me = ((const R4 *)S.pos[T.cur])[i];
-  integrate<P>(S, E, T, i, me, lo_at<P>(me, S.plo[T.cur], i),
-               mass_of<P>(S, me, i), v, fl, f0.x, f0.y, f0.z);
+  integrate<P>(S, E, T, i, me, ml, mass, v, fl, f0.x, f0.y, f0.z);
 }
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }

@@ -156,6 +156,7 @@ class DeviceMirror:
             store.adopt_mass_allocator(_native.pinned_empty)
         m, s = store.mass_slot_count, store.spring_slot_count
         touched = store.take_touched()
+        full = False  # a whole-column mass upload happened
         if masses or self.ctx.m_n != m:
             # the device holds the host state when nothing but this mirror
             # moved it since the last sync (same arrays, no steps since);
@@ -169,6 +170,7 @@ class DeviceMirror:
                     "_m_pos", "_m_vel", "_m_acc", "_m_fext", "_m_load",
                     "_m_mass", "_m_fixed", "_m_alive", "_m_gen")))
                 self.full_pushes = getattr(self, "full_pushes", 0) + 1
+                full = True
             elif touched:
                 self.ctx.write_state(
                     *(raw(c)[:m] if c in touched else None
@@ -201,10 +203,11 @@ class DeviceMirror:
             self.ctx.set_spring_damping(store._s_damp[:s])
             self._damp_key = key
             self._damp_sent = True
-        ckey = (m, store.constraint_version, store._column_id("_m_pos"))
-        if ckey != self._constraints_key or masses:
-            # the CSR is rebuilt only when the constraints change; a mass
-            # upload re-sends the cached one
+        ckey = (m, store.constraint_version)
+        if ckey != self._constraints_key or full:
+            # the CSR is rebuilt only when the constraints change; a whole
+            # mass upload re-sends the cached one (state-only writes keep
+            # the device's constraint flags)
             if ckey != self._constraints_key or self._lc_csr is None:
                 self._lc_csr = local_constraint_csr(store)
             self.ctx.set_local_constraints(*self._lc_csr)
@@ -260,8 +263,14 @@ class DeviceMirror:
     def set_env(self, store: ObjectStore, env: Environment):
         planes, balls = flatten_contacts(env)
         gk, gv = global_constraint_arrays(store)
-        self.ctx.set_environment(env.gravity.as_array(), env.drag_coeff,
-                                 planes, balls, gk, gv, V_STICK)
+        g = np.asarray(env.gravity.as_array(), np.float64)
+        key = (g.tobytes(), float(env.drag_coeff), planes.tobytes(),
+               balls.tobytes(), gk.tobytes(), gv.tobytes())
+        if key == getattr(self, "_env_key", None):
+            return  # the device already holds this environment
+        self.ctx.set_environment(g, env.drag_coeff, planes, balls, gk, gv,
+                                 V_STICK)
+        self._env_key = key
 
     @property
     def has_custom(self) -> bool:
