@@ -337,10 +337,11 @@ __device__ __forceinline__ double act_factor(const KState &S, int64_t s,
 __device__ __forceinline__ bool stopped(const KState &S, int64_t step) {
   // a strictly earlier step of this launch went non-finite: do nothing
   // (written only by earlier launches -- every caller reads it after
-  // griddepcontrol.wait -- so an L2 load sees it; a volatile load was a
-  // system-scope LDG.STRONG.SYS per thread, the first stall of k_mass)
+  // griddepcontrol.wait -- so the read-only path sees it, and every warp
+  // after an SM's first hits L1, instead of a volatile system-scope
+  // LDG.STRONG.SYS per thread to one L2 line)
   const unsigned long long e =
-      __ldcg((const unsigned long long *)(S.status + 4));
+      __ldg((const unsigned long long *)(S.status + 4));
   return e != 0ull && (int64_t)e - 1 < step;
 }
 
@@ -1468,10 +1469,14 @@ static __global__ void __launch_bounds__(256)
     fixed_mass<P>(S, T, i, v, fl | MF_FEXT);
     return;
   }
+  integrate<P>(S, E, T, i, me, ml, mass, v, fl, f0.x, f0.y, f0.z);
+  // f_ext cleared after the update's stores: a constant store issued while
+  // the load of the same line is still in flight (the compiler hoisted it
+  // there) held the SM's later memory instructions behind that miss --
+  // 57 us instead of ~21 on config B (tools/probe/kmass_probe.cu)
   R4 z;
   z.x = z.y = z.z = z.w = (R)0.0;
   *fe = z;
-  integrate<P>(S, E, T, i, me, ml, mass, v, fl, f0.x, f0.y, f0.z);
 }
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
