@@ -21,6 +21,7 @@ b E1 --config E --steps 100 --warmup 5
 # checks, O(edits) topology sync vs the device re-index
 timeout 600 python tools/e2e_settle.py --steps 20 > $out/e2e_settle_B.txt 2>&1
 timeout 600 python tools/e2e_settle.py --steps 20 --config D > $out/e2e_settle_D.txt 2>&1
+timeout 600 python tools/e2e_trace.py --steps 20 > $out/e2e_trace_B20.txt 2>&1
 timeout 600 python tools/predicate_bench.py > $out/predicate.txt 2>&1
 timeout 900 python tools/edit_latency.py > $out/edit_latency.txt 2>&1
 SL_NO_INCREMENTAL=1 timeout 900 python tools/edit_latency.py > $out/edit_latency_full.txt 2>&1
@@ -35,6 +36,7 @@ cap win_fp64 k_win_tma 6 --precision fp64
 cap win_mixed k_win_tma 6 --precision mixed
 cap fused k_fused_small 0 --config D
 cap split_atomic k_split_atomic 3 --accumulation atomic
+cap mass k_mass 3 --accumulation atomic
 cap win_E200 k_win_tma 6 --config E
 s() { echo "## $*"; timeout 1800 compute-sanitizer "$@" 2>&1 | grep -E "passed|failed|SUMMARY|ERROR" | tail -4; }
 {

@@ -26,7 +26,7 @@ with open(os.path.join(DST, "bench_lines.json"), "w") as fh:
     json.dump(lines, fh, indent=1)
 for f in ("pytest.txt", "smoke.txt", "sanitizer.txt", "e2e_settle_B.txt",
           "e2e_settle_D.txt", "predicate.txt", "edit_latency.txt",
-          "edit_latency_full.txt", "build_timing.txt"):
+          "edit_latency_full.txt", "build_timing.txt", "e2e_trace_B20.txt"):
     if os.path.exists(os.path.join(SRC, f)):
         shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
 
@@ -61,7 +61,7 @@ if os.path.exists(p):
 algo = {"win_fp32": lines.get("default", {}).get("roofline", {}).get(
             "algorithmic_bytes_per_step"),
         "win_fp64": 409563104, "win_mixed": 307708736,
-        "fused": None, "split_atomic": None,
+        "fused": None, "split_atomic": None, "mass": None,
         "win_E200": lines.get("E1", {}).get("roofline", {}).get(
             "algorithmic_bytes_per_step_per_gpu")}
 traffic = {"_source": "ncu --set full (profiles/r3/ncu_*.txt): "
