@@ -1387,12 +1387,15 @@ void configure_split_tma(sl_ctx *c, const std::vector<uint32_t> &widths) {
   c->split_warps = 0;
   if (!c->tma_enabled || c->n_slices == 0) return;
   const bool act = c->agrp.n > 1;
-  // fp64 state doubles the gather registers: batches of 4 (r1e sweep)
-  const int cands_fp32[] = {4, 8, 13}, cands_act[] = {4, 8}, cands_mixed[] = {4};
+  // fp64 state doubles the gather registers: batches of 4 (r1e sweep);
+  // fp32 batches of 13 spill since the compensated positions (config B:
+  // 140.7 us against 101.2 for 4 and 102.9 for 8, profiles/r3/
+  // sweep_split_u_warps.txt)
+  const int cands_fp32[] = {4, 8}, cands_act[] = {4, 8}, cands_mixed[] = {4};
   const int *cands = c->prec != PREC_FP32 ? cands_mixed
                      : act                ? cands_act
                                           : cands_fp32;
-  const int n_cands = c->prec != PREC_FP32 ? 1 : act ? 2 : 3;
+  const int n_cands = c->prec != PREC_FP32 ? 1 : 2;
   int best_u = 4;
   double best = 1e300;
   for (int q = 0; q < n_cands; q++) {

@@ -1365,24 +1365,44 @@ static __global__ void __launch_bounds__(256)
   const int width = (int)((S.slice_ptr[w + 1] - S.slice_ptr[w]) >> 5);
   R4 *fe = (R4 *)S.fext;
   R ox = 0, oy = 0, oz = 0;
-  for (int t = 0; t < width; t++) {
-    const int64_t e = ebase + 32 * (int64_t)t;
-    const uint32_t jr = __ldg(S.ent_j + e);
-    if (jr & (EJ_DEAD | EJ_M2)) continue;  // dead, padding, or m2 side
-    const uint32_t j = jr & EJ_MASK;
-    const R4 o = pos[j];
-    // entry_force on a zeroed accumulator: the m1-side force itself
-    R gx = 0, gy = 0, gz = 0;
-    const int32_t s = S.ent_s[e];
-    const bool was_alive = S.s_alive[s] != 0;
-    if (!entry_force<P>(S, e, jr, me, ml, o, lo_at<P>(o, plo, j),
-                        ((const F2 *)S.ent_kL0)[e], T.sim_t, gx, gy, gz))
-      continue;
-    if (was_alive && !S.s_alive[s]) kill_entries(S, s);  // broke: both
-    ox += gx;
-    oy += gy;
-    oz += gz;
-    red_add(fe + j, -gx, -gy, -gz);
+  // four entries' words, partners and (k, L0) requested together, then
+  // evaluated one by one in slot order (the r3 ncu: one dependent
+  // entry -> partner round trip per entry, long-scoreboard 26 per issue)
+  constexpr int U = 4;
+  for (int t0 = 0; t0 < width; t0 += U) {
+    uint32_t jr[U];
+    R4 o[U];
+    F2 kl[U];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      jr[u] = t0 + u < width ? __ldg(S.ent_j + ebase + 32 * (int64_t)(t0 + u))
+                             : EJ_PAD;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (jr[u] & (EJ_DEAD | EJ_M2)) continue;  // dead, padding, m2 side
+      o[u] = pos[jr[u] & EJ_MASK];
+      kl[u] = ((const F2 *)S.ent_kL0)[ebase + 32 * (int64_t)(t0 + u)];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (jr[u] & (EJ_DEAD | EJ_M2)) continue;
+      const int64_t e = ebase + 32 * (int64_t)(t0 + u);
+      const uint32_t j = jr[u] & EJ_MASK;
+      // entry_force on a zeroed accumulator: the m1-side force itself
+      R gx = 0, gy = 0, gz = 0;
+      // a yield break (special entries only) kills both entries
+      const bool sp = (jr[u] & EJ_SPECIAL) != 0;
+      const int32_t s = sp ? S.ent_s[e] : 0;
+      const bool was_alive = sp && S.s_alive[s] != 0;
+      if (!entry_force<P>(S, e, jr[u], me, ml, o[u], lo_at<P>(o[u], plo, j),
+                          kl[u], T.sim_t, gx, gy, gz))
+        continue;
+      if (was_alive && !S.s_alive[s]) kill_entries(S, s);
+      ox += gx;
+      oy += gy;
+      oz += gz;
+      red_add(fe + j, -gx, -gy, -gz);
+    }
   }
   red_add(fe + i, ox, oy, oz);
 }

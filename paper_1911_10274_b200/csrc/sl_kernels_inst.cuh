@@ -96,9 +96,7 @@ struct SplitLaunch {
     switch (C.u) {
       case 4: tma_u<4, false>(S, E, T, C, A, grid, st); break;
       case 8: tma_u<8, false>(S, E, T, C, A, grid, st); break;
-      default:
-        if constexpr (P == PREC_FP32) tma_u<13, false>(S, E, T, C, A, grid, st);
-        else tma_u<8, false>(S, E, T, C, A, grid, st);
+      default: tma_u<8, false>(S, E, T, C, A, grid, st);
     }
   }
   // tiled window kernel (fp32 and mixed)
@@ -171,8 +169,7 @@ struct SplitLaunch {
       case 4: return setup_u<4, false>(smem_bytes);
       case 8: return setup_u<8, false>(smem_bytes);
       default:
-        if constexpr (P == PREC_FP32) return setup_u<13, false>(smem_bytes);
-        else return setup_u<8, false>(smem_bytes);
+        return setup_u<8, false>(smem_bytes);
     }
   }
 };
