@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/softlat_cuda.h"
 #include "sl_device.cuh"
@@ -71,6 +72,14 @@ struct DevBuf {
     return (T *)p;
   }
 };
+
+// NVTX ranges on the API entry points and the layout build: the host-side
+// timeline in nsys / `ncu --nvtx` (near free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SL_RANGE(name) NvtxRange sl_nvtx_range_(name)
 
 }  // namespace
 
@@ -1988,6 +1997,7 @@ int resolve_accumulation(sl_ctx *c, int acc) {
 }
 
 int build_layout(sl_ctx *c) {
+  SL_RANGE("build_layout");
   c->split = false;
   if (c->prec != PREC_FP64 && c->split_enabled) {
     bool used = false;
@@ -2253,6 +2263,7 @@ int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
                      const double *load, const double *mass,
                      const uint8_t *fixed, const uint8_t *alive,
                      const int64_t *gen) {
+  SL_RANGE("sl_upload_masses");
   if (!c) return fail(c, SL_EINVAL, "NULL context");
   if (m_n < 0 || (m_n > 0 && (!pos || !vel || !mass || !fixed || !alive ||
                               !gen)))
@@ -2427,6 +2438,7 @@ int sl_upload_springs(sl_ctx *c, int64_t s_n, const int64_t *m1,
                       const double *amp, const double *freq,
                       const double *off, const double *per,
                       const uint8_t *alive, const uint8_t *degen) {
+  SL_RANGE("sl_upload_springs");
   if (!c) return fail(c, SL_EINVAL, "NULL context");
   if (!c->masses_set)
     return fail(c, SL_ESTATE, "upload masses before springs");
@@ -2636,6 +2648,7 @@ int sl_write_springs(sl_ctx *c, int64_t n, const int64_t *slots,
                      const double *amp, const double *freq, const double *off,
                      const double *per, const uint8_t *alive,
                      const uint8_t *degen) {
+  SL_RANGE("sl_write_springs");
   if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
   if (n < 0 || (n > 0 && (!slots || !m1 || !m2 || !m1gen || !m2gen ||
                           !rest || !k || !diam || !yield || !mode || !amp ||
@@ -2711,6 +2724,7 @@ int sl_write_spring_params(sl_ctx *c, int64_t n, const int64_t *slots,
 }
 
 int sl_kill_springs(sl_ctx *c, int64_t n, const int64_t *slots) {
+  SL_RANGE("sl_kill_springs");
   if (!c || !c->springs_set) return fail(c, SL_ESTATE, "no springs");
   if (n <= 0) return SL_OK;
   for (int64_t r = 0; r < n; r++)
@@ -2979,6 +2993,7 @@ static void halo_sync(sl_ctx *c) {
 int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
             int accumulation, int64_t *counters, int64_t *err_slot,
             int64_t *steps_done) {
+  SL_RANGE("sl_step");
   if (!c) return fail(c, SL_EINVAL, "NULL context");
   if (n_steps < 0 || (n_steps > 0 && !sim_times))
     return fail(c, SL_EINVAL, "sl_step: bad arguments");
@@ -3138,6 +3153,7 @@ int sl_mass_pass(sl_ctx *c, double dt, int64_t *err_slot) {
 
 int sl_energy(sl_ctx *c, double sim_t, const double *gravity,
               double *out) {
+  SL_RANGE("sl_energy");
   if (!c || !gravity || !out) return fail(c, SL_EINVAL, "sl_energy: NULL");
   if (!c->masses_set || !c->springs_set)
     return fail(c, SL_ESTATE, "masses and springs must be uploaded first");
@@ -3170,6 +3186,7 @@ int sl_energy(sl_ctx *c, double sim_t, const double *gravity,
 
 int sl_spring_loads(sl_ctx *c, double sim_t, double *lengths,
                     double *force_magnitudes) {
+  SL_RANGE("sl_spring_loads");
   if (!c || !lengths || !force_magnitudes)
     return fail(c, SL_EINVAL, "sl_spring_loads: NULL");
   if (!c->masses_set || !c->springs_set)
@@ -3195,6 +3212,7 @@ int sl_spring_loads(sl_ctx *c, double sim_t, double *lengths,
 
 int sl_download_masses(sl_ctx *c, double *pos, double *vel, double *acc,
                        double *fext) {
+  SL_RANGE("sl_download_masses");
   if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
   const int64_t m = c->m_n;
   if (m == 0) return SL_OK;
@@ -3257,6 +3275,7 @@ int sl_download_state(sl_ctx *c, double *pos, double *vel, double *acc,
 int sl_download_state_ex(sl_ctx *c, double *pos, double *vel, double *acc,
                          double *fext, double *pos2, double *vel2,
                          int wait_head) {
+  SL_RANGE("sl_download_state_ex");
   if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
   const int64_t m = c->m_n;
   if (m == 0) return SL_OK;
@@ -3321,6 +3340,7 @@ int sl_stash_state(sl_ctx *c) {
 }
 
 int sl_checkpoint(sl_ctx *c, double *view_pos, double *view_vel) {
+  SL_RANGE("sl_checkpoint");
   if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
   if (c->async_open)
     return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
@@ -3385,6 +3405,7 @@ int sl_checkpoint_view_wait(sl_ctx *c) {
 }
 
 int sl_restore(sl_ctx *c) {
+  SL_RANGE("sl_restore");
   if (!c || c->ck_cur < 0) return fail(c, SL_ESTATE, "no checkpoint");
   if (c->async_open)
     return fail(c, SL_ESTATE, "asynchronous run open (sl_step_finish)");
@@ -3461,6 +3482,7 @@ int sl_download_springs(sl_ctx *c, uint8_t *alive, uint8_t *degen) {
 }
 
 int sl_snapshot_begin(sl_ctx *c) {
+  SL_RANGE("sl_snapshot_begin");
   if (!c || !c->masses_set) return fail(c, SL_ESTATE, "no masses");
   const int64_t m = c->m_n;
   CK(cudaSetDevice(c->device));
@@ -3576,6 +3598,7 @@ static int enqueue_steps(sl_ctx *c, const KState &S, int64_t n_steps,
 
 int sl_step_async(sl_ctx *c, int64_t n_steps, const double *sim_times,
                   double dt, int accumulation) {
+  SL_RANGE("sl_step_async");
   if (!c) return fail(c, SL_EINVAL, "NULL context");
   if (n_steps < 0 || (n_steps > 0 && !sim_times))
     return fail(c, SL_EINVAL, "sl_step_async: bad arguments");
