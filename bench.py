@@ -675,19 +675,26 @@ def bench_config_e(args, rank, world, local, dist, reduce_):
     stats = run.ctx.stats()
     # e2e through the same API with host buffers: this rank's state up,
     # K steps, its owned state down
+    # (a control segment as config B's: new positions / velocities up from
+    # page-locked host buffers, K steps, positions / velocities down into
+    # page-locked buffers; median of E2E_REPS segments)
     m_loc = len(shards[rank].local_to_global)
     c = shards[rank].case
-    w0 = time.perf_counter()
-    run.ctx.upload_masses(c["m_pos"], c["m_vel"], c["m_acc"], c["m_fext"],
-                          c["m_load"], c["m_mass"], c["m_fixed"],
-                          c["m_alive"], c["m_gen"])
-    if world > 1:
-        dist.barrier()
-    run.step(times[warm:], dt, acc)
-    pos = np.empty((m_loc, 3))
-    vel = np.empty((m_loc, 3))
-    run.ctx.download_masses(pos, vel)
-    wall = time.perf_counter() - w0
+    pin = [_native.pinned_empty((m_loc, 3), np.float64) for _ in range(4)]
+    pin[0][...] = np.asarray(c["m_pos"]).reshape(m_loc, 3)
+    pin[1][...] = np.asarray(c["m_vel"]).reshape(m_loc, 3)
+    walls = []
+    for _ in range(E2E_REPS):
+        if world > 1:
+            dist.barrier()
+        w0 = time.perf_counter()
+        run.ctx.write_state(pin[0], pin[1], None)
+        if world > 1:
+            dist.barrier()
+        run.step(times[warm:], dt, acc)
+        run.ctx.download_masses(pin[2], pin[3])
+        walls.append(time.perf_counter() - w0)
+    wall = float(np.median(walls))
     if dist is not None:
         wall = float(reduce_(wall, dist.ReduceOp.MAX, torch.float64))
     run.close()
@@ -717,9 +724,11 @@ def bench_config_e(args, rank, world, local, dist, reduce_):
                                  stats["step_path"], "?") +
                              (" + k_halo_sync" if world > 1 else "")},
                 "e2e": {"value": springs * args.steps / wall, "unit": unit,
-                        "h2d_bytes_per_step": m_loc * 138 / args.steps,
+                        "h2d_bytes_per_step": m_loc * 48 / args.steps,
                         "d2h_bytes_per_step": m_loc * 48 / args.steps,
-                        "api": "sl_upload_masses + sl_step + "
+                        "segments": E2E_REPS,
+                        "segment_walls_s": [round(w, 6) for w in walls],
+                        "api": "sl_write_state + sl_step + "
                                "sl_download_masses per rank"},
                 "gpu_launches": args.steps * (2 if world > 1 else 1),
                 "call_ms_per_step": call_ms / args.steps,
