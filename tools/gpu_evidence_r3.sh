@@ -50,3 +50,7 @@ s --tool synccheck python -m pytest tests/test_gpu_fused.py tests/test_gpu_windo
 s --tool initcheck python -m pytest tests/test_gpu_edge.py tests/test_gpu_window.py -q -x -p no:cacheprovider
 } > $out/sanitizer.txt 2>&1
 tail -3 $out/pytest.txt
+# summaries on the box (the raw reports exceed what gpurun brings back)
+mkdir -p $out/saved
+SL_EVIDENCE_DST=$out/saved SL_TRAFFIC_JSON=$out/saved/traffic.json python tools/save_evidence_r3.py > $out/saved.log 2>&1
+rm -f $out/*.ncu-rep

@@ -12,7 +12,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out", "ev_r3")
-DST = os.path.join(ROOT, "profiles", "r3")
+# (SL_EVIDENCE_DST / SL_TRAFFIC_JSON: summarise on the GPU box itself, into
+# gpurun_out/, when the raw ncu reports are too large to bring back)
+DST = os.environ.get("SL_EVIDENCE_DST") or os.path.join(ROOT, "profiles", "r3")
 os.makedirs(DST, exist_ok=True)
 
 # bench lines
@@ -88,7 +90,8 @@ for name, ab in algo.items():
     for l in open(out):
         if l.startswith("traffic (dram r+w) bytes") and name in keys:
             traffic[keys[name]] = int(float(l.split()[-1]))
-with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
+with open(os.environ.get("SL_TRAFFIC_JSON") or
+          os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
     json.dump(traffic, fh, indent=1)
 
 # SASS of the timed kernel: the TMA / mbarrier / elect instructions
