@@ -3028,6 +3028,12 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
     }
   }
   c->k_valid = false;
+  // diagnostic (SL_FIRST_STEP_MS=1): the first step's device time apart
+  static cudaEvent_t first_ev = [] {
+    cudaEvent_t e = nullptr;
+    if (getenv("SL_FIRST_STEP_MS")) cudaEventCreate(&e);
+    return e;
+  }();
   CK(cudaEventRecord(c->k0, c->st));
   for (int64_t n = 0; n < n_steps; n++) {
     StepP T;
@@ -3075,12 +3081,20 @@ int sl_step(sl_ctx *c, int64_t n_steps, const double *sim_times, double dt,
       c->launches += 2;
     }
     if (c->halo_on) halo_sync(c);
+    if (n == 0 && first_ev) CK(cudaEventRecord(first_ev, c->st));
   }
   CKL();
   CK(cudaEventRecord(c->k1, c->st));
   c->k_valid = true;
   int64_t err = 0;
   if ((rc = finish_status(c, counters, &err))) return rc;
+  if (first_ev && n_steps > 1) {  // SL_FIRST_STEP_MS: diagnostic split
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, c->k0, first_ev);
+    cudaEventElapsedTime(&b, first_ev, c->k1);
+    fprintf(stderr, "sl_step: first step %.2f us, later steps %.2f us each\n",
+            1e3 * a, 1e3 * b / (double)(n_steps - 1));
+  }
   int64_t done = n_steps;
   if (c->h_status[4]) done = (int64_t)c->h_status[4];
   c->cur = (int)((c->cur + done) & 1);
