@@ -2312,10 +2312,16 @@ int sl_upload_masses(sl_ctx *c, int64_t m_n, const double *pos,
                                            : nullptr);
     CKL();
     c->launches++;
-    if (c->has_lc) {
+    if (c->has_lc && m_n == c->m_n) {
       k_set_lc_flags<<<blocks_for(m_n), 256, 0, c->st>>>(
           m_n, c->lc_off.as<int64_t>(), c->vel.p, c->rsz == 8);
       CKL();
+    } else if (c->has_lc) {
+      // the constraint table was built for the old mass count (reading it
+      // for the new one ran past its end -- compute-sanitizer memcheck on
+      // tests/test_gpu_fuzz_edits.py): dropped until the host re-sends it
+      // (sl_set_local_constraints, which the engine does on a count change)
+      c->has_lc = false;
     }
   }
   CK(cudaStreamSynchronize(c->st));  // staging is reused by the next call

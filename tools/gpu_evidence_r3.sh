@@ -42,7 +42,7 @@ s() { echo "## $*"; timeout 1800 compute-sanitizer "$@" 2>&1 | grep -E "passed|f
 {
 s --tool memcheck --leak-check no python -m pytest tests/test_gpu_fuzz.py tests/test_gpu_edge.py tests/test_gpu_damping.py -q -x -p no:cacheprovider
 s --tool memcheck --leak-check no python -m pytest tests/test_gpu_halo.py -q -x -p no:cacheprovider -k "in_process"
-s --tool memcheck --leak-check no python -m pytest tests/test_gpu_inplace_edits.py tests/test_gpu_control.py -q -x -p no:cacheprovider
+s --tool memcheck --leak-check no python -m pytest tests/test_gpu_inplace_edits.py tests/test_gpu_fuzz_edits.py tests/test_gpu_control.py -q -x -p no:cacheprovider
 s --tool racecheck python -m pytest tests/test_gpu_inplace_edits.py -q -x -p no:cacheprovider -k fp32
 s --tool racecheck python -m pytest tests/test_gpu_fused.py -q -x -p no:cacheprovider
 s --tool racecheck python -m pytest tests/test_gpu_window.py -q -x -p no:cacheprovider -k "lattices or exact"
